@@ -1,0 +1,192 @@
+/*
+ * ubs_b200.h — C ABI of the B200-native Universal Beta Splatting render path.
+ *
+ * Drop-in boundary for the reference package `betasplat`
+ * (/root/reference/pkg/src/betasplat).  The reference has no plugin registry;
+ * its boundary is (i) the Python entry points render / render_with_cache /
+ * gradients.backward and (ii) the two numba kernels tile_forward /
+ * tile_backward, whose ABI is "caller allocates every array, kernel writes
+ * outputs in place, returns a plain int".  This header keeps that ownership
+ * model at frame granularity on the device:
+ *
+ *   - every pointer is a caller-owned DEVICE buffer (the Python host layer
+ *     allocates them as torch tensors); the library never allocates;
+ *   - every call is stream-ordered on the given cudaStream_t, performs no
+ *     host synchronisation and keeps no global mutable state (re-entrant per
+ *     stream);
+ *   - return value 0 = success, negative = UBS_E_* below.
+ *
+ * Stage map (reference function -> entry point here):
+ *   slice_scene + project_scene        slicing.py:185-235, raster.py:95-134
+ *                                      -> ubs_preprocess
+ *   order = lexsort((ids, depth))      raster.py:274-275
+ *   build_tiles                        raster.py:252-266
+ *                                      -> ubs_bin_depth + ubs_bin_tiles
+ *   tile_forward over all tiles        _tiles.py:19-56, raster.py:284-316
+ *                                      -> ubs_raster_forward (+ ubs_raster_fixup)
+ *   L1 + ssim_and_grad -> g_image      gradients.py:110-116, metrics.py:74-114
+ *                                      -> ubs_loss_image_grad
+ *   tile_backward + np.add.at scatter  _tiles.py:59-127, gradients.py:142-173
+ *                                      -> ubs_raster_backward
+ *   _projection_backward/_slice_backward/_clamp_eig_adjoint + regularisers
+ *                                      gradients.py:120-123,179-300
+ *                                      -> ubs_prim_backward
+ *
+ * Primitive layout: the UBS1 record (sceneio.py:3-11) — n rows of 14+6C
+ * floats (f32, or f64 when param_f64 = 1) in PARAM_FIELDS order
+ * (scene.py:17-28): mu_x[3] mu_q[C] rot[3] s_x_raw[3] l_qx[C*3] s_q_raw[C]
+ * b_x b_q[C] opacity_raw color[3].  Parameter gradients use the same layout.
+ */
+#ifndef UBS_B200_H
+#define UBS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
+
+#define UBS_ABI_VERSION 1
+#define UBS_TILE 16
+
+enum {
+    UBS_OK = 0,
+    UBS_E_ARGS = -1,      /* bad argument (null pointer, unsupported n_dims/tile size) */
+    UBS_E_CUDA = -2,      /* a CUDA launch or CUB call failed */
+    UBS_E_CAPACITY = -3,  /* caller-provided pair / temp capacity too small */
+};
+
+/* flag bits in UbsPrimBuffers.flags (16 bits per primitive) */
+enum {
+    UBS_F_VISIBLE = 1,      /* ProjectionCache.visible (raster.py:131) */
+    UBS_F_DEGENERATE = 2,   /* ~SliceCache.valid (covariance.py:122-149) */
+    UBS_F_FLOOR3 = 4,       /* SliceCache.floored (slicing.py:215) */
+    UBS_F_FLOOR2 = 8,       /* ProjectionCache.floored (raster.py:116) */
+    UBS_F_THIN = 16,        /* fp32 raster guard: pixels touching this splat are re-done in fp64 */
+};
+
+/* Camera (camera.py:15-51): intrinsics + rigid world_to_cam. */
+typedef struct UbsCamera {
+    double fx, fy, cx, cy;
+    double rot[9];   /* world_to_cam[:3,:3], row-major */
+    double trans[3]; /* world_to_cam[:3, 3] */
+    int32_t width, height;
+} UbsCamera;
+
+/* RenderSettings (config.py:9-38); tile_size must be 16. */
+typedef struct UbsSettings {
+    double tau_sq, alpha_clamp, transmittance_min, near_plane, cull_margin;
+    double screen_cov_floor, psd_floor_scale;
+    int32_t gate_symmetric, tile_size;
+} UbsSettings;
+
+/* One frame = scene + camera + query (slicing.py:36-77: [], [d], or [t, d]). */
+typedef struct UbsView {
+    const void *params;   /* n x (14+6C) device records */
+    int64_t n;
+    int32_t n_dims;       /* 3, 6 or 7 */
+    int32_t param_f64;    /* 0: f32 records, 1: f64 records */
+    double background[3];
+    double query[4];
+    UbsCamera cam;
+    UbsSettings set;
+} UbsView;
+
+/* Per-primitive preprocess outputs (all length n unless noted). */
+typedef struct UbsPrimBuffers {
+    uint64_t *depth_key;   /* f64 depth bits when visible, else UINT64 sentinel */
+    uint64_t *rect;        /* tile rect packed tx0 | ty0<<16 | tx1<<32 | ty1<<48 */
+    uint32_t *tile_count;  /* tiles touched (0 if not visible) */
+    uint16_t *flags;       /* UBS_F_* | (s_tanh[k] > 0) << (8 + k), k < C (FrameCache.trace_signature) */
+    void *rec32;           /* n x 48 B fp32 raster records (may be NULL in fp64 mode) */
+    void *rec64;           /* n x 80 B fp64 raster records */
+    double *debug;         /* optional n x UBS_DEBUG_STRIDE f64 dump of intermediates, or NULL */
+    uint32_t *n_visible;   /* [1] += number of visible primitives (caller zeroes) */
+    unsigned long long *n_pairs; /* [1] += total tile pairs K (caller zeroes) */
+} UbsPrimBuffers;
+
+/* debug row: 0 depth | 1-2 mean2 | 3-5 p2 00,01,11 | 6-7 radii | 8 gated opacity | 9 beta_x |
+ * 10-12 cov2 00,01,11 | 13-18 cov3 xx,xy,xz,yy,yz,zz | 19-21 t_cam | 22-24 mean3 | 25 gate |
+ * 26 opacity | 27-30 s_tanh[4] | 31 floor_eps */
+#define UBS_DEBUG_STRIDE 32
+
+/* Binning buffers. */
+typedef struct UbsBinBuffers {
+    uint64_t *keys_sorted; /* n: depth keys after sort */
+    uint32_t *ids_iota;    /* n: scratch (0..n-1) */
+    uint32_t *order;       /* n: ids by (depth, id); first n_vis are visible */
+    uint32_t *offsets;     /* n: exclusive scan of tile counts in rank order */
+    uint32_t *pair_keys;   /* capacity: tile id per pair (emit order) */
+    uint32_t *pair_vals;   /* capacity: primitive id per pair (emit order) */
+    uint32_t *pair_keys_sorted;
+    uint32_t *tile_ids;    /* capacity: primitive ids grouped by tile, depth ordered */
+    uint32_t *tile_ranges; /* 2 x n_tiles: [start, end) into tile_ids */
+    int64_t pair_capacity;
+    void *temp;            /* CUB scratch */
+    size_t temp_bytes;
+} UbsBinBuffers;
+
+/* Forward outputs.  Image/alpha/T are f32, or f64 in the fp64 raster. */
+typedef struct UbsImageBuffers {
+    void *image;        /* H x W x 3 */
+    void *alpha_sum;    /* H x W */
+    void *t_stop;       /* H x W */
+    int32_t *n_contrib; /* H x W: splats iterated before the early-out */
+    uint8_t *hit_clamp; /* n: FrameCache.alpha_clamped */
+    unsigned long long *visits; /* [1]: processed_pixels total */
+    uint32_t *fix_list;  /* H*W capacity: pixels re-done in fp64 (fp32 raster only) */
+    uint32_t *fix_count; /* [1] */
+    int32_t raster_f64;  /* 1 = fp64 raster, 0 = fp32 raster + fp64 fix-up */
+} UbsImageBuffers;
+
+/* Backward buffers. */
+typedef struct UbsGradBuffers {
+    const void *g_image; /* H x W x 3 dL/dimage (same float type as the image) */
+    void *grad2d;        /* n x 12 accumulators: g_mean2[2] g_P[00,01,11] g_og g_bx g_color[3] pad[2] */
+    void *grad_params;   /* n x (14+6C) += parameter gradients (f32, or f64 if grad_f64) */
+    int32_t grad_f64;
+    int32_t grad2d_f64;  /* grad2d accumulators are f64 (must equal UbsImageBuffers.raster_f64) */
+    double reg_opacity;  /* loss_scale * lambda_o   (0 to skip, gradients.py:120-123) */
+    double reg_scale;    /* loss_scale * lambda_sigma */
+    uint32_t *nonfinite; /* [1] set to 1 when any gradient is not finite */
+} UbsGradBuffers;
+
+/* --- entry points --- */
+int ubs_abi_version(void);
+const char *ubs_build_info(void);
+
+/* slice + project + tile rects (fp64 arithmetic, one thread per primitive) */
+int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32, ubs_stream_t s);
+
+/* CUB scratch bytes needed for n primitives, pair capacity and tile count */
+size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
+/* depth sort (stable on id) and rank-ordered exclusive scan of tile counts */
+int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb, ubs_stream_t s);
+/* emit (tile, id) pairs in rank order, stable sort on tile bits, per-tile ranges */
+int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                  int64_t n_pairs, ubs_stream_t s);
+
+/* front-to-back composite, one 16x16 tile per CTA */
+int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                       const UbsImageBuffers *ib, ubs_stream_t s);
+
+/* L1 + SSIM image gradient; loss_parts[0] += sum|diff|, loss_parts[1] += sum ssim_map */
+int ubs_loss_image_grad(const void *image, const void *target, int32_t height, int32_t width,
+                        int32_t f64, double lambda_ssim, double scale, void *g_image,
+                        double *loss_parts, void *scratch, ubs_stream_t s);
+size_t ubs_loss_scratch_bytes(int32_t height, int32_t width, int32_t f64);
+
+/* reverse replay of the blend -> per-primitive 2D gradients (grad2d, +=) */
+int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                        const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t s);
+
+/* chain 2D gradients back to raw parameters (fp64), += into grad_params */
+int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int32_t add_regularisers, ubs_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UBS_B200_H */

@@ -1,0 +1,240 @@
+// Loss image gradient: L1 + (1 - SSIM) and its exact adjoint.
+//
+// Reference: gradients.py:110-116 (g_image = scale * ((1-l) sign(diff)/size
+// - l * g_ssim)), metrics.py:35-114 (separable 11-tap sigma 1.5 Gaussian
+// window with reflect padding folded into a banded operator; the adjoint is
+// the transposed operator).
+//
+// Four separable passes: horizontal blur of (a, b, a^2, b^2, ab), vertical
+// blur + pointwise SSIM map and its pointwise adjoint, vertical adjoint,
+// horizontal adjoint + combine.  The adjoint of the reflect-folded blur is a
+// gather: output j collects from every (row, tap) whose reflected source is j.
+#include <cuda_runtime.h>
+
+#include "ubs_common.cuh"
+
+namespace ubs {
+
+struct BlurTaps {
+    double k[11];
+};
+
+__device__ __forceinline__ int reflect_idx(int i, int n) {
+    // metrics.py:43-46: period 2n-2, no edge duplication
+    const int period = n > 1 ? 2 * n - 2 : 1;
+    i = abs(i) % period;
+    return i >= n ? period - i : i;
+}
+
+// forward blur along an axis of length n with element stride `stride`
+template <typename T, typename F>
+__device__ __forceinline__ T blur_fwd(const BlurTaps &w, int j, int n, F get) {
+    T s = 0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) s += (T)w.k[t] * get(reflect_idx(j - 5 + t, n));
+    return s;
+}
+
+// adjoint blur: sum over (r, t) with reflect(r - 5 + t) == j of k[t] g[r]
+template <typename T, typename F>
+__device__ __forceinline__ T blur_adj(const BlurTaps &w, int j, int n, F get) {
+    T s = 0;
+    if (n < 12) {
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int t = 0; t < 11; ++t)
+                if (reflect_idx(r - 5 + t, n) == j) s += (T)w.k[t] * get(r);
+        return s;
+    }
+    // n >= 12: a source position p in [-5, n+4] reflects onto j iff p == j,
+    // p == -j (1 <= j <= 5) or p == 2n-2-j (n-6 <= j <= n-2)
+    int ps[3];
+    int np = 0;
+    ps[np++] = j;
+    if (j >= 1 && j <= 5) ps[np++] = -j;
+    if (j >= n - 6 && j <= n - 2) ps[np++] = 2 * n - 2 - j;
+    for (int c = 0; c < np; ++c) {
+        const int p = ps[c];
+#pragma unroll
+        for (int t = 0; t < 11; ++t) {
+            const int r = p + 5 - t;
+            if (r >= 0 && r < n) s += (T)w.k[t] * get(r);
+        }
+    }
+    return s;
+}
+
+template <typename T>
+__global__ void ssim_hblur_kernel(const T *__restrict__ a, const T *__restrict__ b, int H, int W, BlurTaps w,
+                                  T *__restrict__ h5) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = (int64_t)H * W * 3;
+    if (idx >= N) return;
+    const int c = (int)(idx % 3);
+    const int64_t yx = idx / 3;
+    const int x = (int)(yx % W);
+    const int64_t row = (yx / W) * W;
+    T s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+        const int64_t q = (row + reflect_idx(x - 5 + t, W)) * 3 + c;
+        const T av = a[q], bv = b[q], k = (T)w.k[t];
+        s0 += k * av;
+        s1 += k * bv;
+        s2 += k * (av * av);
+        s3 += k * (bv * bv);
+        s4 += k * (av * bv);
+    }
+    h5[idx] = s0;
+    h5[N + idx] = s1;
+    h5[2 * N + idx] = s2;
+    h5[3 * N + idx] = s3;
+    h5[4 * N + idx] = s4;
+}
+
+template <typename T>
+__global__ void ssim_vblur_map_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *__restrict__ h5,
+                                      int H, int W, BlurTaps w, T *__restrict__ g3, double *__restrict__ sums) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = (int64_t)H * W * 3;
+    double l1 = 0.0, sm = 0.0;
+    if (idx < N) {
+        const int64_t rc = idx % ((int64_t)W * 3);  // x*3 + c
+        const int y = (int)(idx / ((int64_t)W * 3));
+        const int64_t rs = (int64_t)W * 3;
+        T m[5];
+#pragma unroll
+        for (int qd = 0; qd < 5; ++qd) {
+            const T *src = h5 + qd * N + rc;
+            m[qd] = blur_fwd<T>(w, y, H, [&](int r) { return src[(int64_t)r * rs]; });
+        }
+        const T C1 = (T)(0.01 * 0.01), C2 = (T)(0.03 * 0.03);
+        const T mu_a = m[0], mu_b = m[1];
+        const T va = m[2] - mu_a * mu_a, vb = m[3] - mu_b * mu_b, cab = m[4] - mu_a * mu_b;
+        const T n1 = (T)2 * mu_a * mu_b + C1, n2 = (T)2 * cab + C2;
+        const T d1 = mu_a * mu_a + mu_b * mu_b + C1, d2 = va + vb + C2;
+        const T den = d1 * d2;
+        const T s = n1 * n2 / den;
+        const T g = (T)(1.0 / (double)N);
+        const T g_n1 = g * n2 / den, g_n2 = g * n1 / den;
+        const T g_den = -g * s / den;
+        const T g_d1 = g_den * d2, g_d2 = g_den * d1;
+        const T g_cab = (T)2 * g_n2;
+        const T g_mu_a = (T)2 * mu_b * g_n1 + (T)2 * mu_a * g_d1 - (T)2 * mu_a * g_d2 - mu_b * g_cab;
+        g3[idx] = g_mu_a;
+        g3[N + idx] = g_d2;   // g_E[a^2]
+        g3[2 * N + idx] = g_cab;  // g_E[ab]
+        sm = (double)s;
+        l1 = fabs((double)a[idx] - (double)b[idx]);
+    }
+    // block reduction of (sum |diff|, sum ssim)
+    for (int o = 16; o > 0; o >>= 1) {
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    __shared__ double red[2][32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { red[0][wid] = l1; red[1][wid] = sm; }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        l1 = lane < nw ? red[0][lane] : 0.0;
+        sm = lane < nw ? red[1][lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        }
+        if (lane == 0) {
+            atomicAdd(sums, l1);
+            atomicAdd(sums + 1, sm);
+        }
+    }
+}
+
+template <typename T>
+__global__ void ssim_vadj_kernel(const T *__restrict__ g3, int H, int W, BlurTaps w, T *__restrict__ v3) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = (int64_t)H * W * 3;
+    if (idx >= N) return;
+    const int64_t rc = idx % ((int64_t)W * 3);
+    const int y = (int)(idx / ((int64_t)W * 3));
+    const int64_t rs = (int64_t)W * 3;
+#pragma unroll
+    for (int qd = 0; qd < 3; ++qd) {
+        const T *src = g3 + qd * N + rc;
+        v3[qd * N + idx] = blur_adj<T>(w, y, H, [&](int r) { return src[(int64_t)r * rs]; });
+    }
+}
+
+template <typename T>
+__global__ void ssim_hadj_combine_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *__restrict__ v3,
+                                         int H, int W, BlurTaps w, double lambda_ssim, double scale,
+                                         T *__restrict__ g_image) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = (int64_t)H * W * 3;
+    if (idx >= N) return;
+    const int c = (int)(idx % 3);
+    const int64_t yx = idx / 3;
+    const int x = (int)(yx % W);
+    const int64_t row = (yx / W) * W;
+    T adj[3];
+#pragma unroll
+    for (int qd = 0; qd < 3; ++qd) {
+        const T *src = v3 + qd * N;
+        adj[qd] = blur_adj<T>(w, x, W, [&](int r) { return src[(row + r) * 3 + c]; });
+    }
+    const T av = a[idx], bv = b[idx];
+    const T gs = adj[0] + adj[1] * (T)2 * av + adj[2] * bv;
+    const T diff = av - bv;
+    const T sgn = diff > (T)0 ? (T)1 : (diff < (T)0 ? (T)-1 : (T)0);
+    g_image[idx] = (T)scale * ((T)(1.0 - lambda_ssim) * sgn / (T)N - (T)lambda_ssim * gs);
+}
+
+static BlurTaps make_taps() {
+    BlurTaps w;
+    double s = 0.0;
+    for (int t = 0; t < 11; ++t) {
+        const double u = (t - 5) / 1.5;
+        w.k[t] = exp(-0.5 * u * u);
+        s += w.k[t];
+    }
+    for (int t = 0; t < 11; ++t) w.k[t] /= s;
+    return w;
+}
+
+template <typename T>
+static void run_loss(const T *a, const T *b, int H, int W, double lam, double scale, T *g, double *sums, T *scr,
+                     cudaStream_t s) {
+    const int64_t N = (int64_t)H * W * 3;
+    const BlurTaps w = make_taps();
+    const int thr = 256;
+    const unsigned blocks = (unsigned)((N + thr - 1) / thr);
+    T *h5 = scr, *g3 = scr + 5 * N, *v3 = scr + 8 * N;
+    ssim_hblur_kernel<T><<<blocks, thr, 0, s>>>(a, b, H, W, w, h5);
+    ssim_vblur_map_kernel<T><<<blocks, thr, 0, s>>>(a, b, h5, H, W, w, g3, sums);
+    ssim_vadj_kernel<T><<<blocks, thr, 0, s>>>(g3, H, W, w, v3);
+    ssim_hadj_combine_kernel<T><<<blocks, thr, 0, s>>>(a, b, v3, H, W, w, lam, scale, g);
+}
+
+}  // namespace ubs
+
+using namespace ubs;
+
+extern "C" size_t ubs_loss_scratch_bytes(int32_t height, int32_t width, int32_t f64) {
+    return (size_t)11 * height * width * 3 * (f64 ? 8 : 4);
+}
+
+extern "C" int ubs_loss_image_grad(const void *image, const void *target, int32_t height, int32_t width,
+                                   int32_t f64, double lambda_ssim, double scale, void *g_image,
+                                   double *loss_parts, void *scratch, ubs_stream_t stream) {
+    if (!image || !target || !g_image || !loss_parts || !scratch || height < 1 || width < 1) return UBS_E_ARGS;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (f64)
+        run_loss<double>((const double *)image, (const double *)target, height, width, lambda_ssim, scale,
+                         (double *)g_image, loss_parts, (double *)scratch, s);
+    else
+        run_loss<float>((const float *)image, (const float *)target, height, width, lambda_ssim, scale,
+                        (float *)g_image, loss_parts, (float *)scratch, s);
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}

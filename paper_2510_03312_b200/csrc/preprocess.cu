@@ -1,0 +1,180 @@
+// K1 preprocess: conditioning + projection + tile rect, one thread per primitive.
+//
+// Reference: slicing.py:185-235 (slice_scene), raster.py:95-134 (project_scene),
+// raster.py:252-266 (build_tiles' inclusive AABB test, restated as an exact
+// rect formula: SURVEY.md Appendix A).
+//
+// HBM: reads 4P B of parameters, writes 8 (depth key) + 8 (rect) + 4 (count)
+// + 2 (flags) + 64/80 B (raster record) per primitive.  Arithmetic is fp64.
+// Parameters are staged into shared memory with coalesced loads (the UBS1
+// record is AoS with a 56..152 B stride; one thread per record would issue
+// 32 scattered 4 B loads per warp instruction).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "ubs_common.cuh"
+
+namespace ubs {
+
+constexpr int kPreThreads = 128;
+
+template <int C, typename PT>
+__global__ void __launch_bounds__(kPreThreads)
+preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
+    constexpr int P = 14 + 6 * C;
+    __shared__ PT stage[kPreThreads * P];
+    __shared__ uint32_t block_vis;
+    __shared__ unsigned long long block_pairs;
+    const int64_t base = (int64_t)blockIdx.x * kPreThreads;
+    const int64_t n = v.n;
+    const int nloc = (int)min((int64_t)kPreThreads, n - base);
+    const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
+    if (threadIdx.x == 0) { block_vis = 0; block_pairs = 0; }
+    for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
+    __syncthreads();
+    const int t = threadIdx.x;
+    bool vis = false;
+    uint32_t my_count = 0;
+    if (t < nloc) {
+        const int64_t i = base + t;
+        PrimGeom<C> g;
+        double mu_x[3];
+        prim_geom<C, PT>(stage + t * P, v, g, mu_x);
+
+        const int W = v.cam.width, H = v.cam.height;
+        const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
+        uint32_t count = 0;
+        uint64_t rect = 0;
+        vis = g.visible;
+        if (vis) {
+            // inclusive tile test of raster.py:261-264 as a closed form:
+            // tile tx is hit iff hi >= 16 tx and lo <= min(16 (tx+1), W)
+            const double lox = g.mean2[0] - g.radii[0], hix = g.mean2[0] + g.radii[0];
+            const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
+            if (hix >= 0.0 && lox <= (double)W && hiy >= 0.0 && loy <= (double)H) {
+                double tx0 = fmax(0.0, ceil(lox / kTile) - 1.0), tx1 = fmin((double)(TX - 1), floor(hix / kTile));
+                double ty0 = fmax(0.0, ceil(loy / kTile) - 1.0), ty1 = fmin((double)(TY - 1), floor(hiy / kTile));
+                if (tx1 >= tx0 && ty1 >= ty0) {
+                    uint64_t a = (uint64_t)tx0, b = (uint64_t)ty0, c = (uint64_t)tx1, d = (uint64_t)ty1;
+                    rect = a | (b << 16) | (c << 32) | (d << 48);
+                    count = (uint32_t)((c - a + 1) * (d - b + 1));
+                }
+            }
+        }
+        pb.depth_key[i] = vis ? (uint64_t)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
+        pb.rect[i] = rect;
+        pb.tile_count[i] = count;
+        my_count = count;
+        uint16_t fl = (vis ? UBS_F_VISIBLE : 0) | (g.valid ? 0 : UBS_F_DEGENERATE) |
+                      (g.floored3 ? UBS_F_FLOOR3 : 0) | (g.floored2 ? UBS_F_FLOOR2 : 0);
+        if constexpr (C > 0) {
+#pragma unroll
+            for (int k = 0; k < C; ++k) fl |= (g.s_tanh[k] > 0.0 ? 1 : 0) << (8 + k);
+        }
+
+        // raster records (only read for visible primitives)
+        if (pb.rec64) {
+            Rec64 r;
+            r.mx = g.mean2[0]; r.my = g.mean2[1];
+            r.p00 = g.p2[0]; r.p01 = g.p2[1]; r.p11 = g.p2[2];
+            r.og = g.og; r.bx = g.beta_x;
+            r.cr = g.color[0]; r.cg = g.color[1]; r.cb = g.color[2];
+            reinterpret_cast<Rec64 *>(pb.rec64)[i] = r;
+        }
+        if (want_rec32 && pb.rec32) {
+            // P = U^T U with U upper triangular (Cholesky of P, transposed)
+            const double u00 = sqrt(g.p2[0]);
+            const double u01 = g.p2[1] / u00;
+            const double u11 = sqrt(fmax(g.p2[2] - u01 * u01, 0.0));
+            const double fxm = floor(g.mean2[0]), fym = floor(g.mean2[1]);
+            const bool in_range = fabs(g.mean2[0]) < 4.0e6 && fabs(g.mean2[1]) < 4.0e6 && isfinite(u11);
+            const double eps32 = 5.9604644775390625e-08;  // 2^-24
+            const double st = sqrt(v.set.tau_sq);
+            double E = 8.0 * eps32 * (st * (fabs(u00) * (g.radii[0] + 1.0) +
+                                            (fabs(u01) + fabs(u11)) * (g.radii[1] + 1.0)) + v.set.tau_sq);
+            double eb = in_range ? g.beta_x * E : INFINITY;
+            if (!isfinite(eb)) fl |= UBS_F_THIN;
+            Rec32 r;
+            r.r0 = make_float4(__int_as_float(in_range ? (int)fxm : 0), __int_as_float(in_range ? (int)fym : 0),
+                               (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
+            r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)g.og);
+            r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
+            r.r3 = make_float4((float)eb, (float)E, 0.f, 0.f);
+            reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
+        }
+        pb.flags[i] = fl;
+
+        if (pb.debug) {
+            double *d = pb.debug + i * UBS_DEBUG_STRIDE;
+            d[0] = g.tcam[2];
+            d[1] = g.mean2[0]; d[2] = g.mean2[1];
+            d[3] = g.p2[0]; d[4] = g.p2[1]; d[5] = g.p2[2];
+            d[6] = g.radii[0]; d[7] = g.radii[1];
+            d[8] = g.og; d[9] = g.beta_x;
+            d[10] = g.cov2[0]; d[11] = g.cov2[1]; d[12] = g.cov2[2];
+            d[13] = g.cov3[0][0]; d[14] = g.cov3[0][1]; d[15] = g.cov3[0][2];
+            d[16] = g.cov3[1][1]; d[17] = g.cov3[1][2]; d[18] = g.cov3[2][2];
+            d[19] = g.tcam[0]; d[20] = g.tcam[1]; d[21] = g.tcam[2];
+            d[22] = g.mean3[0]; d[23] = g.mean3[1]; d[24] = g.mean3[2];
+            d[25] = g.gate; d[26] = g.opacity;
+            for (int k = 0; k < 4; ++k) d[27 + k] = 0.0;
+            if constexpr (C > 0) {
+                for (int k = 0; k < C; ++k) d[27 + k] = g.s_tanh[k];
+            }
+            d[31] = g.floor_eps;
+        }
+    }
+    // block-aggregated visible count and pair total
+    unsigned ballot = __ballot_sync(0xffffffffu, vis);
+    unsigned long long wsum = my_count;
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (ballot) atomicAdd(&block_vis, (uint32_t)__popc(ballot));
+        if (wsum) atomicAdd(&block_pairs, wsum);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (block_vis) atomicAdd(pb.n_visible, block_vis);
+        if (block_pairs) atomicAdd(pb.n_pairs, block_pairs);
+    }
+}
+
+template <int C, typename PT>
+static void launch_pre(const UbsView &v, const UbsPrimBuffers &pb, int want32, cudaStream_t s) {
+    const int64_t blocks = (v.n + kPreThreads - 1) / kPreThreads;
+    preprocess_kernel<C, PT><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, pb, want32);
+}
+
+}  // namespace ubs
+
+using namespace ubs;
+
+extern "C" int ubs_abi_version(void) { return UBS_ABI_VERSION; }
+
+extern "C" const char *ubs_build_info(void) {
+    return "ubs_b200 sm_100a; fp64 preprocess; CUB radix binning; tile-per-CTA raster fp32/fp64";
+}
+
+extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32,
+                              ubs_stream_t stream) {
+    if (!v || !pb || !pb->n_visible || !pb->n_pairs) return UBS_E_ARGS;
+    if (v->set.tile_size != kTile) return UBS_E_ARGS;
+    if (v->n < 0 || (v->n > 0 && !v->params)) return UBS_E_ARGS;
+    if (!pb->depth_key || !pb->rect || !pb->tile_count || !pb->flags) return UBS_E_ARGS;
+    if (!pb->rec64 && !(want_rec32 && pb->rec32)) return UBS_E_ARGS;
+    if (v->n == 0) return UBS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool f64 = v->param_f64 != 0;
+    switch (v->n_dims) {
+        case 3: f64 ? launch_pre<0, double>(*v, *pb, want_rec32, s)
+                    : launch_pre<0, float>(*v, *pb, want_rec32, s); break;
+        case 6: f64 ? launch_pre<3, double>(*v, *pb, want_rec32, s)
+                    : launch_pre<3, float>(*v, *pb, want_rec32, s); break;
+        case 7: f64 ? launch_pre<4, double>(*v, *pb, want_rec32, s)
+                    : launch_pre<4, float>(*v, *pb, want_rec32, s); break;
+        default: return UBS_E_ARGS;
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}

@@ -1,0 +1,521 @@
+// Tile rasterizer: forward composite, fp64 fix-up, backward replay.
+//
+// Reference: _tiles.py:19-56 (tile_forward), _tiles.py:59-127 (tile_backward),
+// raster.py:284-316 (per-tile driver and assembly), gradients.py:142-173
+// (per-tile partials scattered with np.add.at).
+//
+// Layout: one 16x16 tile per CTA, one pixel per thread (256 threads).  The
+// tile's depth-ordered id list is walked in batches of 256: each thread
+// gathers one splat record into shared memory (vector loads), then every
+// thread walks the batch from shared memory.  A CTA stops staging once
+// __syncthreads_count says all 256 pixels crossed the transmittance cut.
+//
+// Two forward precisions:
+//  * fp64: the reference's arithmetic, same operation order, no FMA
+//    contraction (mul/add helpers) -> images to ~1e-15, counts exact.
+//  * fp32: each pixel also accumulates a first-order bound on the relative
+//    error of its transmittance (from the per-splat bound E on |m32 - m64|
+//    and the float rounding of alpha).  Pixels whose cut decision
+//    (T < t_min), alpha-clamp decision or image error are not certain under
+//    that bound are appended to a fix-up list and recomputed in fp64 by
+//    raster_fixup_kernel (one warp per pixel, sequential blend => the
+//    reference's rounding), so contributor counts and alpha_clamped flags
+//    stay bit-exact while 99+% of pixels take the fp32 path.
+#include <cuda_runtime.h>
+
+#include "ubs_common.cuh"
+
+namespace ubs {
+
+struct RasterParams {
+    int W, H, TX;
+    double tau, clamp, tmin;
+    double bg[3];
+};
+
+static RasterParams make_params(const UbsView &v) {
+    RasterParams p;
+    p.W = v.cam.width;
+    p.H = v.cam.height;
+    p.TX = (p.W + kTile - 1) / kTile;
+    p.tau = v.set.tau_sq;
+    p.clamp = v.set.alpha_clamp;
+    p.tmin = v.set.transmittance_min;
+    for (int k = 0; k < 3; ++k) p.bg[k] = v.background[k];
+    return p;
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long x, unsigned long long *red) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kTileThreads / 32; ++w) t += red[w];
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// forward, fp64 (bit-faithful to tile_forward)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTileThreads)
+raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                    const Rec64 *__restrict__ recs, double *__restrict__ image, double *__restrict__ asum,
+                    double *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
+                    unsigned long long *__restrict__ visits) {
+    __shared__ Rec64 srec[kTileThreads];
+    __shared__ uint32_t sid[kTileThreads];
+    __shared__ unsigned long long red[kTileThreads / 32];
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
+    const int py = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = px < P.W && py < P.H;
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+    const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
+    double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
+    int cnt = 0;
+    bool done = !inside;
+    for (uint32_t b = start; b < end; b += kTileThreads) {
+        if (__syncthreads_count(done) == kTileThreads) break;
+        const uint32_t q = b + threadIdx.x;
+        if (q < end) {
+            const uint32_t id = ids[q];
+            sid[threadIdx.x] = id;
+            srec[threadIdx.x] = recs[id];
+        }
+        __syncthreads();
+        const int nb = (int)min((uint32_t)kTileThreads, end - b);
+        if (!done) {
+            for (int j = 0; j < nb; ++j) {
+                if (T < tmin) { done = true; break; }
+                ++cnt;
+                const Rec64 &r = srec[j];
+                const double dx = sub(pxc, r.mx), dy = sub(pyc, r.my);
+                const double m = add(add(mul(mul(r.p00, dx), dx), mul(mul(mul(2.0, r.p01), dx), dy)),
+                                     mul(mul(r.p11, dy), dy));
+                if (m >= tau) continue;
+                double a = mul(r.og, exp(mul(r.bx, log1p(-m / tau))));
+                if (a > clamp) {
+                    a = clamp;
+                    hit[sid[j]] = 1;
+                }
+                const double w = mul(a, T);
+                a0 = add(a0, mul(w, r.cr));
+                a1 = add(a1, mul(w, r.cg));
+                a2 = add(a2, mul(w, r.cb));
+                ws = add(ws, w);
+                T = mul(T, sub(1.0, a));
+            }
+            done = done || (T < tmin);
+        }
+    }
+    if (inside) {
+        const int64_t pix = (int64_t)py * P.W + px;
+        image[3 * pix] = add(a0, mul(T, P.bg[0]));
+        image[3 * pix + 1] = add(a1, mul(T, P.bg[1]));
+        image[3 * pix + 2] = add(a2, mul(T, P.bg[2]));
+        asum[pix] = ws;
+        tstop[pix] = T;
+        ncontrib[pix] = cnt;
+    }
+    __syncthreads();
+    const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
+    if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
+}
+
+// ---------------------------------------------------------------------------
+// forward, fp32 with certified fall-back to fp64
+// ---------------------------------------------------------------------------
+// Linear worst-case bound on the relative transmittance error above which a
+// pixel is re-done in fp64 regardless of its decisions.  The bound adds every
+// per-visit error with the same sign, so it overestimates the real fp32 error
+// (~1e-5, measured against the oracle in tests/) by 10-100x; this threshold
+// only catches pathological splats (needle conics, huge beta at the support
+// edge), the image tolerance itself is asserted by the parity tests.
+constexpr float kImgErrTol = 1.0e-3f;
+
+__global__ void __launch_bounds__(kTileThreads)
+raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                    const Rec32 *__restrict__ recs, float *__restrict__ image, float *__restrict__ asum,
+                    float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
+                    unsigned long long *__restrict__ visits, uint32_t *__restrict__ fix_list,
+                    uint32_t *__restrict__ fix_count) {
+    __shared__ float4 s0[kTileThreads], s1[kTileThreads], s2[kTileThreads], s3[kTileThreads];
+    __shared__ uint32_t sid[kTileThreads];
+    __shared__ unsigned long long red[kTileThreads / 32];
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
+    const int py = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = px < P.W && py < P.H;
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
+    const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    const float tmin = (float)P.tmin;
+    float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
+    float err = 0.f;  // bound on |T32 - T64| / T
+    int cnt = 0;
+    bool flag = false;
+    bool done = !inside;
+    for (uint32_t b = start; b < end; b += kTileThreads) {
+        if (__syncthreads_count(done) == kTileThreads) break;
+        const uint32_t q = b + threadIdx.x;
+        if (q < end) {
+            const uint32_t id = ids[q];
+            const float4 *r = reinterpret_cast<const float4 *>(recs + id);
+            sid[threadIdx.x] = id;
+            s0[threadIdx.x] = __ldg(r);
+            s1[threadIdx.x] = __ldg(r + 1);
+            s2[threadIdx.x] = __ldg(r + 2);
+            s3[threadIdx.x] = __ldg(r + 3);
+        }
+        __syncthreads();
+        const int nb = (int)min((uint32_t)kTileThreads, end - b);
+        if (!done) {
+            for (int j = 0; j < nb; ++j) {
+                const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
+                if (T < tmin) {
+                    if (T > tmin * (1.0f - band)) flag = true;
+                    done = true;
+                    break;
+                }
+                if (T < tmin * (1.0f + band)) flag = true;
+                ++cnt;
+                const float4 r0 = s0[j], r1 = s1[j];
+                const float dx = (float)(px - __float_as_int(r0.x)) + r0.z;
+                const float dy = (float)(py - __float_as_int(r0.y)) + r0.w;
+                const float y0 = fmaf(r1.x, dx, r1.y * dy);
+                const float y1 = r1.z * dy;
+                const float m = fmaf(y0, y0, y1 * y1);
+                if (m >= tau) {
+                    if (m < tau + s3[j].y) flag = true;  // support edge not certain
+                    continue;
+                }
+                const float4 r2 = s2[j];
+                const float lg = r2.x * log1pf(-m * inv_tau);
+                float a = r1.w * __expf(lg);
+                const float qrel = __fdividef(s3[j].x, tau - m) + 2.5e-7f * (2.0f - lg);
+                float om;
+                if (a > clamp) {
+                    if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
+                    else flag = true;
+                    a = clamp;
+                    om = one_minus_clamp;
+                } else {
+                    if (a * (1.0f + qrel) > clamp) flag = true;
+                    om = 1.0f - a;
+                }
+                err += __fdividef(a * qrel, om) + 6.0e-8f;
+                const float w = a * T;
+                a0 = fmaf(w, r2.y, a0);
+                a1 = fmaf(w, r2.z, a1);
+                a2 = fmaf(w, r2.w, a2);
+                ws += w;
+                T *= om;
+            }
+            if (!done && T < tmin) {
+                // crossed on the batch's last splat: the next check would stop
+                const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
+                if (T > tmin * (1.0f - band)) flag = true;
+                done = true;
+            }
+        }
+    }
+    if (inside && !done && T < tmin * (1.0f + fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f))) flag = true;
+    if (err > kImgErrTol) flag = flag || inside;
+    if (inside) {
+        const int64_t pix = (int64_t)py * P.W + px;
+        image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
+        image[3 * pix + 1] = fmaf(T, (float)P.bg[1], a1);
+        image[3 * pix + 2] = fmaf(T, (float)P.bg[2], a2);
+        asum[pix] = ws;
+        tstop[pix] = T;
+        ncontrib[pix] = cnt;
+    }
+    flag = flag && inside;
+    const unsigned fb = __ballot_sync(0xffffffffu, flag);
+    if (fb) {
+        uint32_t base = 0;
+        const int lane = threadIdx.x & 31;
+        if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (flag) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
+    }
+    __syncthreads();
+    const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
+    if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
+}
+
+// fp64 replay of flagged pixels: one warp per pixel.  Lanes evaluate 32
+// splats' alphas in parallel (reference formula and rounding), then the warp
+// blends them sequentially in list order so T matches tile_forward bit for bit.
+__global__ void __launch_bounds__(256)
+raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                    const Rec64 *__restrict__ recs, const uint32_t *__restrict__ fix_list,
+                    const uint32_t *__restrict__ fix_count, float *__restrict__ image, float *__restrict__ asum,
+                    float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
+                    unsigned long long *__restrict__ visits) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nfix = *fix_count;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix; w += warps) {
+        const uint32_t pix = fix_list[w];
+        const int py = pix / P.W, px = pix - py * P.W;
+        const int tile = (py / kTile) * P.TX + px / kTile;
+        const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+        const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+        double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
+        int cnt = 0;
+        bool done = false;
+        for (uint32_t b = start; b < end && !done; b += 32) {
+            const uint32_t q = b + lane;
+            double a = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
+            uint32_t id = 0;
+            if (q < end) {
+                id = ids[q];
+                const Rec64 r = recs[id];
+                const double dx = sub(pxc, r.mx), dy = sub(pyc, r.my);
+                const double m = add(add(mul(mul(r.p00, dx), dx), mul(mul(mul(2.0, r.p01), dx), dy)),
+                                     mul(mul(r.p11, dy), dy));
+                if (m < tau) a = mul(r.og, exp(mul(r.bx, log1p(-m / tau))));
+                cr = r.cr; cg = r.cg; cb = r.cb;
+            }
+            const int nb = (int)min(32u, end - b);
+            for (int k = 0; k < nb; ++k) {
+                if (T < tmin) { done = true; break; }
+                ++cnt;
+                double ak = __shfl_sync(0xffffffffu, a, k);
+                const double ck0 = __shfl_sync(0xffffffffu, cr, k);
+                const double ck1 = __shfl_sync(0xffffffffu, cg, k);
+                const double ck2 = __shfl_sync(0xffffffffu, cb, k);
+                if (ak == 0.0) continue;  // m >= tau (or underflow): no-op in tile_forward
+                if (ak > clamp) {
+                    ak = clamp;
+                    if (lane == k) hit[id] = 1;
+                }
+                const double wgt = mul(ak, T);
+                a0 = add(a0, mul(wgt, ck0));
+                a1 = add(a1, mul(wgt, ck1));
+                a2 = add(a2, mul(wgt, ck2));
+                ws = add(ws, wgt);
+                T = mul(T, sub(1.0, ak));
+            }
+        }
+        if (lane == 0) {
+            image[3 * (int64_t)pix] = (float)add(a0, mul(T, P.bg[0]));
+            image[3 * (int64_t)pix + 1] = (float)add(a1, mul(T, P.bg[1]));
+            image[3 * (int64_t)pix + 2] = (float)add(a2, mul(T, P.bg[2]));
+            asum[pix] = (float)ws;
+            tstop[pix] = (float)T;
+            const int old = ncontrib[pix];
+            ncontrib[pix] = cnt;
+            if (old != cnt) atomicAdd(visits, (unsigned long long)(long long)(cnt - old));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward: reverse replay of the blend (tile_backward), warp-reduced atomics
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+template <typename Real>
+struct BwdTraits;
+template <>
+struct BwdTraits<double> {
+    using Rec = Rec64;
+};
+template <>
+struct BwdTraits<float> {
+    using Rec = Rec32;
+};
+
+// alpha (clamped), 1 - alpha, and the operands of its derivative at a pixel
+template <typename Real>
+struct SplatEval {
+    Real dx, dy, m, a, om, og, bx, c0, c1, c2, pd0, pd1;
+};
+
+__device__ __forceinline__ void eval_splat(const Rec64 &r, int px, int py, double tau, double clamp,
+                                           double one_minus_clamp, SplatEval<double> &e) {
+    e.dx = sub((double)px + 0.5, r.mx);
+    e.dy = sub((double)py + 0.5, r.my);
+    e.m = add(add(mul(mul(r.p00, e.dx), e.dx), mul(mul(mul(2.0, r.p01), e.dx), e.dy)), mul(mul(r.p11, e.dy), e.dy));
+    e.og = r.og; e.bx = r.bx; e.c0 = r.cr; e.c1 = r.cg; e.c2 = r.cb;
+    e.pd0 = r.p00 * e.dx + r.p01 * e.dy;
+    e.pd1 = r.p01 * e.dx + r.p11 * e.dy;
+    e.a = (e.m < tau) ? mul(e.og, exp(mul(e.bx, log1p(-e.m / tau)))) : 0.0;
+    if (e.a > clamp) e.a = clamp;
+    e.om = sub(1.0, e.a);
+}
+
+__device__ __forceinline__ void eval_splat(const Rec32 &r, int px, int py, float tau, float clamp,
+                                           float one_minus_clamp, SplatEval<float> &e) {
+    e.dx = (float)(px - __float_as_int(r.r0.x)) + r.r0.z;
+    e.dy = (float)(py - __float_as_int(r.r0.y)) + r.r0.w;
+    const float y0 = fmaf(r.r1.x, e.dx, r.r1.y * e.dy), y1 = r.r1.z * e.dy;
+    e.m = fmaf(y0, y0, y1 * y1);
+    e.og = r.r1.w; e.bx = r.r2.x; e.c0 = r.r2.y; e.c1 = r.r2.z; e.c2 = r.r2.w;
+    e.pd0 = r.r1.x * y0;  // P d = U^T (U d)
+    e.pd1 = fmaf(r.r1.y, y0, r.r1.z * y1);
+    e.a = (e.m < tau) ? e.og * __expf(e.bx * log1pf(-e.m / tau)) : 0.f;
+    if (e.a > clamp) {
+        e.a = clamp;
+        e.om = one_minus_clamp;  // same factor the forward multiplied T by
+    } else {
+        e.om = 1.0f - e.a;
+    }
+}
+
+__device__ __forceinline__ double log1p_(double x) { return log1p(x); }
+__device__ __forceinline__ float log1p_(float x) { return log1pf(x); }
+
+template <typename Real>
+__global__ void __launch_bounds__(kTileThreads)
+raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                  const typename BwdTraits<Real>::Rec *__restrict__ recs, const Real *__restrict__ tstop,
+                  const int32_t *__restrict__ ncontrib, const Real *__restrict__ g_image, Real *__restrict__ grad2d) {
+    using Rec = typename BwdTraits<Real>::Rec;
+    __shared__ Rec srec[kTileThreads];
+    __shared__ uint32_t sid[kTileThreads];
+    __shared__ int smax;
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
+    const int py = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = px < P.W && py < P.H;
+    const uint32_t start = ranges[2 * tile];
+    const int64_t pix = (int64_t)py * P.W + px;
+    int my_cnt = 0;
+    Real T = 0, g0 = 0, g1 = 0, g2 = 0;
+    if (threadIdx.x == 0) smax = 0;
+    __syncthreads();
+    if (inside) {
+        my_cnt = ncontrib[pix];
+        T = tstop[pix];
+        g0 = g_image[3 * pix];
+        g1 = g_image[3 * pix + 1];
+        g2 = g_image[3 * pix + 2];
+        atomicMax(&smax, my_cnt);
+    }
+    __syncthreads();
+    const int max_cnt = smax;
+    const Real tau = (Real)P.tau, clamp = (Real)P.clamp, one_minus_clamp = (Real)(1.0 - P.clamp);
+    Real suffix = (g0 * (Real)P.bg[0] + g1 * (Real)P.bg[1] + g2 * (Real)P.bg[2]) * T;
+    const int lane = threadIdx.x & 31;
+    for (int hi = max_cnt; hi > 0; hi -= kTileThreads) {
+        const int lo = hi > kTileThreads ? hi - kTileThreads : 0;
+        __syncthreads();
+        const int q = lo + (int)threadIdx.x;
+        if (q < hi) {
+            const uint32_t id = ids[start + q];
+            sid[threadIdx.x] = id;
+            srec[threadIdx.x] = recs[id];
+        }
+        __syncthreads();
+        for (int j = hi - 1; j >= lo; --j) {
+            Real v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+            bool contrib = false;
+            if (j < my_cnt) {
+                SplatEval<Real> e;
+                eval_splat(srec[j - lo], px, py, tau, clamp, one_minus_clamp, e);
+                if (e.a != (Real)0) {
+                    // _tiles.py:97-127, T_i rebuilt by division from T_final
+                    contrib = true;
+                    const Real ti = T / e.om;
+                    const Real w = e.a * ti;
+                    v[7] = w * g0;
+                    v[8] = w * g1;
+                    v[9] = w * g2;
+                    const Real gc = g0 * e.c0 + g1 * e.c1 + g2 * e.c2;
+                    const Real ga = gc * ti - suffix / e.om;
+                    suffix += gc * w;
+                    T = ti;
+                    if (e.a < clamp) {
+                        const Real x = e.m / tau;
+                        const Real gaa = ga * e.a;
+                        v[5] = ga * (e.a / e.og);
+                        v[6] = gaa * log1p_(-x);
+                        const Real gm = gaa * (-e.bx / ((Real)1 - x)) / tau;
+                        v[0] = (Real)-2 * gm * e.pd0;
+                        v[1] = (Real)-2 * gm * e.pd1;
+                        v[2] = gm * e.dx * e.dx;
+                        v[3] = gm * e.dx * e.dy;  // both off-diagonals of pg_p2 get this (_tiles.py:125-126)
+                        v[4] = gm * e.dy * e.dy;
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) v[k] = warp_sum(v[k]);
+                Real mine = v[0];
+#pragma unroll
+                for (int k = 1; k < 10; ++k)
+                    if (lane == k) mine = v[k];
+                if (lane < 10 && mine != (Real)0)
+                    atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + lane, mine);
+            }
+        }
+    }
+}
+
+}  // namespace ubs
+
+using namespace ubs;
+
+extern "C" int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                                  const UbsImageBuffers *ib, ubs_stream_t stream) {
+    if (!v || !pb || !bb || !ib || !ib->image || !ib->alpha_sum || !ib->t_stop || !ib->n_contrib ||
+        !ib->hit_clamp || !ib->visits)
+        return UBS_E_ARGS;
+    const RasterParams P = make_params(*v);
+    const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ib->raster_f64) {
+        if (!pb->rec64) return UBS_E_ARGS;
+        raster_fwd64_kernel<<<n_tiles, kTileThreads, 0, s>>>(
+            P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (double *)ib->image, (double *)ib->alpha_sum,
+            (double *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits);
+    } else {
+        if (!pb->rec32 || !pb->rec64 || !ib->fix_list || !ib->fix_count) return UBS_E_ARGS;
+        raster_fwd32_kernel<<<n_tiles, kTileThreads, 0, s>>>(
+            P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (float *)ib->image, (float *)ib->alpha_sum,
+            (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits, ib->fix_list, ib->fix_count);
+        UBS_CUDA_CHECK();
+        // one pass over the (device-counted) fix-up list; grid sized for the GPU, not the list
+        raster_fixup_kernel<<<148 * 4, 256, 0, s>>>(P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64,
+                                                    ib->fix_list, ib->fix_count, (float *)ib->image,
+                                                    (float *)ib->alpha_sum, (float *)ib->t_stop, ib->n_contrib,
+                                                    ib->hit_clamp, ib->visits);
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                                   const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t stream) {
+    if (!v || !pb || !bb || !ib || !gb || !gb->g_image || !gb->grad2d) return UBS_E_ARGS;
+    if ((gb->grad2d_f64 != 0) != (ib->raster_f64 != 0)) return UBS_E_ARGS;
+    const RasterParams P = make_params(*v);
+    const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ib->raster_f64) {
+        raster_bwd_kernel<double><<<n_tiles, kTileThreads, 0, s>>>(
+            P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
+            (const double *)gb->g_image, (double *)gb->grad2d);
+    } else {
+        raster_bwd_kernel<float><<<n_tiles, kTileThreads, 0, s>>>(
+            P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
+            (const float *)gb->g_image, (float *)gb->grad2d);
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}

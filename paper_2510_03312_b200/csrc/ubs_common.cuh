@@ -1,0 +1,421 @@
+// Shared device code for the B200 UBS render path (sm_100a).
+//
+// The per-primitive math (conditioning + projection) is evaluated in fp64,
+// one thread per primitive.  B200 runs fp64 at half the fp32 rate, and the
+// survey measured that fp32 geometry mis-bins primitives and reorders depth
+// ties, so bit-exact binning needs fp64 here.  The same
+// routine feeds the preprocess kernel and the backward chain (which
+// recomputes instead of storing ~120 doubles per primitive).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ubs_b200.h"
+
+namespace ubs {
+
+constexpr int kTile = 16;
+constexpr int kTileThreads = kTile * kTile;
+constexpr uint64_t kInvisibleKey = 0xFFFFFFFFFFFFFFFFull;
+constexpr int kGrad2dStride = 12;  // g_mean2[2] g_P[00,01,11] g_og g_bx g_color[3] pad[2]
+
+// fp64 raster record: exactly the operands tile_forward reads (_tiles.py:36-50).
+struct __align__(16) Rec64 {
+    double mx, my;          // mean2
+    double p00, p01, p11;   // inverse screen covariance (raster.py:436-446)
+    double og, bx;          // gated opacity, spatial exponent
+    double cr, cg, cb;      // raw colour (not activated, raster.py:297)
+};
+static_assert(sizeof(Rec64) == 80, "Rec64 layout");
+
+// fp32 raster record, 64 B = 4 x 16 B vector loads.
+//  r0: ix, iy (floor of mean2, int bits), ox, oy = 0.5 - frac(mean2)
+//      -> dx = float(px - ix) + ox is exact to ~1e-7 px at any image size
+//  r1: u00, u01, u11 (P = U^T U, m = (u00 dx + u01 dy)^2 + (u11 dy)^2), og
+//  r2: beta_x, colour
+//  r3: eb = beta_x * E, E a bound on |m32 - m64| over the splat's support;
+//      flags
+struct __align__(16) Rec32 {
+    float4 r0, r1, r2, r3;
+};
+static_assert(sizeof(Rec32) == 64, "Rec32 layout");
+
+// --- fp64 helpers with contraction disabled: the tile loops must round like
+// numba (no FMA contraction by default) so the contributor count decision
+// T < t_min matches the reference.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename PT>
+__device__ __forceinline__ double ld(const PT *p, int64_t i) { return (double)p[i]; }
+
+// ---------------------------------------------------------------------------
+// small dense fp64 linear algebra
+// ---------------------------------------------------------------------------
+
+// Cholesky of a CxC SPD matrix (row-major), LAPACK dpotrf failure rule:
+// a pivot that is not > 0 (or NaN) fails.
+template <int C>
+__device__ __forceinline__ bool cholesky(const double (&A)[C][C], double (&L)[C][C]) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        double s = A[j][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+        if (!(s > 0.0)) return false;
+        double d = sqrt(s);
+        L[j][j] = d;
+#pragma unroll
+        for (int i = j + 1; i < C; ++i) {
+            double t = A[i][j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+            L[i][j] = t / d;
+        }
+#pragma unroll
+        for (int i = 0; i < j; ++i) L[i][j] = 0.0;
+    }
+    return true;
+}
+
+// inverse from a Cholesky factor: A^-1 = L^-T L^-1
+template <int C>
+__device__ __forceinline__ void chol_inverse(const double (&L)[C][C], double (&M)[C][C]) {
+    double Li[C][C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+#pragma unroll
+        for (int i = 0; i < C; ++i) Li[i][j] = 0.0;
+        Li[j][j] = 1.0 / L[j][j];
+#pragma unroll
+        for (int i = j + 1; i < C; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = j; k < i; ++k) s += L[i][k] * Li[k][j];
+            Li[i][j] = -s / L[i][i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < C; ++i)
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < C; ++k) s += Li[k][i] * Li[k][j];
+            M[i][j] = s;
+        }
+}
+
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi; ascending eigenvalues,
+// eigenvectors as columns of V.  Only reached for primitives whose
+// conditioned covariance needs the PSD floor (rare), so robustness beats speed.
+__device__ inline void eigh3(const double (&A)[3][3], double (&w)[3], double (&V)[3][3]) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            a[i][j] = A[i][j];
+            V[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+    for (int sweep = 0; sweep < 32; ++sweep) {
+        double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+        double scale = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]);
+        if (off == 0.0 || off <= 1e-300 || off < 1e-18 * scale) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                double apq = a[p][q];
+                if (apq == 0.0) continue;
+                double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+                double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 3; ++k) {
+                    double akp = a[k][p], akq = a[k][q];
+                    a[k][p] = c * akp - s * akq;
+                    a[k][q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double apk = a[p][k], aqk = a[q][k];
+                    a[p][k] = c * apk - s * aqk;
+                    a[q][k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double vkp = V[k][p], vkq = V[k][q];
+                    V[k][p] = c * vkp - s * vkq;
+                    V[k][q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    for (int i = 0; i < 3; ++i) w[i] = a[i][i];
+    // sort ascending (selection sort, swap columns)
+    for (int i = 0; i < 2; ++i) {
+        int m = i;
+        for (int j = i + 1; j < 3; ++j)
+            if (w[j] < w[m]) m = j;
+        if (m != i) {
+            double t = w[i]; w[i] = w[m]; w[m] = t;
+            for (int k = 0; k < 3; ++k) { double u = V[k][i]; V[k][i] = V[k][m]; V[k][m] = u; }
+        }
+    }
+}
+
+// Symmetric 2x2 eigen-decomposition [[a,b],[b,d]], ascending, columns of V.
+__device__ inline void eigh2(double a, double b, double d, double (&w)[2], double (&V)[2][2]) {
+    double h = 0.5 * (a + d), g = 0.5 * (a - d);
+    double r = sqrt(g * g + b * b);
+    w[0] = h - r;
+    w[1] = h + r;
+    if (b == 0.0) {
+        if (a <= d) { V[0][0] = 1; V[1][0] = 0; V[0][1] = 0; V[1][1] = 1; }
+        else { V[0][0] = 0; V[1][0] = 1; V[0][1] = 1; V[1][1] = 0; }
+        if (a == d) { V[0][0] = 1; V[1][0] = 0; V[0][1] = 0; V[1][1] = 1; }
+        return;
+    }
+    // eigenvector of the larger eigenvalue, from the better conditioned row
+    double x1, y1;
+    if (g >= 0.0) { x1 = g + r; y1 = b; } else { x1 = b; y1 = r - g; }
+    double nrm = sqrt(x1 * x1 + y1 * y1);
+    x1 /= nrm; y1 /= nrm;
+    V[0][1] = x1; V[1][1] = y1;
+    V[0][0] = -y1; V[1][0] = x1;
+}
+
+// ---------------------------------------------------------------------------
+// Per-primitive conditioning + projection (fp64).
+// slicing.py:185-235 (with covariance.py:57-159, kernels.py:18-25) and
+// raster.py:95-134.
+// ---------------------------------------------------------------------------
+template <int C>
+struct PrimGeom {
+    static constexpr int CC = C > 0 ? C : 1;
+    // activated parameters
+    double sx[3], sq[CC], lqx[CC][3], R[3][3], Lx[3][3];
+    double beta_x, beta_q[CC], opacity, color[3];
+    // conditioning
+    double Sxq[3][CC], M[CC][CC];
+    double delta[CC], u[CC], v[CC], mean3[3];
+    double sym3[3][3], cov3[3][3], floor_eps;
+    double s_tanh[CC], d_gate[CC], gate, og;
+    bool valid, floored3;
+    // projection
+    double tcam[3], z, mean2[2], V[2][3], raw2[3], cov2[3], p2[3], radii[2];
+    bool in_front, floored2, visible;
+};
+
+template <int C, typename PT>
+__device__ inline void load_params(const PT *rec, double (&mu_x)[3], double *mu_q, double (&rot)[3],
+                                   double (&sxr)[3], double *lqx /*C*3*/, double *sqr, double &bxr,
+                                   double *bqr, double &oraw, double (&col)[3]) {
+    int o = 0;
+    for (int k = 0; k < 3; ++k) mu_x[k] = (double)rec[o++];
+    for (int k = 0; k < C; ++k) mu_q[k] = (double)rec[o++];
+    for (int k = 0; k < 3; ++k) rot[k] = (double)rec[o++];
+    for (int k = 0; k < 3; ++k) sxr[k] = (double)rec[o++];
+    for (int k = 0; k < 3 * C; ++k) lqx[k] = (double)rec[o++];
+    for (int k = 0; k < C; ++k) sqr[k] = (double)rec[o++];
+    bxr = (double)rec[o++];
+    for (int k = 0; k < C; ++k) bqr[k] = (double)rec[o++];
+    oraw = (double)rec[o++];
+    for (int k = 0; k < 3; ++k) col[k] = (double)rec[o++];
+}
+
+__device__ __forceinline__ double sigmoid64(double x) {
+    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+    double e = exp(x);
+    return e / (1.0 + e);
+}
+
+template <int C, typename PT>
+__device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g, double (&mu_x)[3]) {
+    constexpr int CC = PrimGeom<C>::CC;
+    double mu_q[CC], rot[3], sxr[3], lq[CC * 3], sqr[CC], bxr, bqr[CC], oraw;
+    load_params<C>(rec, mu_x, mu_q, rot, sxr, lq, sqr, bxr, bqr, oraw, g.color);
+
+    for (int k = 0; k < 3; ++k) g.sx[k] = exp(sxr[k]);
+    // R = I + A, A skew from (a1, a2, a3)  (covariance.py:57-72)
+    g.R[0][0] = 1.0;     g.R[0][1] = -rot[2]; g.R[0][2] = rot[1];
+    g.R[1][0] = rot[2];  g.R[1][1] = 1.0;     g.R[1][2] = -rot[0];
+    g.R[2][0] = -rot[1]; g.R[2][1] = rot[0];  g.R[2][2] = 1.0;
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) g.Lx[i][k] = g.R[i][k] * g.sx[k];
+    double Sx[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            Sx[i][j] = g.Lx[i][0] * g.Lx[j][0] + g.Lx[i][1] * g.Lx[j][1] + g.Lx[i][2] * g.Lx[j][2];
+
+    g.beta_x = 4.0 * exp(bxr);
+    g.opacity = sigmoid64(oraw);
+    g.valid = true;
+    double mean3[3] = {mu_x[0], mu_x[1], mu_x[2]};
+    double raw[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) raw[i][j] = Sx[i][j];
+    g.gate = 1.0;
+
+    if constexpr (C > 0) {
+        for (int k = 0; k < C; ++k) {
+            g.sq[k] = exp(sqr[k]);
+            g.beta_q[k] = exp(bqr[k]);
+            for (int j = 0; j < 3; ++j) g.lqx[k][j] = lq[3 * k + j];
+        }
+        double Sq[C][C];
+        for (int i = 0; i < 3; ++i)
+            for (int k = 0; k < C; ++k)
+                g.Sxq[i][k] = g.Lx[i][0] * g.lqx[k][0] + g.Lx[i][1] * g.lqx[k][1] + g.Lx[i][2] * g.lqx[k][2];
+        bool finite = true;
+        for (int i = 0; i < C; ++i)
+            for (int j = 0; j < C; ++j) {
+                double s = g.lqx[i][0] * g.lqx[j][0] + g.lqx[i][1] * g.lqx[j][1] + g.lqx[i][2] * g.lqx[j][2];
+                if (i == j) s += g.sq[i] * g.sq[i];
+                Sq[i][j] = s;
+                finite &= isfinite(s);
+            }
+        // invert_query_block (covariance.py:122-149): Cholesky test, one
+        // 1e-8 jitter, still failing -> degenerate with identity slot
+        double L[C][C];
+        bool ok = finite && cholesky<C>(Sq, L);
+        if (finite && !ok) {
+            for (int i = 0; i < C; ++i) Sq[i][i] += 1e-8;
+            ok = cholesky<C>(Sq, L);
+        }
+        if (ok) {
+            chol_inverse<C>(L, g.M);
+        } else {
+            g.valid = false;
+            for (int i = 0; i < C; ++i)
+                for (int j = 0; j < C; ++j) g.M[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        // conditional mean (slicing.py:205-208)
+        for (int k = 0; k < C; ++k) {
+            g.delta[k] = v.query[k] - mu_q[k];
+            g.u[k] = g.beta_q[k] * g.delta[k];
+        }
+        for (int i = 0; i < C; ++i) {
+            double s = 0.0;
+            for (int k = 0; k < C; ++k) s += g.M[i][k] * g.u[k];
+            g.v[i] = s;
+        }
+        for (int i = 0; i < 3; ++i) {
+            double s = 0.0;
+            for (int k = 0; k < C; ++k) s += g.Sxq[i][k] * g.v[k];
+            mean3[i] = mu_x[i] + s;
+        }
+        // conditional covariance: Sx - Sxq M diag(beta_q) Sqx (slicing.py:210-211)
+        double H[3][C];  // Sxq M
+        for (int i = 0; i < 3; ++i)
+            for (int k = 0; k < C; ++k) {
+                double s = 0.0;
+                for (int j = 0; j < C; ++j) s += g.Sxq[i][j] * g.M[j][k];
+                H[i][k] = s;
+            }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double s = 0.0;
+                for (int k = 0; k < C; ++k) s += H[i][k] * g.beta_q[k] * g.Sxq[j][k];
+                raw[i][j] = Sx[i][j] - s;
+            }
+        // opacity gate (slicing.py:224-228)
+        double lsum = 0.0;
+        for (int i = 0; i < C; ++i) {
+            double dr = 0.0;
+            for (int k = 0; k < C; ++k) dr += g.M[i][k] * g.delta[k];
+            double s = tanh(0.5 * dr);
+            g.s_tanh[i] = s;
+            double d = v.set.gate_symmetric ? fabs(s) : fmax(s, 0.0);
+            g.d_gate[i] = d;
+            lsum += 4.0 * g.beta_q[i] * log1p(-d);
+        }
+        g.gate = exp(lsum);
+    }
+    for (int i = 0; i < 3; ++i) g.mean3[i] = mean3[i];
+    g.og = g.opacity * g.gate;
+
+    // symmetrise + PSD eigen floor (slicing.py:212-222)
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) g.sym3[i][j] = 0.5 * (raw[i][j] + raw[j][i]);
+    g.floor_eps = v.set.psd_floor_scale * (Sx[0][0] + Sx[1][1] + Sx[2][2]) / 3.0;
+    {
+        // cheap test first: sym - eps I positive definite <=> lambda_min > eps
+        double T[3][3], L3[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) T[i][j] = g.sym3[i][j] - (i == j ? g.floor_eps : 0.0);
+        bool pd = cholesky<3>(T, L3);
+        g.floored3 = false;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) g.cov3[i][j] = g.sym3[i][j];
+        if (!pd) {
+            double w[3], Vv[3][3];
+            eigh3(g.sym3, w, Vv);
+            if (w[0] < g.floor_eps) {
+                g.floored3 = true;
+                for (int k = 0; k < 3; ++k) w[k] = fmax(w[k], g.floor_eps);
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        g.cov3[i][j] = Vv[i][0] * w[0] * Vv[j][0] + Vv[i][1] * w[1] * Vv[j][1] +
+                                       Vv[i][2] * w[2] * Vv[j][2];
+            }
+        }
+    }
+
+    // projection (raster.py:99-131)
+    const double *Rc = v.cam.rot;
+    for (int i = 0; i < 3; ++i)
+        g.tcam[i] = Rc[3 * i] * mean3[0] + Rc[3 * i + 1] * mean3[1] + Rc[3 * i + 2] * mean3[2] + v.cam.trans[i];
+    g.in_front = g.tcam[2] > v.set.near_plane;
+    g.z = g.in_front ? g.tcam[2] : 1.0;
+    const double z = g.z, x = g.tcam[0], y = g.tcam[1];
+    const double fx = v.cam.fx, fy = v.cam.fy;
+    g.mean2[0] = fx * x / z + v.cam.cx;
+    g.mean2[1] = fy * y / z + v.cam.cy;
+    double J[2][3] = {{fx / z, 0.0, -fx * x / (z * z)}, {0.0, fy / z, -fy * y / (z * z)}};
+    for (int i = 0; i < 2; ++i)
+        for (int k = 0; k < 3; ++k) g.V[i][k] = J[i][0] * Rc[k] + J[i][1] * Rc[3 + k] + J[i][2] * Rc[6 + k];
+    double VC[2][3];
+    for (int i = 0; i < 2; ++i)
+        for (int k = 0; k < 3; ++k)
+            VC[i][k] = g.V[i][0] * g.cov3[0][k] + g.V[i][1] * g.cov3[1][k] + g.V[i][2] * g.cov3[2][k];
+    double r00 = VC[0][0] * g.V[0][0] + VC[0][1] * g.V[0][1] + VC[0][2] * g.V[0][2];
+    double r01 = VC[0][0] * g.V[1][0] + VC[0][1] * g.V[1][1] + VC[0][2] * g.V[1][2];
+    double r10 = VC[1][0] * g.V[0][0] + VC[1][1] * g.V[0][1] + VC[1][2] * g.V[0][2];
+    double r11 = VC[1][0] * g.V[1][0] + VC[1][1] * g.V[1][1] + VC[1][2] * g.V[1][2];
+    g.raw2[0] = r00;
+    g.raw2[1] = 0.5 * (r01 + r10);
+    g.raw2[2] = r11;
+    {
+        double w[2], E[2][2];
+        eigh2(g.raw2[0], g.raw2[1], g.raw2[2], w, E);
+        g.floored2 = w[0] < v.set.screen_cov_floor;
+        if (g.floored2) {
+            double f0 = fmax(w[0], v.set.screen_cov_floor), f1 = fmax(w[1], v.set.screen_cov_floor);
+            g.cov2[0] = E[0][0] * f0 * E[0][0] + E[0][1] * f1 * E[0][1];
+            g.cov2[1] = E[0][0] * f0 * E[1][0] + E[0][1] * f1 * E[1][1];
+            g.cov2[2] = E[1][0] * f0 * E[1][0] + E[1][1] * f1 * E[1][1];
+        } else {
+            g.cov2[0] = g.raw2[0];
+            g.cov2[1] = g.raw2[1];
+            g.cov2[2] = g.raw2[2];
+        }
+    }
+    const double a = g.cov2[0], b = g.cov2[1], d = g.cov2[2];
+    const double det = a * d - b * b;
+    g.p2[0] = d / det;
+    g.p2[1] = -b / det;
+    g.p2[2] = a / det;
+    g.radii[0] = sqrt(v.set.tau_sq * a);
+    g.radii[1] = sqrt(v.set.tau_sq * d);
+    const double mg = v.set.cull_margin;
+    const double lox = g.mean2[0] - g.radii[0], hix = g.mean2[0] + g.radii[0];
+    const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
+    bool on_screen = (hix >= -mg) && (lox <= v.cam.width + mg) && (hiy >= -mg) && (loy <= v.cam.height + mg);
+    g.visible = g.in_front && on_screen && g.valid;
+}
+
+}  // namespace ubs
+
+#define UBS_CUDA_CHECK()                                   \
+    do {                                                   \
+        if (cudaPeekAtLastError() != cudaSuccess) {        \
+            (void)cudaGetLastError();                      \
+            return UBS_E_CUDA;                             \
+        }                                                  \
+    } while (0)

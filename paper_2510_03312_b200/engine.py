@@ -1,0 +1,372 @@
+"""Device-resident render engine: HBM scene, per-frame workspaces, stage driver.
+
+The engine strings the C-ABI stages together on one CUDA stream:
+
+    ubs_preprocess -> ubs_bin_depth -> (read K) -> ubs_bin_tiles -> ubs_raster_forward
+    [ubs_loss_image_grad] -> ubs_raster_backward -> ubs_prim_backward
+
+Buffers are torch tensors (PyTorch is the device allocator and stream owner;
+the kernels are ours).  Workspaces grow geometrically and are reused across
+frames, so a steady-state frame allocates nothing.  One 16-byte device->host
+read per frame fetches the tile-pair count K before the pair buffers are
+used; everything else is stream ordered.
+
+Precision modes (``precision=``):
+  * ``"fp32"``: fp32 records and raster, fp64 preprocess, fp64 fix-up of the
+    pixels whose cut/clamp decisions are not certified in fp32 -> integer
+    outputs bit-exact, images within ~1e-5 of the reference;
+  * ``"fp64"``: fp64 records and raster with the reference's operation order.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (GRAD2D_STRIDE, REC32_BYTES, REC64_BYTES, UbsBinBuffers, UbsCamera, UbsGradBuffers,
+                   UbsImageBuffers, UbsPrimBuffers, UbsSettings, UbsView, check)
+from .types import DEFAULT_SETTINGS, PARAM_FIELDS, pack_records, record_width
+
+TILE = 16
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _require_cuda(device) -> torch.device:
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise _lib.UbsError("the UBS engine runs on CUDA devices only (no CPU fallback)")
+    if not torch.cuda.is_available():
+        raise _lib.UbsError("no CUDA device available: the UBS engine has no CPU fallback")
+    return dev
+
+
+class DeviceScene:
+    """A scene resident in HBM as packed UBS1 records (n x (14+6C))."""
+
+    def __init__(self, params: torch.Tensor, n_dims: int, background):
+        if params.dim() != 2 or params.shape[1] != record_width(n_dims):
+            raise ValueError("params must be (n, 14+6C)")
+        if params.dtype not in (torch.float32, torch.float64):
+            raise ValueError("params must be float32 or float64")
+        self.params = params.contiguous()
+        self.n_dims = int(n_dims)
+        self.background = tuple(float(b) for b in np.asarray(background, dtype=np.float64).reshape(3))
+
+    @classmethod
+    def from_scene(cls, scene, dtype=torch.float32, device="cuda") -> "DeviceScene":
+        dev = _require_cuda(device)
+        npdt = np.float64 if dtype == torch.float64 else np.float32
+        rec = pack_records(scene, npdt)
+        t = torch.from_numpy(rec).to(dev, non_blocking=False)
+        return cls(t, scene.n_dims, scene.background)
+
+    @property
+    def n(self) -> int:
+        return int(self.params.shape[0])
+
+    @property
+    def device(self):
+        return self.params.device
+
+
+def make_view(ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS) -> UbsView:
+    if int(settings.tile_size) != TILE:
+        raise ValueError("tile_size must be 16 on the device path")
+    c = ds.n_dims - 3
+    q = np.asarray(query.dims, dtype=np.float64).reshape(-1)
+    if q.shape[0] != c:
+        raise ValueError(f"query has {q.shape[0]} dims, scene expects {c}")
+    v = UbsView()
+    v.params = _ptr(ds.params)
+    v.n = ds.n
+    v.n_dims = ds.n_dims
+    v.param_f64 = 1 if ds.params.dtype == torch.float64 else 0
+    for k in range(3):
+        v.background[k] = ds.background[k]
+    for k in range(4):
+        v.query[k] = float(q[k]) if k < c else 0.0
+    w2c = np.asarray(cam.world_to_cam, dtype=np.float64).reshape(4, 4)
+    cc = UbsCamera()
+    cc.fx, cc.fy, cc.cx, cc.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    for i in range(3):
+        for j in range(3):
+            cc.rot[3 * i + j] = w2c[i, j]
+        cc.trans[i] = w2c[i, 3]
+    cc.width, cc.height = int(cam.width), int(cam.height)
+    v.cam = cc
+    st = UbsSettings()
+    st.tau_sq = float(settings.tau_sq)
+    st.alpha_clamp = float(settings.alpha_clamp)
+    st.transmittance_min = float(settings.transmittance_min)
+    st.near_plane = float(settings.near_plane)
+    st.cull_margin = float(settings.cull_margin)
+    st.screen_cov_floor = float(settings.screen_cov_floor)
+    st.psd_floor_scale = float(settings.psd_floor_scale)
+    st.gate_symmetric = 1 if settings.gate_symmetric else 0
+    st.tile_size = TILE
+    v.set = st
+    return v
+
+
+@dataclass
+class Frame:
+    """Device-side result of one forward frame (views into engine workspaces).
+
+    The tensors are overwritten by the next frame rendered with the same
+    workspace; clone what you keep.
+    """
+
+    view: UbsView
+    width: int
+    height: int
+    n: int
+    n_visible: int
+    n_pairs: int
+    image: torch.Tensor       # (H, W, 3)
+    alpha_sum: torch.Tensor   # (H, W)
+    t_stop: torch.Tensor      # (H, W)
+    n_contrib: torch.Tensor   # (H, W) int32
+    hit_clamp: torch.Tensor   # (n,) uint8
+    ws: "Workspace"
+    raster_f64: bool
+
+    @property
+    def processed_pixels(self) -> int:
+        return int(self.ws.counters[1].item())
+
+    @property
+    def n_fixed(self) -> int:
+        return int(self.ws.counters32[6].item())
+
+
+class Workspace:
+    """Every device buffer one frame needs; grows on demand, reused across frames."""
+
+    def __init__(self, device, precision: str = "fp32"):
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+        self.device = _require_cuda(device)
+        self.precision = precision
+        self.f64 = precision == "fp64"
+        self.lib = _lib.load()
+        self.n_cap = 0
+        self.pix_cap = 0
+        self.tile_cap = 0
+        self.pair_cap = 0
+        self.temp_bytes = 0
+        # [0] n_pairs u64 | [1] visits u64 | [2] lo: n_visible u32 | [3] lo: fix_count u32
+        self.counters = torch.zeros(8, dtype=torch.int64, device=self.device)
+        self.counters32 = self.counters.view(torch.int32)
+        self.debug = None
+        self.grad2d = None
+        self.loss_scratch = None
+        self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    # --- allocation -------------------------------------------------------
+    def _i(self, n, dtype):
+        return torch.empty(max(int(n), 1), dtype=dtype, device=self.device)
+
+    def ensure_prims(self, n: int):
+        if n <= self.n_cap:
+            return
+        cap = max(n, int(self.n_cap * 1.25))
+        self.depth_key = self._i(cap, torch.int64)
+        self.rect = self._i(cap, torch.int64)
+        self.tile_count = self._i(cap, torch.int32)
+        self.flags = self._i(cap, torch.int16)
+        self.rec64 = self._i(cap * REC64_BYTES // 8, torch.float64)
+        self.rec32 = None if self.f64 else self._i(cap * REC32_BYTES // 4, torch.float32)
+        self.keys_sorted = self._i(cap, torch.int64)
+        self.ids_iota = self._i(cap, torch.int32)
+        self.order = self._i(cap, torch.int32)
+        self.offsets = self._i(cap, torch.int32)
+        self.hit_clamp = self._i(cap, torch.uint8)
+        self.n_cap = cap
+        self.temp_bytes = 0  # CUB scratch depends on n
+
+    def ensure_pixels(self, width: int, height: int):
+        npix = width * height
+        ntiles = math.ceil(width / TILE) * math.ceil(height / TILE)
+        fdt = torch.float64 if self.f64 else torch.float32
+        if npix > self.pix_cap:
+            cap = npix
+            self.image_buf = self._i(cap * 3, fdt)
+            self.asum_buf = self._i(cap, fdt)
+            self.tstop_buf = self._i(cap, fdt)
+            self.ncontrib_buf = self._i(cap, torch.int32)
+            self.fix_list = self._i(cap, torch.int32)
+            self.g_image_buf = self._i(cap * 3, fdt)
+            self.loss_scratch = None
+            self.pix_cap = cap
+        if ntiles > self.tile_cap:
+            self.tile_ranges = self._i(2 * ntiles, torch.int32)
+            self.tile_cap = ntiles
+            self.temp_bytes = 0
+
+    def ensure_pairs(self, k: int):
+        if k > self.pair_cap:
+            cap = max(k, int(self.pair_cap * 1.3), 1024)
+            self.pair_keys = self._i(cap, torch.int32)
+            self.pair_vals = self._i(cap, torch.int32)
+            self.pair_keys_sorted = self._i(cap, torch.int32)
+            self.tile_ids = self._i(cap, torch.int32)
+            self.pair_cap = cap
+            self.temp_bytes = 0
+        need = int(self.lib.ubs_bin_temp_bytes(self.n_cap, self.pair_cap, self.tile_cap))
+        if need > self.temp_bytes:
+            self.temp = self._i(need, torch.uint8)
+            self.temp_bytes = need
+
+    # --- C structs --------------------------------------------------------
+    def prim_buffers(self, want_debug=False) -> UbsPrimBuffers:
+        pb = UbsPrimBuffers()
+        pb.depth_key = _ptr(self.depth_key)
+        pb.rect = _ptr(self.rect)
+        pb.tile_count = _ptr(self.tile_count)
+        pb.flags = _ptr(self.flags)
+        pb.rec32 = _ptr(self.rec32)
+        pb.rec64 = _ptr(self.rec64)
+        pb.debug = _ptr(self.debug) if want_debug else 0
+        pb.n_visible = _ptr(self.counters) + 16
+        pb.n_pairs = _ptr(self.counters)
+        return pb
+
+    def bin_buffers(self) -> UbsBinBuffers:
+        bb = UbsBinBuffers()
+        bb.keys_sorted = _ptr(self.keys_sorted)
+        bb.ids_iota = _ptr(self.ids_iota)
+        bb.order = _ptr(self.order)
+        bb.offsets = _ptr(self.offsets)
+        if self.pair_cap:
+            bb.pair_keys = _ptr(self.pair_keys)
+            bb.pair_vals = _ptr(self.pair_vals)
+            bb.pair_keys_sorted = _ptr(self.pair_keys_sorted)
+            bb.tile_ids = _ptr(self.tile_ids)
+        bb.tile_ranges = _ptr(self.tile_ranges)
+        bb.pair_capacity = self.pair_cap
+        bb.temp = _ptr(self.temp) if self.temp_bytes else 0
+        bb.temp_bytes = self.temp_bytes
+        return bb
+
+    def image_buffers(self) -> UbsImageBuffers:
+        ib = UbsImageBuffers()
+        ib.image = _ptr(self.image_buf)
+        ib.alpha_sum = _ptr(self.asum_buf)
+        ib.t_stop = _ptr(self.tstop_buf)
+        ib.n_contrib = _ptr(self.ncontrib_buf)
+        ib.hit_clamp = _ptr(self.hit_clamp)
+        ib.visits = _ptr(self.counters) + 8
+        ib.fix_list = _ptr(self.fix_list)
+        ib.fix_count = _ptr(self.counters) + 24
+        ib.raster_f64 = 1 if self.f64 else 0
+        return ib
+
+
+def _stream_ptr() -> int:
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS,
+                 want_debug: bool = False) -> Frame:
+    """Forward one frame on the current stream; returns device views."""
+    lib = ws.lib
+    if ds.device != ws.device:
+        raise ValueError("scene and workspace live on different devices")
+    v = make_view(ds, cam, query, settings)
+    W, H, n = int(cam.width), int(cam.height), ds.n
+    ws.ensure_prims(max(n, 1))
+    ws.ensure_pixels(W, H)
+    if want_debug:
+        if ws.debug is None or ws.debug.numel() < n * _lib.DEBUG_STRIDE:
+            ws.debug = torch.zeros(max(n, 1) * _lib.DEBUG_STRIDE, dtype=torch.float64, device=ws.device)
+    if ws.temp_bytes == 0:
+        ws.ensure_pairs(0)
+    s = _stream_ptr()
+    ws.counters.zero_()
+    pb = ws.prim_buffers(want_debug)
+    if n:
+        check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
+        check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
+    host = ws.counters[:3].cpu()  # the one per-frame sync: K and n_visible
+    k = int(host[0])
+    n_vis = int(host.view(torch.int32)[4])
+    if k >= 2 ** 31:
+        raise _lib.UbsError(f"{k} tile pairs exceed the 2^31 device limit")
+    ws.ensure_pairs(k)
+    bb = ws.bin_buffers()
+    check(lib.ubs_bin_tiles(v, pb, bb, k, s), "ubs_bin_tiles")
+    ws.hit_clamp[:max(n, 1)].zero_()
+    check(lib.ubs_raster_forward(v, pb, bb, ws.image_buffers(), s), "ubs_raster_forward")
+    npix = W * H
+    return Frame(view=v, width=W, height=H, n=n, n_visible=n_vis, n_pairs=k,
+                 image=ws.image_buf[:npix * 3].view(H, W, 3), alpha_sum=ws.asum_buf[:npix].view(H, W),
+                 t_stop=ws.tstop_buf[:npix].view(H, W), n_contrib=ws.ncontrib_buf[:npix].view(H, W),
+                 hit_clamp=ws.hit_clamp[:n], ws=ws, raster_f64=ws.f64)
+
+
+def loss_image_grad(fr: Frame, target: torch.Tensor, lambda_ssim: float, scale: float):
+    """L1 + SSIM image gradient into the workspace g_image buffer.
+
+    Returns (g_image view, loss_parts tensor [sum|diff|, sum ssim_map]) — the
+    parts are accumulated (zero ``ws.loss_parts`` to start a batch)."""
+    ws = fr.ws
+    H, W = fr.height, fr.width
+    f64 = 1 if fr.raster_f64 else 0
+    tgt = target.to(device=ws.device, dtype=fr.image.dtype).contiguous()
+    need = int(ws.lib.ubs_loss_scratch_bytes(H, W, f64))
+    if ws.loss_scratch is None or ws.loss_scratch.numel() < need:
+        ws.loss_scratch = torch.empty(need, dtype=torch.uint8, device=ws.device)
+    g = ws.g_image_buf[:H * W * 3]
+    check(ws.lib.ubs_loss_image_grad(_ptr(fr.image), _ptr(tgt), H, W, f64, float(lambda_ssim), float(scale),
+                                     _ptr(g), _ptr(ws.loss_parts), _ptr(ws.loss_scratch), _stream_ptr()),
+          "ubs_loss_image_grad")
+    return g.view(H, W, 3), ws.loss_parts
+
+
+def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
+                   add_regularisers: bool = False, reg_opacity: float = 0.0, reg_scale: float = 0.0):
+    """Accumulate d(loss)/d(params) of one frame into ``grad_params`` (n x P)."""
+    ws = fr.ws
+    n = fr.n
+    if n == 0:
+        return
+    gdt = torch.float64 if fr.raster_f64 else torch.float32
+    if ws.grad2d is None or ws.grad2d.numel() < n * GRAD2D_STRIDE or ws.grad2d.dtype != gdt:
+        ws.grad2d = torch.empty(ws.n_cap * GRAD2D_STRIDE, dtype=gdt, device=ws.device)
+    ws.grad2d[:n * GRAD2D_STRIDE].zero_()
+    g_img = g_image.to(device=ws.device, dtype=fr.image.dtype).contiguous()
+    if grad_params.shape != ds.params.shape or not grad_params.is_contiguous():
+        raise ValueError("grad_params must be a contiguous (n, 14+6C) tensor")
+    gb = UbsGradBuffers()
+    gb.g_image = _ptr(g_img)
+    gb.grad2d = _ptr(ws.grad2d)
+    gb.grad_params = _ptr(grad_params)
+    gb.grad_f64 = 1 if grad_params.dtype == torch.float64 else 0
+    gb.grad2d_f64 = 1 if fr.raster_f64 else 0
+    gb.reg_opacity = float(reg_opacity)
+    gb.reg_scale = float(reg_scale)
+    gb.nonfinite = _ptr(ws.nonfinite)
+    s = _stream_ptr()
+    check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb, s),
+          "ubs_raster_backward")
+    check(ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, s), "ubs_prim_backward")
+
+
+def field_slices(n_dims: int) -> dict:
+    """PARAM_FIELDS name -> (column slice, per-primitive shape) in the packed record."""
+    c = n_dims - 3
+    out, off = {}, 0
+    for name, fn in PARAM_FIELDS:
+        shape = fn(c)
+        size = int(np.prod(shape)) if shape else 1
+        out[name] = (slice(off, off + size), shape)
+        off += size
+    return out

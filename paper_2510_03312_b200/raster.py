@@ -1,0 +1,166 @@
+"""Drop-in render entry points (reference raster.py:269-322) on the B200 engine.
+
+``render`` / ``render_with_cache`` take the reference's own argument objects
+(``Scene``, ``Camera``, ``Query``, ``RenderSettings``: duck-typed, so objects
+from ``betasplat`` work as well as this package's mirrors) and return float64
+numpy arrays like the reference.  The work happens on the GPU:
+parameters are uploaded as packed UBS1 records, and every stage runs in the
+sm_100a kernels of ``libubs_b200.so``.  There is no CPU fallback.
+
+Extra keyword arguments (not in the reference signature):
+  ``precision``  "fp32" (default: fp64 geometry, fp32 raster, certified
+                 fp64 fix-up) or "fp64" (reference arithmetic throughout);
+  ``device``     CUDA device (default: current).
+"""
+
+from __future__ import annotations
+
+import math
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+from . import engine
+from ._lib import DEBUG_STRIDE, F_DEGENERATE, F_FLOOR2, F_FLOOR3, F_VISIBLE
+from .types import DEFAULT_SETTINGS
+
+DEFAULT_PRECISION = "fp32"
+_WORKSPACES: dict = {}
+
+
+def workspace(precision: str | None = None, device=None) -> engine.Workspace:
+    """The shared per-(device, precision) workspace used by the numpy API."""
+    precision = precision or DEFAULT_PRECISION
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device()) \
+        if torch.cuda.is_available() else torch.device("cuda")
+    key = (str(dev), precision)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = engine.Workspace(dev, precision)
+        _WORKSPACES[key] = ws
+    return ws
+
+
+def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
+    # re-uploaded every call: callers such as fd_check mutate arrays in place,
+    # so a cached copy keyed on identity would go stale
+    dtype = torch.float64 if ws.f64 else torch.float32
+    return engine.DeviceScene.from_scene(scene, dtype=dtype, device=ws.device)
+
+
+def _host_image(fr: engine.Frame, background) -> np.ndarray:
+    """(H, W, 3) float64; pixels nothing was composited into get the exact fp64
+    background (acc = 0, T = 1 gives 0 + 1 * bg in tile_forward, _tiles.py:51-53)."""
+    img = fr.image.double().cpu().numpy().reshape(fr.height, fr.width, 3)
+    if not fr.raster_f64:
+        empty = ((fr.alpha_sum == 0) & (fr.t_stop == 1)).cpu().numpy()
+        if empty.any():
+            img[empty] = np.asarray(background, dtype=np.float64).reshape(3)
+    return img
+
+
+class FrameCache:
+    """Host view of one forward frame (reference raster.py:63-92).
+
+    Eager: image, alpha_sum, t_stop, alpha_clamped, processed_pixels, order,
+    n_contrib (per-pixel contributor count, not in the reference).
+    Lazy: ``tiles`` (per-tile id lists), ``slices`` / ``proj`` (a subset of the
+    reference's SliceCache / ProjectionCache fields, from a debug re-run).
+    """
+
+    def __init__(self, scene, camera, query, settings, precision, fr: engine.Frame):
+        self.scene, self.camera, self.query, self.settings = scene, camera, query, settings
+        self.precision = precision
+        H, W = fr.height, fr.width
+        self.image = _host_image(fr, scene.background)
+        self.alpha_sum = fr.alpha_sum.double().cpu().numpy()
+        self.t_stop = fr.t_stop.double().cpu().numpy()
+        self.n_contrib = fr.n_contrib.cpu().numpy()
+        self.alpha_clamped = fr.hit_clamp.cpu().numpy().astype(bool)
+        self.processed_pixels = fr.processed_pixels
+        self.n_fixed = 0 if fr.raster_f64 else fr.n_fixed
+        ws = fr.ws
+        self.order = ws.order[:fr.n_visible].to(torch.int64).cpu().numpy()
+        ntiles = math.ceil(W / 16) * math.ceil(H / 16)
+        self.tile_ranges = ws.tile_ranges[:2 * ntiles].view(ntiles, 2).to(torch.int64).cpu().numpy()
+        self.tile_ids = ws.tile_ids[:fr.n_pairs].to(torch.int64).cpu().numpy() if fr.n_pairs else \
+            np.zeros(0, dtype=np.int64)
+        self._flags = ws.flags[:fr.n].to(torch.int32).cpu().numpy() & 0xFFFF
+        self._tiles = None
+        self._debug = None
+
+    @property
+    def tiles(self) -> list:
+        """[(y0, y1, x0, x1, ids)] in row-major tile order (raster.py:252-266)."""
+        if self._tiles is None:
+            W, H = int(self.camera.width), int(self.camera.height)
+            tx_n = math.ceil(W / 16)
+            out = []
+            for t, (s, e) in enumerate(self.tile_ranges):
+                ty, tx = divmod(t, tx_n)
+                out.append((16 * ty, min(16 * ty + 16, H), 16 * tx, min(16 * tx + 16, W),
+                            self.tile_ids[s:e]))
+            self._tiles = out
+        return self._tiles
+
+    def _dump(self):
+        if self._debug is None:
+            ws = workspace(self.precision)
+            ds = _device_scene(self.scene, ws)
+            fr = engine.render_frame(ws, ds, self.camera, self.query, self.settings, want_debug=True)
+            self._debug = ws.debug[:fr.n * DEBUG_STRIDE].view(fr.n, DEBUG_STRIDE).cpu().numpy().copy()
+        return self._debug
+
+    @property
+    def proj(self):
+        d, f = self._dump(), self._flags
+        p2 = np.stack([np.stack([d[:, 3], d[:, 4]], 1), np.stack([d[:, 4], d[:, 5]], 1)], 1)
+        cov2 = np.stack([np.stack([d[:, 10], d[:, 11]], 1), np.stack([d[:, 11], d[:, 12]], 1)], 1)
+        return SimpleNamespace(depth=d[:, 0], mean2=d[:, 1:3], p2=p2, radii=d[:, 6:8], cov2=cov2,
+                               t_cam=d[:, 19:22], visible=(f & F_VISIBLE) != 0,
+                               floored=(f & F_FLOOR2) != 0)
+
+    @property
+    def slices(self):
+        d, f = self._dump(), self._flags
+        c = self.scene.n_dims - 3
+        i = [0, 1, 2, 1, 3, 4, 2, 4, 5]
+        cov3 = d[:, 13:19][:, i].reshape(-1, 3, 3)
+        return SimpleNamespace(valid=(f & F_DEGENERATE) == 0, mean3=d[:, 22:25], cov3=cov3,
+                               gated_opacity=d[:, 8], beta_x=d[:, 9], gate=d[:, 25], opacity=d[:, 26],
+                               s_tanh=d[:, 27:27 + c], floor_eps=d[:, 31], floored=(f & F_FLOOR3) != 0)
+
+    def trace_signature(self) -> tuple:
+        """Discrete branch state (raster.py:81-92)."""
+        c = self.scene.n_dims - 3
+        f = self._flags
+        sgn = np.stack([(f >> (8 + k)) & 1 for k in range(c)], 1).astype(bool) if c else \
+            np.zeros((f.shape[0], 0), bool)
+        return (((f & F_VISIBLE) != 0).tobytes(), ((f & F_FLOOR3) != 0).tobytes(),
+                ((f & F_FLOOR2) != 0).tobytes(), sgn.tobytes(), self.alpha_clamped.tobytes(),
+                self.order.tobytes(), self.processed_pixels)
+
+
+def render_with_cache(scene, cam, query, settings=DEFAULT_SETTINGS, *, precision: str | None = None,
+                      device=None) -> FrameCache:
+    """Full forward pass returning the image plus per-frame state (raster.py:269-316)."""
+    c = scene.n_dims - 3
+    if np.asarray(query.dims).reshape(-1).shape[0] != c:
+        raise ValueError(f"query has {np.asarray(query.dims).size} dims, scene expects {c}")
+    ws = workspace(precision, device)
+    ds = _device_scene(scene, ws)
+    fr = engine.render_frame(ws, ds, cam, query, settings)
+    return FrameCache(scene, cam, query, settings, ws.precision, fr)
+
+
+def render(scene, cam, query, settings=DEFAULT_SETTINGS, *, precision: str | None = None,
+           device=None) -> np.ndarray:
+    """Render to an (H, W, 3) float64 image (raster.py:319-322); not clipped."""
+    c = scene.n_dims - 3
+    if np.asarray(query.dims).reshape(-1).shape[0] != c:
+        raise ValueError(f"query has {np.asarray(query.dims).size} dims, scene expects {c}")
+    ws = workspace(precision, device)
+    ds = _device_scene(scene, ws)
+    fr = engine.render_frame(ws, ds, cam, query, settings)
+    return _host_image(fr, scene.background)

@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Integer outputs (visible set, depth order, per-tile id lists, per-pixel
+contributor counts, alpha_clamped flags, processed_pixels) must be
+bit-exact.  Images: fp64 path <= 1e-12, fp32 path <= 1e-4 max-abs
+(north-star tolerance).  Gradients: SURVEY §8(d) metric (field-norm
+relative <= 1e-3 and per-element <= 1e-3|g| + 1e-3 max|g|).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import ubs_oracle as O
+from paper_2510_03312_b200 import synthetic as S
+from paper_2510_03312_b200.types import DEFAULT_SETTINGS, LossConfig, Query, RenderSettings, Scene, quantize_f32
+
+from .helpers import branch_scene, grad_close, screen_floor_case
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = {"fp64": 1e-12, "fp32": 1e-4}
+
+
+def _render(scene, cam, q, settings, precision):
+    from paper_2510_03312_b200 import raster
+    return raster.render_with_cache(scene, cam, q, settings, precision=precision)
+
+
+def assert_frame_parity(scene, cam, q, settings=DEFAULT_SETTINGS, precision="fp32"):
+    ref = O.render_frame(scene, cam, q, settings)
+    got = _render(scene, cam, q, settings, precision)
+    assert np.array_equal(got.order, ref["order"]), "depth order differs"
+    st, ids = ref["tile_start"], ref["tile_ids"]
+    assert got.tile_ranges.shape[0] == st.size - 1
+    lens = got.tile_ranges[:, 1] - got.tile_ranges[:, 0]
+    assert np.array_equal(lens, np.diff(st)), "per-tile list lengths differ"
+    ne = lens > 0
+    assert np.array_equal(got.tile_ranges[ne, 0], st[:-1][ne]), "tile ranges differ"
+    assert np.array_equal(got.tile_ids, ids), "per-tile id lists differ"
+    assert np.array_equal(got.n_contrib, ref["count"]), \
+        f"contributor counts differ at {int((got.n_contrib != ref['count']).sum())} px"
+    assert np.array_equal(got.alpha_clamped, ref["alpha_clamped"]), "alpha_clamped differs"
+    assert got.processed_pixels == ref["processed_pixels"]
+    tol = IMG_TOL[precision]
+    assert np.abs(got.image - ref["image"]).max() <= tol
+    assert np.abs(got.t_stop - ref["t_stop"]).max() <= tol
+    assert np.abs(got.alpha_sum - ref["alpha_sum"]).max() <= tol
+    return got, ref
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("nd", [3, 6, 7])
+def test_small_scene_parity(nd, precision):
+    # reference tests/test_raster.py:155-162 fixtures
+    sc = quantize_f32(S.random_scene(nd, 60, seed=nd * 3 + 1))
+    cam = S.random_camera(56, nd + 10)
+    q = S.random_query(nd, nd + 20)
+    assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, precision)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_config1_parity(precision):
+    sc = quantize_f32(S.random_scene(7, 10000, seed=1))
+    cam = S.random_camera(128, 2)
+    q = Query.view_time(0.5, cam.forward)
+    assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, precision)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_exact_settings_no_early_out(precision):
+    sc = quantize_f32(S.random_scene(6, 200, seed=11))
+    cam = S.random_camera(48, 12)
+    q = S.random_query(6, 13)
+    assert_frame_parity(sc, cam, q, RenderSettings(transmittance_min=0.0), precision)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_branch_coverage_parity(precision):
+    sc = branch_scene()
+    cam = S.random_camera(96, 3)
+    q = S.random_query(7, 4)
+    got, ref = assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, precision)
+    sl = O.slice_scene(sc, q, DEFAULT_SETTINGS)
+    assert sl["floored"].any() and (~sl["valid"]).any() and ref["alpha_clamped"].any()
+    assert np.array_equal(got.slices.floored, sl["floored"])
+    assert np.array_equal(got.slices.valid, sl["valid"])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_screen_floor_parity(precision):
+    sc, cam, q = screen_floor_case()
+    got, ref = assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, precision)
+    assert ref["proj"]["floored"].any()
+    assert np.array_equal(got.proj.floored, ref["proj"]["floored"])
+
+
+def test_odd_image_size_parity():
+    sc = quantize_f32(S.random_scene(6, 3000, seed=21))
+    from paper_2510_03312_b200.types import Camera
+    cam = Camera.look_at((2.5, 1.0, 0.8), (0, 0, 0), (0, 0, 1), 0.9, 333, 211)
+    q = Query.view(cam.forward)
+    assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, "fp32")
+
+
+def test_intermediates_match_oracle():
+    sc = quantize_f32(S.random_scene(7, 500, seed=3))
+    cam = S.random_camera(64, 4)
+    q = S.random_query(7, 5)
+    got = _render(sc, cam, q, DEFAULT_SETTINGS, "fp64")
+    sl = O.slice_scene(sc, q, DEFAULT_SETTINGS)
+    pr = O.project_scene(sl, cam, DEFAULT_SETTINGS)
+    v = pr["visible"]
+    assert np.array_equal(got.proj.visible, v)
+    for a, b in ((got.proj.mean2, pr["mean2"]), (got.proj.p2, pr["p2"]), (got.proj.depth, pr["depth"]),
+                 (got.slices.gated_opacity, sl["gated_opacity"]), (got.slices.mean3, sl["mean3"]),
+                 (got.slices.cov3, sl["cov3"])):
+        a, b = np.asarray(a)[v], np.asarray(b)[v]
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
+
+
+def test_empty_scene_is_background():
+    from paper_2510_03312_b200 import raster
+    sc = Scene.empty(6, background=(0.1, 0.5, 0.9))
+    img = raster.render(sc, S.random_camera(24, 1), S.random_query(6, 2))
+    assert np.abs(img - np.array([0.1, 0.5, 0.9])).max() == 0.0
+
+
+def test_query_length_mismatch_raises():
+    from paper_2510_03312_b200 import raster
+    sc = S.random_scene(6, 5, seed=1)
+    with pytest.raises(ValueError):
+        raster.render(sc, S.random_camera(16, 1), Query.static())
+
+
+def test_conservation():
+    sc = S.random_scene(6, 50, seed=51)
+    got = _render(sc, S.random_camera(40, 52), S.random_query(6, 53), DEFAULT_SETTINGS, "fp32")
+    assert np.abs(got.alpha_sum + got.t_stop - 1.0).max() <= 1e-5
+
+
+def test_deterministic_forward():
+    sc = S.random_scene(7, 2000, seed=8)
+    cam, q = S.random_camera(96, 9), S.random_query(7, 10)
+    a = _render(sc, cam, q, DEFAULT_SETTINGS, "fp32")
+    b = _render(sc, cam, q, DEFAULT_SETTINGS, "fp32")
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.n_contrib, b.n_contrib)
+
+
+# --- larger sizes: 1080p ------------------------------------------------------
+
+@pytest.mark.slow
+@pytest.mark.parametrize("nd,count", [(7, 100_000), (3, 100_000)])
+def test_1080p_parity(nd, count):
+    sc = S.synth(nd, count, seed=1)
+    cam = S.bench_camera()
+    q = S.bench_query(nd, cam, 0.5)
+    got, _ = assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, "fp32")
+    assert got.n_fixed < 0.02 * cam.width * cam.height
+
+
+# --- gradients ----------------------------------------------------------------
+
+def _frames(scene, size, seed, count):
+    """random_frames (testing.py:55-69) with oracle-rendered targets."""
+    out = []
+    for k in range(count):
+        cam = S.random_camera(size, seed + 11 * k)
+        q = S.random_query(scene.n_dims, seed + 13 * k)
+        other = S.random_scene(scene.n_dims, max(2, scene.n_primitives // 2), seed + 977 + k)
+        tgt = np.clip(O.render_frame(other, cam, q, DEFAULT_SETTINGS)["image"], 0.0, 1.0)
+        out.append((cam, q, tgt))
+    return out
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("nd", [3, 6, 7])
+def test_backward_parity(nd, precision):
+    from paper_2510_03312_b200.gradients import backward
+    sc = quantize_f32(S.random_scene(nd, 60, seed=nd + 40))
+    frames = _frames(sc, 48, seed=nd + 50, count=2)
+    cfg = LossConfig()
+    l_ref, g_ref = O.backward(sc, frames, cfg, DEFAULT_SETTINGS)
+    l_got, g_got = backward(sc, frames, cfg, DEFAULT_SETTINGS, precision=precision)
+    assert abs(l_got - l_ref) <= (1e-10 if precision == "fp64" else 1e-5) * max(1.0, abs(l_ref))
+    bad = grad_close(g_got.arrays(), g_ref, rel=1e-6 if precision == "fp64" else 1e-3)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_backward_config1(precision):
+    from paper_2510_03312_b200.gradients import backward
+    sc = quantize_f32(S.random_scene(7, 10000, seed=1))
+    cam = S.random_camera(128, 2)
+    q = Query.view_time(0.5, cam.forward)
+    other = quantize_f32(S.random_scene(7, 5000, seed=978))
+    tgt = np.clip(O.render_frame(other, cam, q, DEFAULT_SETTINGS)["image"], 0.0, 1.0)
+    frames = [(cam, q, tgt)]
+    l_ref, g_ref = O.backward(sc, frames, LossConfig(), DEFAULT_SETTINGS)
+    l_got, g_got = backward(sc, frames, LossConfig(), DEFAULT_SETTINGS, precision=precision)
+    assert abs(l_got - l_ref) <= 1e-5 * abs(l_ref)
+    bad = grad_close(g_got.arrays(), g_ref, rel=1e-6 if precision == "fp64" else 1e-3)
+    assert not bad, bad
+
+
+def test_backward_branch_coverage():
+    from paper_2510_03312_b200.gradients import backward
+    sc = branch_scene(seed=6, n=200)
+    sc.s_q_raw[200 // 8 * 3] = 0.0  # keep the degenerate row out: it is skipped, not differentiated
+    frames = _frames(sc, 64, seed=70, count=1)
+    l_ref, g_ref = O.backward(sc, frames, LossConfig(), DEFAULT_SETTINGS)
+    l_got, g_got = backward(sc, frames, LossConfig(), DEFAULT_SETTINGS, precision="fp64")
+    bad = grad_close(g_got.arrays(), g_ref, rel=1e-6)
+    assert not bad, bad
+
+
+def test_gradient_error_on_saturated_gate():
+    # tanh saturates -> 0 * inf in the gate adjoint -> GradientError
+    from paper_2510_03312_b200.gradients import backward
+    from paper_2510_03312_b200.types import GradientError
+    sc = S.random_scene(7, 4, seed=2)
+    sc.s_q_raw[0, 0] = np.log(0.01)
+    sc.l_qx[0] = 0.0
+    sc.mu_q[0, 0] = 0.0
+    cam = S.random_camera(32, 3)
+    q = Query.view_time(0.9, cam.forward)
+    tgt = np.zeros((32, 32, 3))
+    with pytest.raises(GradientError):
+        backward(sc, [(cam, q, tgt)], LossConfig(), DEFAULT_SETTINGS)
