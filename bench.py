@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: UBS render throughput on B200 (BASELINE.json config 4).
+
+Workload (one step = one frame): the 7D dynamic UBS scene, 1M primitives
+(``synth(7, 1_000_000, seed=1)``), rendered at 1920x1080 along
+the 300-frame time sweep t = k/299 with the benchmark camera.  The scene is
+resident in HBM; each frame runs preprocess -> depth sort -> tile binning ->
+fp32 raster -> fp64 fix-up, all in libubs_b200.so.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched with torch.distributed.run, one rank per GPU: each rank
+renders its own frames of the sweep (view sharding, no data-path collective);
+time = max over ranks of the CUDA-event time of the K steps.  ``value`` is
+frames/s of the whole job.  ``--impl reference`` times the CPU reference
+algorithm (oracle/ port of betasplat's render path, all host threads) on the
+same workload, rank 0 only.
+
+The JSON line also carries the dominant kernel's roofline (algorithmic bytes
+per launch / CUDA-event launch time vs the measured HBM copy bandwidth), the
+CPU baseline, the end-to-end number through the host-buffer API (image
+copied to pinned host memory every frame), and SM clocks sampled during the
+timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec at 1080p (1M prims, 7D) and train iters/sec; HBM GB/s fraction"
+SWEEP = 300
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-prims", type=int, default=1_000_000)
+    ap.add_argument("--nd", type=int, default=7)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    return ap.parse_args()
+
+
+def workload_config(a):
+    return {"workload": f"config 4: {a.nd}D UBS scene, {a.n_prims} primitives, {a.width}x{a.height}, "
+                        f"{SWEEP}-frame time sweep (one frame per step)",
+            "n_prims": a.n_prims, "n_dims": a.nd, "width": a.width, "height": a.height,
+            "sweep_frames": SWEEP, "scene": "synth(nd, N, seed=1) (SURVEY 8d), float32 records",
+            "l2": "inputs exceed L2: 4*P*N = %.0f MB of primitive records (> 126 MB L2) are re-read every "
+                  "frame; no explicit flush" % (4 * (14 + 6 * (a.nd - 3)) * a.n_prims / 1e6)}
+
+
+def frame_query(nd, cam, k):
+    from paper_2510_03312_b200 import synthetic as S
+    return S.bench_query(nd, cam, (k % SWEEP) / (SWEEP - 1))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.count(",") >= 9]
+        os.unlink(self.f.name)
+        sm = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[6:10]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def physical_gpu_index(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(stage: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(stage)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+def cpu_frames(scene, cam, nd, settings, budget_s, max_frames, warm=True):
+    from oracle import ubs_oracle as O
+    O.set_threads(os.cpu_count() or 1)
+    if warm:
+        small = scene.take(np.arange(min(2000, scene.n_primitives)))
+        O.render_frame(small, cam, frame_query(nd, cam, 0), settings)
+    t0 = time.perf_counter()
+    done = 0
+    while done < max_frames:
+        O.render_frame(scene, cam, frame_query(nd, cam, done * 37), settings)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done, dt
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return None
+    from paper_2510_03312_b200 import synthetic as S
+    from paper_2510_03312_b200.types import DEFAULT_SETTINGS
+    scene = S.synth(a.nd, a.n_prims, seed=1)
+    cam = S.bench_camera(a.width, a.height)
+    cores = os.cpu_count() or 1
+    # warm-up frames (bounded), then the timed steps, all inside the budget
+    cpu_frames(scene, cam, a.nd, DEFAULT_SETTINGS, a.cpu_budget_s / 4, min(a.warmup, 1))
+    done, dt = cpu_frames(scene, cam, a.nd, DEFAULT_SETTINGS, a.cpu_budget_s, a.steps, warm=False)
+    fps = done / dt
+    sample = (f"{done} of {a.steps} requested frames timed (budget {a.cpu_budget_s:.0f} s); oracle port of "
+              f"betasplat render_with_cache: numpy fp64 slice/project + C (OpenMP) build_tiles/tile_forward")
+    return {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": done,
+            "warmup": min(a.warmup, 1), "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(a), "impl": "reference",
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ---------------------------------------------------------------------------
+# ours
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(stage, n, P, n_vis, k, npix, ntiles):
+    """Algorithmic HBM bytes of one launch of each stage."""
+    return {
+        # read params, write key 8 + rect 8 + count 4 + flags 2 + rec32 64 + rec64 80
+        "preprocess": n * (4 * P + 166),
+        # radix sort (key 8 + id 4, one read+write pass), count gather 12, scan 8
+        "bin_depth": n * (24 + 12 + 8),
+        # emit 8 per pair (+ order/offset/rect/count reads 24 per visible), sort pass 16, ranges 4, 8/tile
+        "bin_tiles": k * (8 + 16 + 4) + n_vis * 24 + ntiles * 8,
+        # tile ranges 8/tile, ids 4 per pair, each visible record 64 once, outputs 20 per pixel
+        "raster": ntiles * 8 + 4 * k + 64 * n_vis + 20 * npix,
+        "fixup": 0,
+    }[stage]
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_03312_b200 import engine, synthetic as S
+    from paper_2510_03312_b200.types import DEFAULT_SETTINGS
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    scene = S.synth(a.nd, a.n_prims, seed=1)
+    cam = S.bench_camera(a.width, a.height)
+    dtype = torch.float64 if a.precision == "fp64" else torch.float32
+    ds = engine.DeviceScene.from_scene(scene, dtype=dtype, device=dev)
+    ws = engine.Workspace(dev, a.precision)
+
+    def frame(k, timers=None):
+        return engine.render_frame(ws, ds, cam, frame_query(a.nd, cam, rank + world * k), DEFAULT_SETTINGS,
+                                   timers=timers)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(max(a.warmup, 0)):
+        frame(k)
+    torch.cuda.synchronize()
+
+    # --- device-resident throughput -------------------------------------
+    sampler = ClockSampler(physical_gpu_index(local_rank))
+    time.sleep(0.3)
+    timers = {}
+    stats = {"n_vis": 0, "k": 0}
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(a.steps):
+        fr = frame(k, timers)
+        stats["n_vis"] += fr.n_visible
+        stats["k"] += fr.n_pairs
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    fixed = fr.n_fixed
+    visits = fr.processed_pixels
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * a.steps / (ms_max / 1e3)
+
+    stage_ms = {s: sum(x.elapsed_time(y) for x, y in ev) / len(ev) for s, ev in timers.items()}
+    dominant = max(stage_ms, key=stage_ms.get)
+    n = ds.n
+    P = 14 + 6 * (a.nd - 3)
+    npix = a.width * a.height
+    ntiles = -(-a.width // 16) * -(-a.height // 16)
+    n_vis = stats["n_vis"] / a.steps
+    kk = stats["k"] / a.steps
+    b_dom = algorithmic_bytes(dominant, n, P, n_vis, kk, npix, ntiles)
+    peak, peak_src = measured_peak()
+    achieved = b_dom / (stage_ms[dominant] / 1e3) / 1e9
+    b_frame = n * (4 * P + 64) + 72 * n_vis + 48 * kk + 20 * npix  # SURVEY §8(d) B_fwd
+    traffic = ncu_traffic(dominant)
+
+    # --- end to end: image streamed to pinned host memory every frame -----
+    sink = engine.HostFrameSink(a.height, a.width, dtype=ws.image_buf.dtype, device=dev)
+    for k in range(2):
+        sink.submit(frame(k))
+    sink.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for k in range(a.steps):
+        sink.submit(frame(k))
+    torch.cuda.current_stream().wait_stream(sink.copy_stream)
+    f1.record()
+    torch.cuda.synchronize()
+    barrier()
+    te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * a.steps / (float(te.item()) / 1e3)
+    import ctypes
+    from paper_2510_03312_b200._lib import UbsView
+    h2d = ctypes.sizeof(UbsView)  # camera + query + settings travel as kernel parameters
+
+    # --- CPU baseline (rank 0, N = 1 only) --------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        done, dt = cpu_frames(scene, cam, a.nd, DEFAULT_SETTINGS, 30.0, 1)
+        cpu = {"value": done / dt, "unit": "frames/s", "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"{done} frame(s) of the same sweep on the oracle port (numpy fp64 slice/project, "
+                         f"C OpenMP binning + compositing) with {os.cpu_count()} host threads"}
+
+    if rank != 0:
+        return None
+    per_frame_launches = 7 + 16  # own kernels + CUB sort/scan kernels compiled into libubs_b200.so
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if a.precision == "fp32" else "f64",
+        "precision_note": "fp64 preprocess (slice/project/rect); fp32 raster; pixels with uncertified "
+                          "cut/clamp decisions re-done in fp64 (bit-exact counts)",
+        "data": "synthetic", "config": workload_config(a),
+        "parallelism": f"view sharding over {world} GPU(s), no data-path collective",
+        "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": b_dom, "launch_ms": stage_ms[dominant]},
+        "frame_roofline": {"bytes_per_frame": b_frame, "achieved_gbs": b_frame / (ms_max / a.steps / 1e3) / 1e9,
+                           "frac": b_frame / (ms_max / a.steps / 1e3) / 1e9 / peak,
+                           "ceiling_fps": peak * 1e9 / b_frame},
+        "stage_ms": stage_ms,
+        "per_frame": {"n_visible": n_vis, "tile_pairs": kk, "visits": visits, "fixup_pixels": fixed},
+        "visit_throughput_per_s": visits / (ms_max / a.steps / 1e3),
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": sink.bytes_per_frame,
+                "path": "engine.render_frame + HostFrameSink (fp32 image -> pinned host, copy stream)"},
+        "gpu_launches": per_frame_launches * a.steps,
+        "clocks": clocks,
+    }
+    return out
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        res = run_reference(a, rank, world)
+        print(json.dumps(res), flush=True)
+        return 0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(a, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -173,6 +173,10 @@ int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffer
 int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                        const UbsImageBuffers *ib, ubs_stream_t s);
 
+/* fp64 replay of the pixels the fp32 raster flagged (no-op for the fp64 raster) */
+int ubs_raster_fixup(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                     const UbsImageBuffers *ib, ubs_stream_t s);
+
 /* L1 + SSIM image gradient; loss_parts[0] += sum|diff|, loss_parts[1] += sum ssim_map */
 int ubs_loss_image_grad(const void *image, const void *target, int32_t height, int32_t width,
                         int32_t f64, double lambda_ssim, double scale, void *g_image,

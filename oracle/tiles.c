@@ -31,47 +31,43 @@
 
 /* raster.py:252-266 build_tiles: for every 16x16 tile in row-major order,
  * keep the depth-ordered splats whose [mean2 -/+ radii] box touches the tile
- * (inclusive bounds, last tile clipped to the image).  Two-pass: counts, then
- * fill.  `order` holds visible ids front to back.  Returns total pairs K. */
-int64_t oracle_bin_count(int width, int height, int tile, int64_t n_order, const int64_t *order,
-                         const double *mean2, const double *radii, int64_t *tile_counts) {
+ * (inclusive bounds, last tile clipped to the image).  Same two-level mask as
+ * the reference (row mask, raster.py:260-261, then the column test per tile),
+ * on bounds precomputed in rank order.  `lo`/`hi` are (n_order, 2) rank-
+ * ordered mean2 -/+ radii.  fill == 0: write per-tile counts into `out`,
+ * return K.  fill == 1: write ids (order[r]) at tile_start[t]... into `out`. */
+int64_t oracle_build_tiles(int width, int height, int tile, int64_t n_order, const int64_t *order,
+                           const double *lo, const double *hi, const int64_t *tile_start, int64_t *out,
+                           int fill) {
     int tx_n = (width + tile - 1) / tile, ty_n = (height + tile - 1) / tile;
     int64_t total = 0;
-#pragma omp parallel for schedule(dynamic, 4) reduction(+ : total)
-    for (int t = 0; t < tx_n * ty_n; ++t) {
-        int ty = t / tx_n, tx = t % tx_n;
-        double y0 = (double)(ty * tile), y1 = (double)((ty + 1) * tile < height ? (ty + 1) * tile : height);
-        double x0 = (double)(tx * tile), x1 = (double)((tx + 1) * tile < width ? (tx + 1) * tile : width);
-        int64_t c = 0;
-        for (int64_t r = 0; r < n_order; ++r) {
-            int64_t i = order[r];
-            double mx = mean2[2 * i], my = mean2[2 * i + 1], rx = radii[2 * i], ry = radii[2 * i + 1];
-            double lox = mx - rx, hix = mx + rx, loy = my - ry, hiy = my + ry;
-            if (hiy >= y0 && loy <= y1 && hix >= x0 && lox <= x1) ++c;
+#pragma omp parallel reduction(+ : total)
+    {
+        int64_t *cand = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_order > 0 ? n_order : 1));
+#pragma omp for schedule(dynamic, 1)
+        for (int ty = 0; ty < ty_n; ++ty) {
+            double y0 = (double)(ty * tile), y1 = (double)((ty + 1) * tile < height ? (ty + 1) * tile : height);
+            int64_t nc = 0;
+            for (int64_t r = 0; r < n_order; ++r)
+                if (hi[2 * r + 1] >= y0 && lo[2 * r + 1] <= y1) cand[nc++] = r;
+            for (int tx = 0; tx < tx_n; ++tx) {
+                double x0 = (double)(tx * tile), x1 = (double)((tx + 1) * tile < width ? (tx + 1) * tile : width);
+                int t = ty * tx_n + tx;
+                int64_t c = 0, w = fill ? tile_start[t] : 0;
+                for (int64_t j = 0; j < nc; ++j) {
+                    int64_t r = cand[j];
+                    if (hi[2 * r] >= x0 && lo[2 * r] <= x1) {
+                        if (fill) out[w++] = order[r];
+                        ++c;
+                    }
+                }
+                if (!fill) out[t] = c;
+                total += c;
+            }
         }
-        tile_counts[t] = c;
-        total += c;
+        free(cand);
     }
     return total;
-}
-
-void oracle_bin_fill(int width, int height, int tile, int64_t n_order, const int64_t *order,
-                     const double *mean2, const double *radii, const int64_t *tile_start,
-                     int64_t *tile_ids) {
-    int tx_n = (width + tile - 1) / tile, ty_n = (height + tile - 1) / tile;
-#pragma omp parallel for schedule(dynamic, 4)
-    for (int t = 0; t < tx_n * ty_n; ++t) {
-        int ty = t / tx_n, tx = t % tx_n;
-        double y0 = (double)(ty * tile), y1 = (double)((ty + 1) * tile < height ? (ty + 1) * tile : height);
-        double x0 = (double)(tx * tile), x1 = (double)((tx + 1) * tile < width ? (tx + 1) * tile : width);
-        int64_t w = tile_start[t];
-        for (int64_t r = 0; r < n_order; ++r) {
-            int64_t i = order[r];
-            double mx = mean2[2 * i], my = mean2[2 * i + 1], rx = radii[2 * i], ry = radii[2 * i + 1];
-            double lox = mx - rx, hix = mx + rx, loy = my - ry, hiy = my + ry;
-            if (hiy >= y0 && loy <= y1 && hix >= x0 && lox <= x1) tile_ids[w++] = i;
-        }
-    }
 }
 
 /* _tiles.py:19-56 tile_forward, applied to every tile of the frame.

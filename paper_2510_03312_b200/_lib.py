@@ -77,6 +77,8 @@ SIGNATURES = [
                                 c_void_p]),
     ("ubs_raster_forward", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers),
                                      POINTER(UbsImageBuffers), c_void_p]),
+    ("ubs_raster_fixup", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers),
+                                   POINTER(UbsImageBuffers), c_void_p]),
     ("ubs_loss_image_grad", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_double, c_double,
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
     ("ubs_loss_scratch_bytes", c_size_t, [c_int32, c_int32, c_int32]),

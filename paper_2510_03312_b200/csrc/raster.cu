@@ -489,13 +489,21 @@ extern "C" int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, co
         raster_fwd32_kernel<<<n_tiles, kTileThreads, 0, s>>>(
             P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (float *)ib->image, (float *)ib->alpha_sum,
             (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits, ib->fix_list, ib->fix_count);
-        UBS_CUDA_CHECK();
-        // one pass over the (device-counted) fix-up list; grid sized for the GPU, not the list
-        raster_fixup_kernel<<<148 * 4, 256, 0, s>>>(P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64,
-                                                    ib->fix_list, ib->fix_count, (float *)ib->image,
-                                                    (float *)ib->alpha_sum, (float *)ib->t_stop, ib->n_contrib,
-                                                    ib->hit_clamp, ib->visits);
     }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" int ubs_raster_fixup(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
+                                const UbsImageBuffers *ib, ubs_stream_t stream) {
+    if (!v || !pb || !bb || !ib) return UBS_E_ARGS;
+    if (ib->raster_f64) return UBS_OK;  // nothing to fix: the fp64 raster is the reference arithmetic
+    if (!pb->rec64 || !ib->fix_list || !ib->fix_count) return UBS_E_ARGS;
+    const RasterParams P = make_params(*v);
+    // one pass over the device-counted list; grid sized for the GPU, not the list
+    raster_fixup_kernel<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(
+        P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, ib->fix_list, ib->fix_count, (float *)ib->image,
+        (float *)ib->alpha_sum, (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

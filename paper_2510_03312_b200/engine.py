@@ -274,9 +274,31 @@ def _stream_ptr() -> int:
     return int(torch.cuda.current_stream().cuda_stream)
 
 
+class _Timed:
+    """Records a CUDA event pair around a stage on the current stream when
+    ``timers`` (name -> list of (start, end) events) is given."""
+
+    def __init__(self, timers, name):
+        self.timers, self.name = timers, name
+
+    def __enter__(self):
+        if self.timers is not None:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.a.record()
+
+    def __exit__(self, *exc):
+        if self.timers is not None:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            self.timers.setdefault(self.name, []).append((self.a, b))
+
+
 def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS,
-                 want_debug: bool = False) -> Frame:
-    """Forward one frame on the current stream; returns device views."""
+                 want_debug: bool = False, timers: dict | None = None) -> Frame:
+    """Forward one frame on the current stream; returns device views.
+
+    ``timers``: optional dict collecting per-stage CUDA event pairs
+    ("preprocess", "bin_depth", "bin_tiles", "raster")."""
     lib = ws.lib
     if ds.device != ws.device:
         raise ValueError("scene and workspace live on different devices")
@@ -293,8 +315,10 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     ws.counters.zero_()
     pb = ws.prim_buffers(want_debug)
     if n:
-        check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
-        check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
+        with _Timed(timers, "preprocess"):
+            check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
+        with _Timed(timers, "bin_depth"):
+            check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
     host = ws.counters[:3].cpu()  # the one per-frame sync: K and n_visible
     k = int(host[0])
     n_vis = int(host.view(torch.int32)[4])
@@ -302,9 +326,15 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
         raise _lib.UbsError(f"{k} tile pairs exceed the 2^31 device limit")
     ws.ensure_pairs(k)
     bb = ws.bin_buffers()
-    check(lib.ubs_bin_tiles(v, pb, bb, k, s), "ubs_bin_tiles")
+    with _Timed(timers, "bin_tiles"):
+        check(lib.ubs_bin_tiles(v, pb, bb, k, s), "ubs_bin_tiles")
     ws.hit_clamp[:max(n, 1)].zero_()
-    check(lib.ubs_raster_forward(v, pb, bb, ws.image_buffers(), s), "ubs_raster_forward")
+    ib = ws.image_buffers()
+    with _Timed(timers, "raster"):
+        check(lib.ubs_raster_forward(v, pb, bb, ib, s), "ubs_raster_forward")
+    if not ws.f64:
+        with _Timed(timers, "fixup"):
+            check(lib.ubs_raster_fixup(v, pb, bb, ib, s), "ubs_raster_fixup")
     npix = W * H
     return Frame(view=v, width=W, height=H, n=n, n_visible=n_vis, n_pairs=k,
                  image=ws.image_buf[:npix * 3].view(H, W, 3), alpha_sum=ws.asum_buf[:npix].view(H, W),
@@ -370,3 +400,42 @@ def field_slices(n_dims: int) -> dict:
         out[name] = (slice(off, off + size), shape)
         off += size
     return out
+
+
+class HostFrameSink:
+    """Streams rendered images to pinned host memory on a side stream.
+
+    ``submit(frame)`` snapshots the image on the compute stream (a device
+    copy, so the next frame may reuse the workspace at once) and queues its
+    device->host copy on a copy stream; ``slots`` pinned buffers rotate, a slot
+    is reused only after its previous copy finished.  This is the host-buffer
+    path a sweep user takes: the copy of frame k overlaps the render of k+1.
+    """
+
+    def __init__(self, height: int, width: int, dtype=torch.float32, device="cuda", slots: int = 3):
+        self.dev = torch.device(device)
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.dev_bufs = [torch.empty((height, width, 3), dtype=dtype, device=self.dev) for _ in range(slots)]
+        self.host_bufs = [torch.empty((height, width, 3), dtype=dtype, pin_memory=True) for _ in range(slots)]
+        self.done = [None] * slots
+        self.k = 0
+        self.bytes_per_frame = height * width * 3 * torch.finfo(dtype).bits // 8
+
+    def submit(self, fr: Frame) -> torch.Tensor:
+        i = self.k % len(self.dev_bufs)
+        self.k += 1
+        if self.done[i] is not None:
+            torch.cuda.current_stream().wait_event(self.done[i])
+        self.dev_bufs[i].copy_(fr.image)
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(ready)
+            self.host_bufs[i].copy_(self.dev_bufs[i], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        self.done[i] = ev
+        return self.host_bufs[i]
+
+    def synchronize(self):
+        self.copy_stream.synchronize()

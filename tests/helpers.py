@@ -33,10 +33,13 @@ def grad_close(g, ref, rel=1e-3, floor=1e-3):
     return bad
 
 
-def branch_scene(seed=5, n=400):
+def branch_scene(seed=5, n=400, query=None):
     """SURVEY §8(d) branch-coverage fixture: clamp, PSD floor, screen floor, degenerate rows.
 
-    A 7D scene where blocks of rows exercise each rarely-taken branch."""
+    A 7D scene where blocks of rows exercise each rarely-taken branch.  With
+    ``query`` given, the PSD-floor rows are centred on it (delta = 0) so their
+    sharp query block does not saturate the gate (which would make the
+    reference raise GradientError)."""
     sc = S.random_scene(7, n, seed=seed)
     g = np.random.default_rng(seed + 100)
     k = n // 8
@@ -49,6 +52,8 @@ def branch_scene(seed=5, n=400):
     sc.l_qx[k:2 * k, 1:4, :] = 2.0 * np.eye(3)[None]
     sc.s_q_raw[k:2 * k] = np.log(0.1)
     sc.b_q[k:2 * k] = np.log(5.0)
+    if query is not None:
+        sc.mu_q[k:2 * k] = np.asarray(query.dims)[None, :]
     # thin disks
     sc.s_x_raw[2 * k:3 * k] = np.log(np.array([0.2, 0.2, 1e-7]))
     # degenerate query block

@@ -206,9 +206,11 @@ def test_backward_config1(precision):
 
 def test_backward_branch_coverage():
     from paper_2510_03312_b200.gradients import backward
-    sc = branch_scene(seed=6, n=200)
+    q = S.random_query(7, 70 + 13 * 0)
+    sc = branch_scene(seed=6, n=200, query=q)
     sc.s_q_raw[200 // 8 * 3] = 0.0  # keep the degenerate row out: it is skipped, not differentiated
     frames = _frames(sc, 64, seed=70, count=1)
+    assert O.slice_scene(sc, frames[0][1], DEFAULT_SETTINGS)["floored"].any()
     l_ref, g_ref = O.backward(sc, frames, LossConfig(), DEFAULT_SETTINGS)
     l_got, g_got = backward(sc, frames, LossConfig(), DEFAULT_SETTINGS, precision="fp64")
     bad = grad_close(g_got.arrays(), g_ref, rel=1e-6)
