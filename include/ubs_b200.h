@@ -106,6 +106,7 @@ typedef struct UbsPrimBuffers {
     double *debug;         /* optional n x UBS_DEBUG_STRIDE f64 dump of intermediates, or NULL */
     uint32_t *n_visible;   /* [1] += number of visible primitives (caller zeroes) */
     unsigned long long *n_pairs; /* [1] += total tile pairs K (caller zeroes) */
+    int32_t *tile_grid;    /* (TY+1) x (TX+1) 2D difference array of rect corners (zeroed by ubs_preprocess) */
 } UbsPrimBuffers;
 
 /* debug row: 0 depth | 1-2 mean2 | 3-5 p2 00,01,11 | 6-7 radii | 8 gated opacity | 9 beta_x |
@@ -163,9 +164,10 @@ int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec3
 
 /* CUB scratch bytes needed for n primitives, pair capacity and tile count */
 size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
-/* depth sort (stable on id) and rank-ordered exclusive scan of tile counts */
+/* depth sort (stable on id), rank-ordered exclusive scan of tile counts, and the
+ * per-tile [start, end) ranges from the corner difference array */
 int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb, ubs_stream_t s);
-/* emit (tile, id) pairs in rank order, stable sort on tile bits, per-tile ranges */
+/* emit (tile, id) pairs in rank order, stable sort on tile bits */
 int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                   int64_t n_pairs, ubs_stream_t s);
 

@@ -44,7 +44,7 @@ class UbsView(Structure):
 class UbsPrimBuffers(Structure):
     _fields_ = [("depth_key", c_void_p), ("rect", c_void_p), ("tile_count", c_void_p), ("flags", c_void_p),
                 ("rec32", c_void_p), ("rec64", c_void_p), ("debug", c_void_p), ("n_visible", c_void_p),
-                ("n_pairs", c_void_p)]
+                ("n_pairs", c_void_p), ("tile_grid", c_void_p)]
 
 
 class UbsBinBuffers(Structure):

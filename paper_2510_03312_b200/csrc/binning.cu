@@ -12,7 +12,9 @@
 //   4. stable radix sort on the tile bits only (ceil(log2 n_tiles) bits, two
 //      8-bit digit passes at 1080p): since emission is already rank ordered,
 //      this equals a full (tile, rank) sort.
-//   5. [start, end) per tile from the sorted keys.
+//   5. [start, end) per tile without touching the pairs: the preprocess
+//      kernel adds each visible rect's corners to a 2D difference array, whose
+//      prefix sums are the per-tile counts (tile_scan_kernel).
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -63,20 +65,77 @@ __global__ void emit_pairs_kernel(const uint32_t *__restrict__ order, const uint
         const uint32_t tx0 = (uint32_t)(q & 0xFFFF), ty0 = (uint32_t)((q >> 16) & 0xFFFF);
         const uint32_t tx1 = (uint32_t)((q >> 32) & 0xFFFF);
         const uint32_t w = tx1 - tx0 + 1;
+        // floor((k + 0.5) / w) in fp32 is exact here: (k + 0.5)/w is >= 0.5/w
+        // away from an integer, far more than the rounding of two fp32 ops
+        const float inv_w = 1.0f / (float)w;
         for (uint32_t k = lane; k < c; k += 32) {
-            const uint32_t ty = ty0 + k / w, tx = tx0 + k % w;
+            const uint32_t dy = (uint32_t)(((float)k + 0.5f) * inv_w);
+            const uint32_t ty = ty0 + dy, tx = tx0 + (k - dy * w);
             pair_keys[o + k] = ty * (uint32_t)tiles_x + tx;
             pair_vals[o + k] = pid;
         }
     }
 }
 
-__global__ void tile_ranges_kernel(const uint32_t *__restrict__ keys, int64_t k_total, uint32_t *__restrict__ ranges) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= k_total) return;
-    const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[2 * (int64_t)k] = (uint32_t)i;
-    if (i == k_total - 1 || keys[i + 1] != k) ranges[2 * (int64_t)k + 1] = (uint32_t)(i + 1);
+// Per-tile [start, end) from the rect-corner difference array (one CTA):
+// row prefix, column prefix -> per-tile pair counts, then an exclusive scan
+// in row-major tile order.  Equals the ranges of the tile-sorted pair array
+// because every visible primitive contributes exactly its rect.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads)
+tile_scan_kernel(int32_t *__restrict__ grid, int TX, int TY, uint32_t *__restrict__ ranges) {
+    const int gw = TX + 1;
+    for (int r = threadIdx.x; r <= TY; r += kScanThreads) {
+        int acc = 0;
+        for (int c = 0; c <= TX; ++c) {
+            acc += grid[r * gw + c];
+            grid[r * gw + c] = acc;
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c <= TX; c += kScanThreads) {
+        int acc = 0;
+        for (int r = 0; r <= TY; ++r) {
+            acc += grid[r * gw + c];
+            grid[r * gw + c] = acc;
+        }
+    }
+    __syncthreads();
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int n_tiles = TX * TY;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < n_tiles; base += kScanThreads) {
+        const int t = base + threadIdx.x;
+        uint32_t c = 0;
+        if (t < n_tiles) c = (uint32_t)grid[(t / TX) * gw + (t % TX)];
+        uint32_t x = c;  // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = warp_tot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_tot[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - c;
+        if (t < n_tiles) {
+            ranges[2 * t] = excl;
+            ranges[2 * t + 1] = excl + c;
+        }
+        __syncthreads();
+        if (threadIdx.x == kScanThreads - 1) carry = excl + c;
+        __syncthreads();
+    }
 }
 
 static int tile_bits(int n_tiles) {
@@ -105,11 +164,16 @@ extern "C" size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n
 
 extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                              ubs_stream_t stream) {
-    if (!v || !pb || !bb || !bb->temp) return UBS_E_ARGS;
+    if (!v || !pb || !bb || !bb->temp || !pb->tile_grid || !bb->tile_ranges) return UBS_E_ARGS;
     const int64_t n = v->n;
-    if (n == 0) return UBS_OK;
     if (n >= (int64_t)1 << 31) return UBS_E_ARGS;
     cudaStream_t s = (cudaStream_t)stream;
+    const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
+    tile_scan_kernel<<<1, kScanThreads, 0, s>>>(pb->tile_grid, TX, TY, bb->tile_ranges);
+    if (n == 0) {
+        UBS_CUDA_CHECK();
+        return UBS_OK;
+    }
     const int thr = 256;
     const unsigned blocks = (unsigned)((n + thr - 1) / thr);
     iota_kernel<<<blocks, thr, 0, s>>>(bb->ids_iota, n);
@@ -133,8 +197,6 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
     const int n_tiles = TX * TY;
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(bb->tile_ranges, 0, sizeof(uint32_t) * 2 * (size_t)n_tiles, s) != cudaSuccess)
-        return UBS_E_CUDA;
     if (n_pairs == 0 || v->n == 0) return UBS_OK;
     if (n_pairs > bb->pair_capacity || n_pairs >= ((int64_t)1 << 31)) return UBS_E_CAPACITY;
     const int64_t n = v->n;
@@ -147,8 +209,6 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
                                         bb->tile_ids, (int)n_pairs, 0, tile_bits(n_tiles > 1 ? n_tiles : 2),
                                         s) != cudaSuccess)
         return UBS_E_CUDA;
-    tile_ranges_kernel<<<(unsigned)((n_pairs + thr - 1) / thr), thr, 0, s>>>(bb->pair_keys_sorted, n_pairs,
-                                                                             bb->tile_ranges);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

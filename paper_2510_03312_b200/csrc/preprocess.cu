@@ -59,6 +59,12 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
                     uint64_t a = (uint64_t)tx0, b = (uint64_t)ty0, c = (uint64_t)tx1, d = (uint64_t)ty1;
                     rect = a | (b << 16) | (c << 32) | (d << 48);
                     count = (uint32_t)((c - a + 1) * (d - b + 1));
+                    // 2D difference array: a prefix sum over it gives every tile's pair count
+                    const int gw = TX + 1;
+                    atomicAdd(pb.tile_grid + (int)b * gw + (int)a, 1);
+                    atomicAdd(pb.tile_grid + (int)b * gw + (int)c + 1, -1);
+                    atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)a, -1);
+                    atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)c + 1, 1);
                 }
             }
         }
@@ -100,7 +106,10 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
                                (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
             r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)g.og);
             r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
-            r.r3 = make_float4((float)eb, (float)E, 0.f, 0.f);
+            // r3: eb (m-error bound times beta), tau + E (support-edge band),
+            //     qc (lg2/ex2 approximation error of the alpha, relative), log2(og)
+            const double qc = 0.6931471805599453 * g.beta_x * 4.76837158203125e-07 + 5.0e-7;
+            r.r3 = make_float4((float)eb, (float)(v.set.tau_sq + E), (float)qc, (float)log2(g.og));
             reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
         }
         pb.flags[i] = fl;
@@ -163,8 +172,14 @@ extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_
     if (v->n < 0 || (v->n > 0 && !v->params)) return UBS_E_ARGS;
     if (!pb->depth_key || !pb->rect || !pb->tile_count || !pb->flags) return UBS_E_ARGS;
     if (!pb->rec64 && !(want_rec32 && pb->rec32)) return UBS_E_ARGS;
-    if (v->n == 0) return UBS_OK;
+    if (!pb->tile_grid) return UBS_E_ARGS;
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
+        if (cudaMemsetAsync(pb->tile_grid, 0, sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1), s) != cudaSuccess)
+            return UBS_E_CUDA;
+    }
+    if (v->n == 0) return UBS_OK;
     const bool f64 = v->param_f64 != 0;
     switch (v->n_dims) {
         case 3: f64 ? launch_pre<0, double>(*v, *pb, want_rec32, s)

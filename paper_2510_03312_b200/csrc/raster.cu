@@ -136,6 +136,30 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 // edge), the image tolerance itself is asserted by the parity tests.
 constexpr float kImgErrTol = 1.0e-3f;
 
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per visit (in support): alpha = 2^(beta * lg2(1 - m/tau) + log2(og)) with
+// the MUFU lg2/ex2 approximations; their error (qc, and 1.2e-7 per unit of
+// the exponent) is part of the per-visit relative alpha bound
+//     q = eb / (tau - m) + qc + 1.2e-7 |arg|,
+// and err accumulates q * a / (1 - a), the first-order relative error of T.
+// Near the cut (T < tmin * (1 + 4e-3)) the exact band test runs; elsewhere a
+// single compare.  A pixel whose bound exceeds kImgErrTol is flagged anyway,
+// so the coarse prefilter width can never hide a needed band test.
 __global__ void __launch_bounds__(kTileThreads)
 raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, float *__restrict__ image, float *__restrict__ asum,
@@ -154,6 +178,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
     const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
     const float tmin = (float)P.tmin;
+    const float tmin_hi = tmin * (1.0f + 4.0e-3f);
     float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
     float err = 0.f;  // bound on |T32 - T64| / T
     int cnt = 0;
@@ -175,13 +200,15 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         const int nb = (int)min((uint32_t)kTileThreads, end - b);
         if (!done) {
             for (int j = 0; j < nb; ++j) {
-                const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
-                if (T < tmin) {
-                    if (T > tmin * (1.0f - band)) flag = true;
-                    done = true;
-                    break;
+                if (T < tmin_hi) {
+                    const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
+                    if (T < tmin) {
+                        if (T > tmin * (1.0f - band)) flag = true;
+                        done = true;
+                        break;
+                    }
+                    if (T < tmin * (1.0f + band)) flag = true;
                 }
-                if (T < tmin * (1.0f + band)) flag = true;
                 ++cnt;
                 const float4 r0 = s0[j], r1 = s1[j];
                 const float dx = (float)(px - __float_as_int(r0.x)) + r0.z;
@@ -189,14 +216,15 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 const float y0 = fmaf(r1.x, dx, r1.y * dy);
                 const float y1 = r1.z * dy;
                 const float m = fmaf(y0, y0, y1 * y1);
+                const float4 r3 = s3[j];
                 if (m >= tau) {
-                    if (m < tau + s3[j].y) flag = true;  // support edge not certain
+                    if (m < r3.y) flag = true;  // support edge within the m-error band
                     continue;
                 }
                 const float4 r2 = s2[j];
-                const float lg = r2.x * log1pf(-m * inv_tau);
-                float a = r1.w * __expf(lg);
-                const float qrel = __fdividef(s3[j].x, tau - m) + 2.5e-7f * (2.0f - lg);
+                const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
+                float a = ex2_approx(arg);
+                const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 1.2e-7f, r3.z));
                 float om;
                 if (a > clamp) {
                     if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
@@ -207,7 +235,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     if (a * (1.0f + qrel) > clamp) flag = true;
                     om = 1.0f - a;
                 }
-                err += __fdividef(a * qrel, om) + 6.0e-8f;
+                err = fmaf(a * qrel, rcp_approx(om), err + 6.0e-8f);
                 const float w = a * T;
                 a0 = fmaf(w, r2.y, a0);
                 a1 = fmaf(w, r2.z, a1);
@@ -224,7 +252,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         }
     }
     if (inside && !done && T < tmin * (1.0f + fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f))) flag = true;
-    if (err > kImgErrTol) flag = flag || inside;
+    if (err > kImgErrTol) flag = true;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);

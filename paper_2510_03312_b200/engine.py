@@ -165,6 +165,7 @@ class Workspace:
         self.counters = torch.zeros(8, dtype=torch.int64, device=self.device)
         self.counters32 = self.counters.view(torch.int32)
         self.debug = None
+        self.tile_grid = None
         self.grad2d = None
         self.loss_scratch = None
         self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
@@ -206,6 +207,9 @@ class Workspace:
             self.g_image_buf = self._i(cap * 3, fdt)
             self.loss_scratch = None
             self.pix_cap = cap
+        grid = (math.ceil(width / TILE) + 1) * (math.ceil(height / TILE) + 1)
+        if self.tile_grid is None or self.tile_grid.numel() < grid:
+            self.tile_grid = self._i(grid, torch.int32)
         if ntiles > self.tile_cap:
             self.tile_ranges = self._i(2 * ntiles, torch.int32)
             self.tile_cap = ntiles
@@ -237,6 +241,7 @@ class Workspace:
         pb.debug = _ptr(self.debug) if want_debug else 0
         pb.n_visible = _ptr(self.counters) + 16
         pb.n_pairs = _ptr(self.counters)
+        pb.tile_grid = _ptr(self.tile_grid)
         return pb
 
     def bin_buffers(self) -> UbsBinBuffers:
@@ -314,11 +319,10 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     s = _stream_ptr()
     ws.counters.zero_()
     pb = ws.prim_buffers(want_debug)
-    if n:
-        with _Timed(timers, "preprocess"):
-            check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
-        with _Timed(timers, "bin_depth"):
-            check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
+    with _Timed(timers, "preprocess"):
+        check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
+    with _Timed(timers, "bin_depth"):
+        check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
     host = ws.counters[:3].cpu()  # the one per-frame sync: K and n_visible
     k = int(host[0])
     n_vis = int(host.view(torch.int32)[4])
