@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step measurement")
+    ap.add_argument("--train-prims", type=int, default=3_000_000)
+    ap.add_argument("--train-views-per-gpu", type=int, default=8)
+    ap.add_argument("--train-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -197,6 +201,58 @@ def algorithmic_bytes(stage, n, P, n_vis, k, npix, ntiles):
     }[stage]
 
 
+def run_train(a, rank, world, local_rank):
+    """Config 5: 7D training step, 3M prims, batch = 8 views per GPU (1080p orbit),
+    views sharded over ranks, one NCCL all-reduce of the flat gradient, device Adam."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_03312_b200 import engine, sharding, synthetic as S
+    from paper_2510_03312_b200.types import LossConfig
+
+    dev = torch.device("cuda", local_rank)
+    scene = S.synth(7, a.train_prims, seed=1)
+    ds = engine.DeviceScene.from_scene(scene, dtype=torch.float32, device=dev)
+    batch = a.train_views_per_gpu * world
+    cams = [S.bench_camera(a.width, a.height, k, batch) for k in range(batch)]
+    views_q = [S.bench_query(7, c, 0.5) for c in cams]
+    # targets: renders of synth(7, N, seed=2) (SURVEY 8d), made on this GPU, then resident
+    tds = engine.DeviceScene.from_scene(S.synth(7, a.train_prims, seed=2), dtype=torch.float32, device=dev)
+    tws = engine.Workspace(dev, "fp32")
+    targets = []
+    for c, q in zip(cams, views_q):
+        targets.append(engine.render_frame(tws, tds, c, q).image.clone().clamp_(0.0, 1.0))
+    del tws, tds
+    views = list(zip(cams, views_q, targets))
+    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32"))
+    adam = sharding.DeviceAdam(ds.params, 7)
+    cfg = LossConfig()
+    grad = step.backend.new_grad()
+    for _ in range(2):
+        loss, grad = step.loss_and_grad(views, cfg, grad)
+        adam.step(grad)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.train_steps):
+        loss, grad = step.loss_and_grad(views, cfg, grad)
+        adam.step(grad)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / a.train_steps
+    return {"metric": "train iters/sec", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
+            "views_per_s": batch * 1e3 / ms, "loss": float(loss),
+            "config": {"workload": f"config 5: 7D UBS training step, {a.train_prims} primitives, batch {batch} "
+                                   f"1920x1080 orbit views ({a.train_views_per_gpu} per GPU), fwd + L1/SSIM + bwd "
+                                   f"+ all-reduce + Adam", "parallelism": f"dp{world} (view sharding, NCCL "
+                                   f"all-reduce of the {4 * 38 * a.train_prims / 1e6:.0f} MB gradient)"},
+            "steps": a.train_steps, "warmup": 2, "dtype": "f32 (fp64 geometry/chain)", "data": "synthetic"}
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -294,6 +350,12 @@ def run_ours(a, rank, world, local_rank):
                "sample": f"{done} frame(s) of the same sweep on the oracle port (numpy fp64 slice/project, "
                          f"C OpenMP binning + compositing) with {os.cpu_count()} host threads"}
 
+    train = None
+    if not a.no_train:
+        del ws
+        torch.cuda.empty_cache()
+        train = run_train(a, rank, world, local_rank)
+
     if rank != 0:
         return None
     per_frame_launches = 7 + 16  # own kernels + CUB sort/scan kernels compiled into libubs_b200.so
@@ -320,6 +382,7 @@ def run_ours(a, rank, world, local_rank):
                 "path": "engine.render_frame + HostFrameSink (fp32 image -> pinned host, copy stream)"},
         "gpu_launches": per_frame_launches * a.steps,
         "clocks": clocks,
+        "train": train,
     }
     return out
 

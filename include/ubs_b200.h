@@ -192,6 +192,19 @@ int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBin
 /* chain 2D gradients back to raw parameters (fp64), += into grad_params */
 int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int32_t add_regularisers, ubs_stream_t s);
 
+/* --- training-step epilogue (optim.py:115-135, gradients.py:120-123) --- */
+
+/* Adam on the flat n x (14+6C) record buffer; lr_group = {position, opacity,
+ * scale, other}; b_x/b_q clamped to [-5, 5]; m, v are f32 moments (zeroed by
+ * the caller before step 1); step is the 1-based Adam step count. */
+int ubs_adam_step(void *params, int32_t param_f64, const void *grads, int32_t grad_f64, float *m, float *v,
+                  int64_t n, int32_t n_dims, const double *lr_group, int32_t step, int32_t freeze_shapes,
+                  ubs_stream_t s);
+
+/* regulariser gradients, once per step (also fused into ubs_prim_backward) */
+int ubs_add_regularisers(const void *params, int32_t param_f64, void *grads, int32_t grad_f64, int64_t n,
+                         int32_t n_dims, double reg_opacity, double reg_scale, ubs_stream_t s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,10 @@ SIGNATURES = [
     ("ubs_raster_backward", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers),
                                       POINTER(UbsImageBuffers), POINTER(UbsGradBuffers), c_void_p]),
     ("ubs_prim_backward", c_int32, [POINTER(UbsView), POINTER(UbsGradBuffers), c_int32, c_void_p]),
+    ("ubs_adam_step", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_int64, c_int32,
+                                POINTER(c_double), c_int32, c_int32, c_void_p]),
+    ("ubs_add_regularisers", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_int32, c_double,
+                                       c_double, c_void_p]),
 ]
 
 _LIB = None

@@ -1,0 +1,128 @@
+// Training-step epilogue on the flat (n x P) parameter buffer.
+//
+// Reference: optim.py:115-135 (adam_step: bias-corrected Adam, per-field
+// learning-rate group, shapes clamped to [-5, 5] after the update,
+// kernels.py:57-60) and gradients.py:120-123 (regularisers, added once per
+// step).  One fused elementwise pass: read param/grad/m/v, write param/m/v;
+// memory bound (16-32 B per element).
+#include <cuda_runtime.h>
+
+#include "ubs_common.cuh"
+
+namespace ubs {
+
+struct AdamCols {
+    float lr[64];          // learning rate of each record column
+    uint64_t clamp_mask;   // columns clamped to [-5, 5] after the step (b_x, b_q)
+    uint64_t frozen_mask;  // columns not updated (freeze_shapes)
+};
+
+template <typename PT, typename GT>
+__global__ void adam_kernel(PT *__restrict__ params, const GT *__restrict__ grads, float *__restrict__ m,
+                            float *__restrict__ v, int64_t total, int P, AdamCols cols, float b1, float b2,
+                            float bc1, float bc2, float eps) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % P);
+        if ((cols.frozen_mask >> c) & 1ull) {
+            // frozen shapes are not updated but still clamped (optim.py:122-135)
+            params[i] = (PT)fmin(fmax((double)params[i], -5.0), 5.0);
+            continue;
+        }
+        const float g = (float)grads[i];
+        const float mi = b1 * m[i] + (1.0f - b1) * g;
+        const float vi = b2 * v[i] + (1.0f - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        double p = (double)params[i] - (double)cols.lr[c] * ((double)mi / bc1) / (sqrt((double)vi / bc2) + eps);
+        if ((cols.clamp_mask >> c) & 1ull) p = fmin(fmax(p, -5.0), 5.0);
+        params[i] = (PT)p;
+    }
+}
+
+// g_opacity_raw += reg_o * o (1 - o); g_s_x_raw += reg_s exp(s_x_raw); g_s_q_raw += reg_s exp(s_q_raw)
+template <typename PT, typename GT>
+__global__ void regulariser_kernel(const PT *__restrict__ params, GT *__restrict__ grads, int64_t n, int C,
+                                   double reg_o, double reg_s) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int P = 14 + 6 * C;
+    const PT *r = params + i * P;
+    GT *g = grads + i * P;
+    const int o_sx = 3 + C + 3, o_sq = o_sx + 3 + 3 * C, o_op = o_sq + C + 1 + C;
+    const double o = sigmoid64((double)r[o_op]);
+    g[o_op] = (GT)((double)g[o_op] + reg_o * o * (1.0 - o));
+    for (int k = 0; k < 3; ++k) g[o_sx + k] = (GT)((double)g[o_sx + k] + reg_s * exp((double)r[o_sx + k]));
+    for (int k = 0; k < C; ++k) g[o_sq + k] = (GT)((double)g[o_sq + k] + reg_s * exp((double)r[o_sq + k]));
+}
+
+}  // namespace ubs
+
+using namespace ubs;
+
+// lr_group: [position, opacity, scale, other] (optim.py:77-89)
+extern "C" int ubs_adam_step(void *params, int32_t param_f64, const void *grads, int32_t grad_f64, float *m,
+                             float *v, int64_t n, int32_t n_dims, const double *lr_group, int32_t step,
+                             int32_t freeze_shapes, ubs_stream_t stream) {
+    if (!params || !grads || !m || !v || !lr_group || step < 1) return UBS_E_ARGS;
+    if (n_dims != 3 && n_dims != 6 && n_dims != 7) return UBS_E_ARGS;
+    if (n == 0) return UBS_OK;
+    const int C = n_dims - 3, P = 14 + 6 * C;
+    AdamCols cols{};
+    // column -> learning-rate group, PARAM_FIELDS order
+    int c = 0;
+    auto put = [&](int count, double lr, bool clampc) {
+        for (int k = 0; k < count; ++k, ++c) {
+            cols.lr[c] = (float)lr;
+            if (clampc) {
+                cols.clamp_mask |= 1ull << c;
+                if (freeze_shapes) cols.frozen_mask |= 1ull << c;
+            }
+        }
+    };
+    const double pos = lr_group[0], opa = lr_group[1], scl = lr_group[2], oth = lr_group[3];
+    put(3, pos, false);      // mu_x
+    put(C, oth, false);      // mu_q
+    put(3, oth, false);      // rot
+    put(3, scl, false);      // s_x_raw
+    put(3 * C, oth, false);  // l_qx
+    put(C, scl, false);      // s_q_raw
+    put(1, oth, true);       // b_x
+    put(C, oth, true);       // b_q
+    put(1, opa, false);      // opacity_raw
+    put(3, oth, false);      // color
+    const float b1 = 0.9f, b2 = 0.999f;
+    const float bc1 = (float)(1.0 - pow(0.9, step)), bc2 = (float)(1.0 - pow(0.999, step));
+    const int64_t total = n * P;
+    const int thr = 256;
+    const int64_t want = (total + thr - 1) / thr;
+    const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (param_f64) {
+        if (grad_f64) adam_kernel<double, double><<<blocks, thr, 0, s>>>((double *)params, (const double *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
+        else adam_kernel<double, float><<<blocks, thr, 0, s>>>((double *)params, (const float *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
+    } else {
+        if (grad_f64) adam_kernel<float, double><<<blocks, thr, 0, s>>>((float *)params, (const double *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
+        else adam_kernel<float, float><<<blocks, thr, 0, s>>>((float *)params, (const float *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" int ubs_add_regularisers(const void *params, int32_t param_f64, void *grads, int32_t grad_f64, int64_t n,
+                                    int32_t n_dims, double reg_opacity, double reg_scale, ubs_stream_t stream) {
+    if (!params || !grads) return UBS_E_ARGS;
+    if (n_dims != 3 && n_dims != 6 && n_dims != 7) return UBS_E_ARGS;
+    if (n == 0) return UBS_OK;
+    const int C = n_dims - 3;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (param_f64) {
+        if (grad_f64) regulariser_kernel<double, double><<<blocks, 256, 0, s>>>((const double *)params, (double *)grads, n, C, reg_opacity, reg_scale);
+        else regulariser_kernel<double, float><<<blocks, 256, 0, s>>>((const double *)params, (float *)grads, n, C, reg_opacity, reg_scale);
+    } else {
+        if (grad_f64) regulariser_kernel<float, double><<<blocks, 256, 0, s>>>((const float *)params, (double *)grads, n, C, reg_opacity, reg_scale);
+        else regulariser_kernel<float, float><<<blocks, 256, 0, s>>>((const float *)params, (float *)grads, n, C, reg_opacity, reg_scale);
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}

@@ -1,0 +1,148 @@
+"""View-batch data parallelism across GPUs.
+
+Views (camera, query[, target]) are independent units.  Rendering a batch of
+views shards them round-robin over ranks with no communication.  A training
+step shards the batch the same way; every rank accumulates the raw-parameter
+gradient of its views (each scaled by loss_scale / B, gradients.py:114-116)
+into one flat n x (14+6C) buffer, then a single all-reduce(sum) over NCCL
+(NVLink/NVSwitch) combines them.  Regulariser gradients are added exactly
+once (by rank 0, before the reduce, gradients.py:120-123) and the scalar
+loss is all-reduced alongside.  The optimizer (device Adam,
+optim.py:115-135) then runs identically on every rank, keeping the
+replicated scene in sync without a broadcast.
+
+The per-view work is done by a backend object; ``GpuViewBackend`` drives
+libubs_b200.so.  (Tests substitute a CPU backend to check the reduction
+logic with world_size 2 over gloo; the product path only ever uses the GPU
+backend.)
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib, engine
+from .types import DEFAULT_SETTINGS, LossConfig
+
+
+def shard(items, rank: int, world: int) -> list:
+    """Round-robin share of ``items`` for ``rank``."""
+    return list(items)[rank::world]
+
+
+def dist_rank_world(group=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+class GpuViewBackend:
+    """Per-view loss + gradient on this rank's GPU through the C-ABI engine."""
+
+    def __init__(self, ds: engine.DeviceScene, precision: str = "fp32", settings=DEFAULT_SETTINGS,
+                 grad_dtype=torch.float32):
+        self.ds = ds
+        self.ws = engine.Workspace(ds.device, precision)
+        self.settings = settings
+        self.grad_dtype = grad_dtype
+
+    def new_grad(self) -> torch.Tensor:
+        return torch.zeros(self.ds.params.shape, dtype=self.grad_dtype, device=self.ds.device)
+
+    def view_loss_grad(self, cam, query, target: torch.Tensor, cfg: LossConfig, scale: float,
+                       grad: torch.Tensor) -> torch.Tensor:
+        """Adds this view's d(loss)/d(params) into ``grad``; returns the view's
+        reconstruction term (1-l) L1 + l (1 - SSIM) as a 0-d device tensor."""
+        fr = engine.render_frame(self.ws, self.ds, cam, query, self.settings)
+        self.ws.loss_parts.zero_()
+        g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
+        engine.backward_frame(fr, self.ds, g_img, grad)
+        size = fr.width * fr.height * 3
+        return (1.0 - cfg.lambda_ssim) * parts[0] / size + cfg.lambda_ssim * (1.0 - parts[1] / size)
+
+    def add_regularisers(self, grad: torch.Tensor, cfg: LossConfig):
+        lib = _lib.load()
+        p = self.ds.params
+        _lib.check(lib.ubs_add_regularisers(p.data_ptr(), int(p.dtype == torch.float64), grad.data_ptr(),
+                                            int(grad.dtype == torch.float64), self.ds.n, self.ds.n_dims,
+                                            cfg.loss_scale * cfg.lambda_o, cfg.loss_scale * cfg.lambda_sigma,
+                                            torch.cuda.current_stream().cuda_stream), "ubs_add_regularisers")
+
+    def regulariser_value(self, cfg: LossConfig) -> torch.Tensor:
+        sl = engine.field_slices(self.ds.n_dims)
+        p = self.ds.params.double()
+        o = torch.sigmoid(p[:, sl["opacity_raw"][0]]).sum()
+        sc = torch.exp(p[:, sl["s_x_raw"][0]]).sum() + torch.exp(p[:, sl["s_q_raw"][0]]).sum()
+        return cfg.lambda_o * o + cfg.lambda_sigma * sc
+
+
+class ViewShardedStep:
+    """loss + all-reduced gradient of a batch of views, views sharded over ranks."""
+
+    def __init__(self, backend, group=None):
+        self.backend = backend
+        self.group = group
+
+    def loss_and_grad(self, views, cfg: LossConfig = LossConfig(), grad: torch.Tensor | None = None):
+        if not views:
+            raise ValueError("empty batch")
+        rank, world = dist_rank_world(self.group)
+        b = self.backend
+        grad = b.new_grad() if grad is None else grad.zero_()
+        scale = cfg.loss_scale / len(views)
+        rec = torch.zeros((), dtype=torch.float64, device=grad.device)
+        for cam, query, target in shard(views, rank, world):
+            rec = rec + b.view_loss_grad(cam, query, target, cfg, scale, grad)
+        if rank == 0:
+            b.add_regularisers(grad, cfg)
+        allreduce_sum_(grad, self.group)
+        rec = allreduce_sum_(rec.reshape(1), self.group)[0]
+        loss = cfg.loss_scale * (rec / len(views) + b.regulariser_value(cfg))
+        return loss, grad
+
+
+class DeviceAdam:
+    """Bias-corrected Adam on the flat record buffer (optim.py:115-135), f32 moments."""
+
+    def __init__(self, params: torch.Tensor, n_dims: int, lr_position=1.6e-4, lr_opacity=5e-2, lr_scale=5e-3,
+                 lr_other=1e-3, freeze_shapes=False):
+        self.params = params
+        self.n_dims = n_dims
+        self.m = torch.zeros(params.shape, dtype=torch.float32, device=params.device)
+        self.v = torch.zeros(params.shape, dtype=torch.float32, device=params.device)
+        self.lr = (ctypes.c_double * 4)(lr_position, lr_opacity, lr_scale, lr_other)
+        self.freeze = 1 if freeze_shapes else 0
+        self.step_count = 0
+
+    def step(self, grad: torch.Tensor):
+        self.step_count += 1
+        lib = _lib.load()
+        _lib.check(lib.ubs_adam_step(self.params.data_ptr(), int(self.params.dtype == torch.float64),
+                                     grad.data_ptr(), int(grad.dtype == torch.float64), self.m.data_ptr(),
+                                     self.v.data_ptr(), int(self.params.shape[0]), self.n_dims, self.lr,
+                                     self.step_count, self.freeze, torch.cuda.current_stream().cuda_stream),
+                   "ubs_adam_step")
+
+
+def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=DEFAULT_SETTINGS, group=None,
+                 sink: engine.HostFrameSink | None = None):
+    """Forward-render this rank's share of ``views`` [(cam, query), ...]; no
+    communication.  Returns the number of frames rendered by this rank."""
+    rank, world = dist_rank_world(group)
+    k = 0
+    for cam, query in shard(views, rank, world):
+        fr = engine.render_frame(ws, ds, cam, query, settings)
+        if sink is not None:
+            sink.submit(fr)
+        k += 1
+    return k
