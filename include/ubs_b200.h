@@ -119,15 +119,18 @@ typedef struct UbsBinBuffers {
     uint64_t *keys_sorted; /* n: depth keys after sort */
     uint32_t *ids_iota;    /* n: scratch (0..n-1) */
     uint32_t *order;       /* n: ids by (depth, id); first n_vis are visible */
-    uint32_t *offsets;     /* n: exclusive scan of tile counts in rank order */
-    uint32_t *pair_keys;   /* capacity: tile id per pair (emit order) */
-    uint32_t *pair_vals;   /* capacity: primitive id per pair (emit order) */
-    uint32_t *pair_keys_sorted;
-    uint32_t *tile_ids;    /* capacity: primitive ids grouped by tile, depth ordered */
+    uint32_t *tile_ids;    /* pair_capacity: primitive ids grouped by tile, depth ordered */
     uint32_t *tile_ranges; /* 2 x n_tiles: [start, end) into tile_ids */
     int64_t pair_capacity;
     void *temp;            /* CUB scratch */
     size_t temp_bytes;
+    uint32_t *chunk_hist;  /* 2 x chunk_count x n_buckets: per-chunk bucket counts, then offsets */
+    int64_t chunk_hist_capacity; /* elements */
+    int32_t chunk_count;   /* G rank chunks */
+    uint64_t *entries;     /* pair_capacity: bucket entries (id | tx0 << 32 | tx1 << 48) */
+    uint32_t *seg_scratch; /* (2 x 128 + 1) x n_buckets */
+    uint32_t *bucket_start;/* n_buckets + 1 */
+    int64_t bucket_capacity; /* elements of bucket_start */
 } UbsBinBuffers;
 
 /* Forward outputs.  Image/alpha/T are f32, or f64 in the fp64 raster. */
@@ -164,10 +167,11 @@ int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec3
 
 /* CUB scratch bytes needed for n primitives, pair capacity and tile count */
 size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
-/* depth sort (stable on id), rank-ordered exclusive scan of tile counts, and the
- * per-tile [start, end) ranges from the corner difference array */
+/* depth sort (stable on id) and the per-tile [start, end) ranges from the
+ * rect-corner difference array */
 int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb, ubs_stream_t s);
-/* emit (tile, id) pairs in rank order, stable sort on tile bits */
+/* per-tile depth-ordered id lists (sort-free two-level stable bucketing);
+ * n_buckets = TY * ceil(TX / 8) */
 int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                   int64_t n_pairs, ubs_stream_t s);
 

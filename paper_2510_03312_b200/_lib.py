@@ -48,10 +48,11 @@ class UbsPrimBuffers(Structure):
 
 
 class UbsBinBuffers(Structure):
-    _fields_ = [("keys_sorted", c_void_p), ("ids_iota", c_void_p), ("order", c_void_p), ("offsets", c_void_p),
-                ("pair_keys", c_void_p), ("pair_vals", c_void_p), ("pair_keys_sorted", c_void_p),
+    _fields_ = [("keys_sorted", c_void_p), ("ids_iota", c_void_p), ("order", c_void_p),
                 ("tile_ids", c_void_p), ("tile_ranges", c_void_p), ("pair_capacity", c_int64),
-                ("temp", c_void_p), ("temp_bytes", c_size_t)]
+                ("temp", c_void_p), ("temp_bytes", c_size_t), ("chunk_hist", c_void_p),
+                ("chunk_hist_capacity", c_int64), ("chunk_count", c_int32), ("entries", c_void_p),
+                ("seg_scratch", c_void_p), ("bucket_start", c_void_p), ("bucket_capacity", c_int64)]
 
 
 class UbsImageBuffers(Structure):

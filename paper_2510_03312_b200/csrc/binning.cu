@@ -4,21 +4,18 @@
 // raster.py:252-266 (build_tiles, an O(tiles x N) mask loop on the CPU).
 //
 // Device algorithm:
-//   1. stable LSD radix sort of (f64 depth bits, id) over all n primitives;
-//      invisible primitives carry an all-ones key and sort to the back.  With
-//      values emitted in id order the stable sort reproduces lexsort.
-//   2. gather each rank's tile count, exclusive scan in rank order.
-//   3. emit (tile, id) pairs rank-major, row-major inside each rect.
-//   4. stable radix sort on the tile bits only (ceil(log2 n_tiles) bits, two
-//      8-bit digit passes at 1080p): since emission is already rank ordered,
-//      this equals a full (tile, rank) sort.
-//   5. [start, end) per tile without touching the pairs: the preprocess
-//      kernel adds each visible rect's corners to a 2D difference array, whose
-//      prefix sums are the per-tile counts (tile_scan_kernel).
+//   1. stable LSD radix sort (CUB) of (f64 depth bits, id) over all n
+//      primitives; invisible primitives carry an all-ones key and sort to the
+//      back.  With values emitted in id order the stable sort reproduces
+//      lexsort.
+//   2. per-tile [start, end): the preprocess kernel adds each visible rect's
+//      corners to a 2D difference array whose prefix sums are the per-tile
+//      counts (tile_scan_kernel); no pass over the K pairs.
+//   3. per-tile depth-ordered lists without a global pair sort: see the
+//      "Sort-free stable binning" block below.
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "ubs_common.cuh"
 
@@ -29,76 +26,25 @@ __global__ void iota_kernel(uint32_t *out, int64_t n) {
     if (i < n) out[i] = (uint32_t)i;
 }
 
-__global__ void gather_counts_kernel(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tile_count,
-                                     uint32_t *__restrict__ counts_by_rank, int64_t n) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) counts_by_rank[r] = tile_count[order[r]];
-}
-
-// One warp per 32 consecutive ranks; for each rank the whole warp writes its
-// pairs cooperatively, so a primitive covering thousands of tiles does not
-// serialise on one thread and every store instruction is coalesced.
-__global__ void emit_pairs_kernel(const uint32_t *__restrict__ order, const uint32_t *__restrict__ offsets,
-                                  const uint64_t *__restrict__ rect, const uint32_t *__restrict__ tile_count,
-                                  const uint32_t *__restrict__ n_visible, int tiles_x,
-                                  uint32_t *__restrict__ pair_keys, uint32_t *__restrict__ pair_vals) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nv = *n_visible;
-    const int64_t r0 = warp * 32;
-    if (r0 >= nv) return;
-    const int64_t r = r0 + lane;
-    uint32_t id = 0, cnt = 0, off = 0;
-    uint64_t rc = 0;
-    if (r < nv) {
-        id = order[r];
-        off = offsets[r];
-        cnt = tile_count[id];
-        rc = rect[id];
-    }
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t c = __shfl_sync(0xffffffffu, cnt, j);
-        if (c == 0) continue;
-        const uint32_t pid = __shfl_sync(0xffffffffu, id, j);
-        const uint32_t o = __shfl_sync(0xffffffffu, off, j);
-        const uint64_t q = __shfl_sync(0xffffffffu, rc, j);
-        const uint32_t tx0 = (uint32_t)(q & 0xFFFF), ty0 = (uint32_t)((q >> 16) & 0xFFFF);
-        const uint32_t tx1 = (uint32_t)((q >> 32) & 0xFFFF);
-        const uint32_t w = tx1 - tx0 + 1;
-        // floor((k + 0.5) / w) in fp32 is exact here: (k + 0.5)/w is >= 0.5/w
-        // away from an integer, far more than the rounding of two fp32 ops
-        const float inv_w = 1.0f / (float)w;
-        for (uint32_t k = lane; k < c; k += 32) {
-            const uint32_t dy = (uint32_t)(((float)k + 0.5f) * inv_w);
-            const uint32_t ty = ty0 + dy, tx = tx0 + (k - dy * w);
-            pair_keys[o + k] = ty * (uint32_t)tiles_x + tx;
-            pair_vals[o + k] = pid;
-        }
-    }
-}
-
 // Per-tile [start, end) from the rect-corner difference array (one CTA):
 // row prefix, column prefix -> per-tile pair counts, then an exclusive scan
 // in row-major tile order.  Equals the ranges of the tile-sorted pair array
 // because every visible primitive contributes exactly its rect.
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(int32_t *__restrict__ grid, int TX, int TY, uint32_t *__restrict__ ranges) {
-    const int gw = TX + 1;
+tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *__restrict__ ranges) {
+    extern __shared__ int32_t g[];
+    const int gw = TX + 1, gsz = (TX + 1) * (TY + 1);
+    for (int i = threadIdx.x; i < gsz; i += kScanThreads) g[i] = grid_in[i];
+    __syncthreads();
     for (int r = threadIdx.x; r <= TY; r += kScanThreads) {
         int acc = 0;
-        for (int c = 0; c <= TX; ++c) {
-            acc += grid[r * gw + c];
-            grid[r * gw + c] = acc;
-        }
+        for (int c = 0; c <= TX; ++c) acc = (g[r * gw + c] += acc);
     }
     __syncthreads();
     for (int c = threadIdx.x; c <= TX; c += kScanThreads) {
         int acc = 0;
-        for (int r = 0; r <= TY; ++r) {
-            acc += grid[r * gw + c];
-            grid[r * gw + c] = acc;
-        }
+        for (int r = 0; r <= TY; ++r) acc = (g[r * gw + c] += acc);
     }
     __syncthreads();
     __shared__ uint32_t warp_tot[kScanThreads / 32];
@@ -110,7 +56,7 @@ tile_scan_kernel(int32_t *__restrict__ grid, int TX, int TY, uint32_t *__restric
     for (int base = 0; base < n_tiles; base += kScanThreads) {
         const int t = base + threadIdx.x;
         uint32_t c = 0;
-        if (t < n_tiles) c = (uint32_t)grid[(t / TX) * gw + (t % TX)];
+        if (t < n_tiles) c = (uint32_t)g[(t / TX) * gw + (t % TX)];
         uint32_t x = c;  // inclusive warp scan
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -138,10 +84,259 @@ tile_scan_kernel(int32_t *__restrict__ grid, int TX, int TY, uint32_t *__restric
     }
 }
 
-static int tile_bits(int n_tiles) {
-    int b = 1;
-    while ((1 << b) < n_tiles) ++b;
-    return b;
+// ---------------------------------------------------------------------------
+// Sort-free stable binning.
+//
+// Per-tile lists are built in two levels so that every large write is
+// contiguous:
+//   level 1: rank-ordered entries (id, tx0, tx1) are stably distributed into
+//            coarse buckets = (tile row, band of kBand tile columns).  Ranks
+//            are cut into G chunks; a chunk's per-bucket counts come from a
+//            rect-corner difference array over the (rows x bands) grid (4
+//            shared atomics per rank), offsets from a scan over chunks, and
+//            the ordered scatter uses warp ballots (warp w owns rows w, w+32,
+//            ...; for each 32-rank batch and each band it ballots the ranks
+//            covering (row, band) and writes them at popc-prefix positions).
+//   level 2: one CTA per tile scans its bucket (~2.3x its own list at
+//            kBand = 8) and appends the entries whose [tx0, tx1] contains the
+//            tile, with a block-ordered compaction, to its contiguous list.
+// Every tile list is the rank-ordered set of visible primitives whose rect
+// contains the tile == build_tiles (raster.py:252-266).
+// HBM: 8 B per bucket entry written + read (L2-resident at 1080p), 4 B per
+// pair written once; no global sort of the K pairs.
+// ---------------------------------------------------------------------------
+constexpr int kBand = 8;  // tile columns per bucket band
+
+// Level-1 work unit: one warp per chunk of kChunkRanks consecutive ranks
+// (8 warps per CTA), each with a private shared-memory counter per bucket.
+constexpr int kChunkRanks = 128;
+constexpr int kBinWarps = 8;
+
+// the buckets of one rank's rect: rows ty0..ty1 x bands b0..b1, row-major
+struct RankBuckets {
+    int ty0, b0, nbw, nb;
+    __device__ __forceinline__ int bucket(int j, int NB) const { return (ty0 + j / nbw) * NB + b0 + j % nbw; }
+};
+__device__ __forceinline__ RankBuckets rank_buckets(uint64_t q) {
+    RankBuckets rb;
+    rb.b0 = (int)(q & 0xFFFF) / kBand;
+    rb.ty0 = (int)((q >> 16) & 0xFFFF);
+    const int b1 = (int)((q >> 32) & 0xFFFF) / kBand, ty1 = (int)((q >> 48) & 0xFFFF);
+    rb.nbw = b1 - rb.b0 + 1;
+    rb.nb = rb.nbw * (ty1 - rb.ty0 + 1);
+    return rb;
+}
+
+// (1) per-chunk bucket counts
+__global__ void __launch_bounds__(kBinWarps * 32)
+bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
+                   const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G, int NB,
+                   int nbk, uint32_t *__restrict__ hist) {
+    extern __shared__ uint32_t scnt[];  // kBinWarps x nbk
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int chunk = blockIdx.x * kBinWarps + w;
+    uint32_t *cnt = scnt + w * nbk;
+    for (int k = lane; k < nbk; k += 32) cnt[k] = 0;
+    __syncwarp();
+    if (chunk >= G) return;
+    const int64_t nv = *n_visible;
+    const int64_t r0 = (int64_t)chunk * kChunkRanks, r1 = min(r0 + kChunkRanks, nv);
+    for (int64_t rb = r0; rb < r1; rb += 32) {
+        const int64_t r = rb + lane;
+        uint64_t q = 0;
+        bool has = false;
+        if (r < r1) {
+            const uint32_t id = order[r];
+            has = tile_count[id] != 0;
+            if (has) q = rect[id];
+        }
+        const int nbatch = (int)min((int64_t)32, r1 - rb);
+        for (int j = 0; j < nbatch; ++j) {
+            if (!__shfl_sync(0xffffffffu, (int)has, j)) continue;
+            const RankBuckets b = rank_buckets(__shfl_sync(0xffffffffu, q, j));
+            for (int i = lane; i < b.nb; i += 32) atomicAdd(&cnt[b.bucket(i, NB)], 1u);
+        }
+    }
+    __syncwarp();
+    uint32_t *h = hist + (int64_t)chunk * nbk;
+    for (int k = lane; k < nbk; k += 32) h[k] = cnt[k];
+}
+
+// (2) offsets[c][k] = bucket_start[k] + sum_{c' < c} hist[c'][k], in three
+// well-parallel passes over S = kSegs segments of chunks:
+//   a) segsum[s][k]  = sum of hist over segment s            (grid: k x s)
+//   b) per bucket k: exclusive scan of segsum over s -> segbase, total[k];
+//      then one CTA scans total -> bucket_start               (grid: k; 1 CTA)
+//   c) offsets over each segment, read hist, write off        (grid: k x s)
+constexpr int kSegs = 128;
+
+__global__ void __launch_bounds__(256)
+bucket_segsum_kernel(const uint32_t *__restrict__ hist, int nbk, int G, uint32_t *__restrict__ segsum) {
+    const int k = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int sg = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (k >= nbk) return;
+    const int L = (G + kSegs - 1) / kSegs;
+    const int c0 = sg * L, c1 = min(G, c0 + L);
+    uint32_t sum = 0;
+    for (int c = c0; c < c1; ++c) sum += hist[(int64_t)c * nbk + k];
+    segsum[(int64_t)sg * nbk + k] = sum;
+}
+
+__global__ void __launch_bounds__(256)
+bucket_segscan_kernel(const uint32_t *__restrict__ segsum, int nbk, uint32_t *__restrict__ segbase,
+                      uint32_t *__restrict__ total) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nbk) return;
+    uint32_t v[kSegs];
+#pragma unroll
+    for (int j = 0; j < kSegs; ++j) v[j] = segsum[(int64_t)j * nbk + k];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kSegs; ++j) {
+        segbase[(int64_t)j * nbk + k] = acc;
+        acc += v[j];
+    }
+    total[k] = acc;
+}
+
+// one CTA: bucket_start = exclusive scan of bucket totals (nbk + 1 entries)
+__global__ void __launch_bounds__(1024)
+bucket_start_kernel(const uint32_t *__restrict__ total, int nbk, uint32_t *__restrict__ bstart) {
+    __shared__ uint32_t warp_tot[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < nbk; base += 1024) {
+        const int k = base + threadIdx.x;
+        const uint32_t c = k < nbk ? total[k] : 0u;
+        uint32_t x = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = warp_tot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_tot[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - c;
+        if (k < nbk) bstart[k] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + c;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bstart[nbk] = carry;
+}
+
+__global__ void __launch_bounds__(256)
+bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restrict__ segbase,
+                      const uint32_t *__restrict__ bstart, int nbk, int G, uint32_t *__restrict__ off) {
+    const int k = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int sg = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (k >= nbk) return;
+    const int L = (G + kSegs - 1) / kSegs;
+    const int c0 = sg * L, c1 = min(G, c0 + L);
+    uint32_t acc = bstart[k] + segbase[(int64_t)sg * nbk + k];
+    for (int c = c0; c < c1; ++c) {
+        const uint32_t v = hist[(int64_t)c * nbk + k];
+        off[(int64_t)c * nbk + k] = acc;
+        acc += v;
+    }
+}
+
+// (3) ordered scatter: each warp walks its chunk's ranks in order, lanes over
+// the rank's buckets (distinct within a rank), bumping private counters.
+__global__ void __launch_bounds__(kBinWarps * 32)
+bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
+                      const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
+                      int NB, int nbk, const uint32_t *__restrict__ hist, uint64_t *__restrict__ entries) {
+    extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int chunk = blockIdx.x * kBinWarps + w;
+    if (chunk >= G) return;
+    const int64_t nv = *n_visible;
+    const int64_t r0 = (int64_t)chunk * kChunkRanks, r1 = min(r0 + kChunkRanks, nv);
+    if (r0 >= r1) return;
+    uint32_t *sfill = sfill_all + w * nbk;
+    const uint32_t *h = hist + (int64_t)chunk * nbk;
+    for (int k = lane; k < nbk; k += 32) sfill[k] = h[k];
+    __syncwarp();
+    for (int64_t rb = r0; rb < r1; rb += 32) {
+        const int64_t r = rb + lane;
+        uint64_t q = 0;
+        uint32_t id = 0;
+        bool has = false;
+        if (r < r1) {
+            id = order[r];
+            has = tile_count[id] != 0;
+            if (has) q = rect[id];
+        }
+        const int nbatch = (int)min((int64_t)32, r1 - rb);
+        for (int j = 0; j < nbatch; ++j) {
+            if (!__shfl_sync(0xffffffffu, (int)has, j)) continue;
+            const uint64_t qj = __shfl_sync(0xffffffffu, q, j);
+            const uint32_t idj = __shfl_sync(0xffffffffu, id, j);
+            const uint64_t ent = (uint64_t)idj | ((qj & 0xFFFFull) << 32) | (((qj >> 32) & 0xFFFFull) << 48);
+            const RankBuckets b = rank_buckets(qj);
+            for (int i = lane; i < b.nb; i += 32) {
+                const int k = b.bucket(i, NB);
+                const uint32_t pos = sfill[k];
+                entries[pos] = ent;
+                sfill[k] = pos + 1;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// (4) per-tile lists: one CTA per tile; each warp owns a contiguous segment
+// of the tile's bucket.  Phase 1 counts matches per warp (no barriers inside
+// the scan), one block scan of the 8 warp totals, phase 2 re-reads the
+// (L2-resident) segment and writes the ids in order.
+constexpr int kListThreads = 256;
+__global__ void __launch_bounds__(kListThreads)
+tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restrict__ bstart,
+                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t *__restrict__ out) {
+    __shared__ uint32_t wtot[kListThreads / 32];
+    const int tile = blockIdx.x;
+    const int ty = tile / TX, tx = tile - ty * TX;
+    const int k = ty * NB + tx / kBand;
+    const uint32_t e0 = bstart[k], e1 = bstart[k + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kListThreads / 32;
+    const uint32_t len = e1 - e0;
+    const uint32_t per = ((len + nw - 1) / nw + 31) & ~31u;  // warp segment, multiple of 32
+    const uint32_t s0 = e0 + min(len, per * wid), s1 = e0 + min(len, per * (wid + 1));
+    auto hit = [&](uint32_t i, uint32_t &id) {
+        const uint64_t e = entries[i];
+        const int tx0 = (int)((e >> 32) & 0xFFFF), tx1 = (int)(e >> 48);
+        id = (uint32_t)e;
+        return tx0 <= tx && tx <= tx1;
+    };
+    uint32_t c = 0;
+    for (uint32_t i = s0 + lane; i < s1; i += 32) {
+        uint32_t id;
+        c += hit(i, id) ? 1u : 0u;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) wtot[wid] = c;
+    __syncthreads();
+    uint32_t w = ranges[2 * tile];
+    for (int j = 0; j < wid; ++j) w += wtot[j];
+    for (uint32_t base = s0; base < s1; base += 32) {
+        const uint32_t i = base + lane;
+        uint32_t id = 0;
+        const bool p = i < s1 && hit(i, id);
+        const unsigned m = __ballot_sync(0xffffffffu, p);
+        if (p) out[w + __popc(m & ((1u << lane) - 1u))] = id;
+        w += __popc(m);
+    }
 }
 
 }  // namespace ubs
@@ -149,17 +344,13 @@ static int tile_bits(int n_tiles) {
 using namespace ubs;
 
 extern "C" size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles) {
-    size_t a = 0, b = 0, c = 0;
+    (void)pair_capacity;
+    (void)n_tiles;
+    size_t a = 0;
     const int nn = (int)(n > 0 ? n : 1);
-    const int kk = (int)(pair_capacity > 0 ? pair_capacity : 1);
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (const uint32_t *)nullptr, (uint32_t *)nullptr, nn, 0, 64);
-    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, nn);
-    cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, kk, 0,
-                                    tile_bits(n_tiles > 1 ? n_tiles : 2));
-    size_t m = a > b ? a : b;
-    return (m > c ? m : c) + 256;
+    return a + 256;
 }
 
 extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
@@ -169,7 +360,10 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
     if (n >= (int64_t)1 << 31) return UBS_E_ARGS;
     cudaStream_t s = (cudaStream_t)stream;
     const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
-    tile_scan_kernel<<<1, kScanThreads, 0, s>>>(pb->tile_grid, TX, TY, bb->tile_ranges);
+    const size_t gbytes = sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1);
+    if (gbytes > 200 * 1024) return UBS_E_ARGS;  // > ~50k tiles (about 3.5k x 3.5k px) is not supported
+    cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbytes);
+    tile_scan_kernel<<<1, kScanThreads, gbytes, s>>>(pb->tile_grid, TX, TY, bb->tile_ranges);
     if (n == 0) {
         UBS_CUDA_CHECK();
         return UBS_OK;
@@ -181,11 +375,6 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
     if (cub::DeviceRadixSort::SortPairs(bb->temp, bytes, pb->depth_key, bb->keys_sorted, bb->ids_iota,
                                         bb->order, (int)n, 0, 64, s) != cudaSuccess)
         return UBS_E_CUDA;
-    // ids_iota is free again: reuse it for the rank-ordered counts
-    gather_counts_kernel<<<blocks, thr, 0, s>>>(bb->order, pb->tile_count, bb->ids_iota, n);
-    bytes = bb->temp_bytes;
-    if (cub::DeviceScan::ExclusiveSum(bb->temp, bytes, bb->ids_iota, bb->offsets, (int)n, s) != cudaSuccess)
-        return UBS_E_CUDA;
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
@@ -196,19 +385,35 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     const int W = v->cam.width, H = v->cam.height;
     const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
     const int n_tiles = TX * TY;
+    const int NB = (TX + kBand - 1) / kBand, nbk = TY * NB;
     cudaStream_t s = (cudaStream_t)stream;
     if (n_pairs == 0 || v->n == 0) return UBS_OK;
-    if (n_pairs > bb->pair_capacity || n_pairs >= ((int64_t)1 << 31)) return UBS_E_CAPACITY;
-    const int64_t n = v->n;
-    const int thr = 256;
-    const int64_t warps = (n + 31) / 32;
-    emit_pairs_kernel<<<(unsigned)((warps * 32 + thr - 1) / thr), thr, 0, s>>>(
-        bb->order, bb->offsets, pb->rect, pb->tile_count, pb->n_visible, TX, bb->pair_keys, bb->pair_vals);
-    size_t bytes = bb->temp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(bb->temp, bytes, bb->pair_keys, bb->pair_keys_sorted, bb->pair_vals,
-                                        bb->tile_ids, (int)n_pairs, 0, tile_bits(n_tiles > 1 ? n_tiles : 2),
-                                        s) != cudaSuccess)
-        return UBS_E_CUDA;
+    if (n_pairs > bb->pair_capacity || n_pairs >= ((int64_t)1 << 32)) return UBS_E_CAPACITY;
+    const int G = bb->chunk_count;
+    if (G < 1 || !bb->chunk_hist || !bb->entries || !bb->seg_scratch || !bb->bucket_start || !bb->tile_ids)
+        return UBS_E_ARGS;
+    if (2 * (int64_t)G * nbk > bb->chunk_hist_capacity || (int64_t)nbk + 1 > bb->bucket_capacity)
+        return UBS_E_CAPACITY;
+    if ((int64_t)G * kChunkRanks < v->n) return UBS_E_ARGS;  // chunk_count must cover n / kChunkRanks
+    const size_t cnt_bytes = sizeof(uint32_t) * (size_t)kBinWarps * nbk;
+    if (cnt_bytes > 200 * 1024) return UBS_E_ARGS;
+    cudaFuncSetAttribute(bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
+    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
+    const unsigned cta = (unsigned)((G + kBinWarps - 1) / kBinWarps);
+    bucket_hist_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count, pb->n_visible, G,
+                                                              NB, nbk, bb->chunk_hist);
+    // seg_scratch: segsum (kSegs x nbk) | segbase (kSegs x nbk) | total (nbk)
+    uint32_t *segsum = bb->seg_scratch, *segbase = segsum + (size_t)kSegs * nbk, *total = segbase + (size_t)kSegs * nbk;
+    uint32_t *off = bb->chunk_hist + (size_t)G * nbk;  // second half of chunk_hist
+    const dim3 kg((unsigned)((nbk + 31) / 32), kSegs / 8);
+    bucket_segsum_kernel<<<kg, 256, 0, s>>>(bb->chunk_hist, nbk, G, segsum);
+    bucket_segscan_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(segsum, nbk, segbase, total);
+    bucket_start_kernel<<<1, 1024, 0, s>>>(total, nbk, bb->bucket_start);
+    bucket_offsets_kernel<<<kg, 256, 0, s>>>(bb->chunk_hist, segbase, bb->bucket_start, nbk, G, off);
+    bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count,
+                                                                 pb->n_visible, G, NB, nbk, off, bb->entries);
+    tile_lists_kernel<<<n_tiles, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, NB,
+                                                       bb->tile_ids);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

@@ -166,6 +166,10 @@ class Workspace:
         self.counters32 = self.counters.view(torch.int32)
         self.debug = None
         self.tile_grid = None
+        self.chunk_hist = None
+        self.seg_scratch = None
+        self.bucket_start = None
+        self.chunk_count = 0
         self.grad2d = None
         self.loss_scratch = None
         self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
@@ -188,7 +192,6 @@ class Workspace:
         self.keys_sorted = self._i(cap, torch.int64)
         self.ids_iota = self._i(cap, torch.int32)
         self.order = self._i(cap, torch.int32)
-        self.offsets = self._i(cap, torch.int32)
         self.hit_clamp = self._i(cap, torch.uint8)
         self.n_cap = cap
         self.temp_bytes = 0  # CUB scratch depends on n
@@ -215,15 +218,26 @@ class Workspace:
             self.tile_cap = ntiles
             self.temp_bytes = 0
 
+    CHUNK_RANKS = 128   # ranks per level-1 binning chunk (one warp each; csrc/binning.cu kChunkRanks)
+    BAND = 8            # tile columns per level-1 bucket (csrc/binning.cu kBand)
+
+    def ensure_chunks(self, n: int, width: int, height: int):
+        tx, ty = math.ceil(width / TILE), math.ceil(height / TILE)
+        nbk = ty * math.ceil(tx / self.BAND)
+        g = max(1, -(-n // self.CHUNK_RANKS))
+        self.chunk_count = g
+        if self.chunk_hist is None or self.chunk_hist.numel() < 2 * g * nbk:
+            self.chunk_hist = self._i(2 * g * nbk, torch.int32)
+        if self.seg_scratch is None or self.seg_scratch.numel() < 257 * nbk:
+            self.seg_scratch = self._i(257 * nbk, torch.int32)
+            self.bucket_start = self._i(nbk + 1, torch.int32)
+
     def ensure_pairs(self, k: int):
         if k > self.pair_cap:
             cap = max(k, int(self.pair_cap * 1.3), 1024)
-            self.pair_keys = self._i(cap, torch.int32)
-            self.pair_vals = self._i(cap, torch.int32)
-            self.pair_keys_sorted = self._i(cap, torch.int32)
             self.tile_ids = self._i(cap, torch.int32)
+            self.entries = self._i(cap, torch.int64)
             self.pair_cap = cap
-            self.temp_bytes = 0
         need = int(self.lib.ubs_bin_temp_bytes(self.n_cap, self.pair_cap, self.tile_cap))
         if need > self.temp_bytes:
             self.temp = self._i(need, torch.uint8)
@@ -249,16 +263,20 @@ class Workspace:
         bb.keys_sorted = _ptr(self.keys_sorted)
         bb.ids_iota = _ptr(self.ids_iota)
         bb.order = _ptr(self.order)
-        bb.offsets = _ptr(self.offsets)
         if self.pair_cap:
-            bb.pair_keys = _ptr(self.pair_keys)
-            bb.pair_vals = _ptr(self.pair_vals)
-            bb.pair_keys_sorted = _ptr(self.pair_keys_sorted)
             bb.tile_ids = _ptr(self.tile_ids)
+            bb.entries = _ptr(self.entries)
         bb.tile_ranges = _ptr(self.tile_ranges)
         bb.pair_capacity = self.pair_cap
         bb.temp = _ptr(self.temp) if self.temp_bytes else 0
         bb.temp_bytes = self.temp_bytes
+        if self.chunk_hist is not None:
+            bb.chunk_hist = _ptr(self.chunk_hist)
+            bb.chunk_hist_capacity = self.chunk_hist.numel()
+            bb.chunk_count = self.chunk_count
+            bb.seg_scratch = _ptr(self.seg_scratch)
+            bb.bucket_start = _ptr(self.bucket_start)
+            bb.bucket_capacity = self.bucket_start.numel()
         return bb
 
     def image_buffers(self) -> UbsImageBuffers:
@@ -311,6 +329,7 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     W, H, n = int(cam.width), int(cam.height), ds.n
     ws.ensure_prims(max(n, 1))
     ws.ensure_pixels(W, H)
+    ws.ensure_chunks(n, W, H)
     if want_debug:
         if ws.debug is None or ws.debug.numel() < n * _lib.DEBUG_STRIDE:
             ws.debug = torch.zeros(max(n, 1) * _lib.DEBUG_STRIDE, dtype=torch.float64, device=ws.device)

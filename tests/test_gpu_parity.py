@@ -230,3 +230,16 @@ def test_gradient_error_on_saturated_gate():
     tgt = np.zeros((32, 32, 3))
     with pytest.raises(GradientError):
         backward(sc, [(cam, q, tgt)], LossConfig(), DEFAULT_SETTINGS)
+
+
+def test_binning_large_list_parity():
+    # a denser scene at an odd size: sort-free two-level bucketing reproduces
+    # build_tiles list for list
+    from paper_2510_03312_b200 import raster
+    sc = quantize_f32(S.random_scene(7, 20000, seed=17))
+    cam = S.random_camera(200, 18)
+    q = S.random_query(7, 19)
+    got = raster.render_with_cache(sc, cam, q, DEFAULT_SETTINGS, precision="fp32")
+    ref = O.render_frame(sc, cam, q, DEFAULT_SETTINGS)
+    assert np.array_equal(got.tile_ids, ref["tile_ids"])
+    assert np.array_equal(got.n_contrib, ref["count"])
