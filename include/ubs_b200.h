@@ -68,6 +68,9 @@ enum {
     UBS_F_THIN = 16,        /* fp32 raster guard: pixels touching this splat are re-done in fp64 */
 };
 
+/* device status bits (UbsBinBuffers.status) */
+enum { UBS_S_PAIR_OVERFLOW = 1 };
+
 /* Camera (camera.py:15-51): intrinsics + rigid world_to_cam. */
 typedef struct UbsCamera {
     double fx, fy, cx, cy;
@@ -107,6 +110,7 @@ typedef struct UbsPrimBuffers {
     uint32_t *n_visible;   /* [1] += number of visible primitives (caller zeroes) */
     unsigned long long *n_pairs; /* [1] += total tile pairs K (caller zeroes) */
     int32_t *tile_grid;    /* (TY+1) x (TX+1) 2D difference array of rect corners (zeroed by ubs_preprocess) */
+    unsigned long long *depth_range; /* [2] min / max visible depth key (initialised by ubs_preprocess) */
 } UbsPrimBuffers;
 
 /* debug row: 0 depth | 1-2 mean2 | 3-5 p2 00,01,11 | 6-7 radii | 8 gated opacity | 9 beta_x |
@@ -116,7 +120,7 @@ typedef struct UbsPrimBuffers {
 
 /* Binning buffers. */
 typedef struct UbsBinBuffers {
-    uint64_t *keys_sorted; /* n: depth keys after sort */
+    uint64_t *keys_sorted; /* n x 8 B scratch: 32-bit sort keys in / out */
     uint32_t *ids_iota;    /* n: scratch (0..n-1) */
     uint32_t *order;       /* n: ids by (depth, id); first n_vis are visible */
     uint32_t *tile_ids;    /* pair_capacity: primitive ids grouped by tile, depth ordered */
@@ -131,6 +135,7 @@ typedef struct UbsBinBuffers {
     uint32_t *seg_scratch; /* (2 x 128 + 1) x n_buckets */
     uint32_t *bucket_start;/* n_buckets + 1 */
     int64_t bucket_capacity; /* elements of bucket_start */
+    uint32_t *status;      /* [1] |= UBS_S_PAIR_OVERFLOW when K > pair_capacity (frame must be re-run) */
 } UbsBinBuffers;
 
 /* Forward outputs.  Image/alpha/T are f32, or f64 in the fp64 raster. */
@@ -167,11 +172,16 @@ int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec3
 
 /* CUB scratch bytes needed for n primitives, pair capacity and tile count */
 size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
-/* depth sort (stable on id) and the per-tile [start, end) ranges from the
- * rect-corner difference array */
+/* depth order = lexsort((ids, depth)): stable radix sort of 32-bit keys
+ * ((depth bits - min) >> shift) with ids in id order, then an exact repair of
+ * the rare runs of equal 32-bit keys by (f64 depth bits, id); plus the per-tile
+ * [start, end) ranges from the rect-corner difference array */
 int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb, ubs_stream_t s);
 /* per-tile depth-ordered id lists (sort-free two-level stable bucketing);
- * n_buckets = TY * ceil(TX / 8) */
+ * n_buckets = TY * ceil(TX / 8).  n_pairs >= 0: K as read by the host
+ * (checked against pair_capacity); n_pairs < 0: K stays on the device, every
+ * kernel that touches the pair buffers checks it against pair_capacity and
+ * sets UBS_S_PAIR_OVERFLOW instead of writing out of bounds (no host sync). */
 int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                   int64_t n_pairs, ubs_stream_t s);
 

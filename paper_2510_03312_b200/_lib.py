@@ -14,6 +14,7 @@ from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_u
 from . import build as _build
 
 UBS_OK, UBS_E_ARGS, UBS_E_CUDA, UBS_E_CAPACITY = 0, -1, -2, -3
+S_PAIR_OVERFLOW = 1
 F_VISIBLE, F_DEGENERATE, F_FLOOR3, F_FLOOR2, F_THIN = 1, 2, 4, 8, 16
 DEBUG_STRIDE = 32
 GRAD2D_STRIDE = 12
@@ -44,7 +45,8 @@ class UbsView(Structure):
 class UbsPrimBuffers(Structure):
     _fields_ = [("depth_key", c_void_p), ("rect", c_void_p), ("tile_count", c_void_p), ("flags", c_void_p),
                 ("rec32", c_void_p), ("rec64", c_void_p), ("debug", c_void_p), ("n_visible", c_void_p),
-                ("n_pairs", c_void_p), ("tile_grid", c_void_p)]
+                ("n_pairs", c_void_p), ("tile_grid", c_void_p),
+                ("depth_range", c_void_p)]
 
 
 class UbsBinBuffers(Structure):
@@ -52,7 +54,8 @@ class UbsBinBuffers(Structure):
                 ("tile_ids", c_void_p), ("tile_ranges", c_void_p), ("pair_capacity", c_int64),
                 ("temp", c_void_p), ("temp_bytes", c_size_t), ("chunk_hist", c_void_p),
                 ("chunk_hist_capacity", c_int64), ("chunk_count", c_int32), ("entries", c_void_p),
-                ("seg_scratch", c_void_p), ("bucket_start", c_void_p), ("bucket_capacity", c_int64)]
+                ("seg_scratch", c_void_p), ("bucket_start", c_void_p), ("bucket_capacity", c_int64),
+                ("status", c_void_p)]
 
 
 class UbsImageBuffers(Structure):

@@ -21,9 +21,47 @@
 
 namespace ubs {
 
-__global__ void iota_kernel(uint32_t *out, int64_t n) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (uint32_t)i;
+// 32-bit sort keys: (depth bits - min) >> shift with shift chosen so every
+// visible key is < 2^31 (strictly below the invisible key 0xFFFFFFFF); ids in
+// id order so the stable sort breaks ties by id.
+__global__ void depth_key32_kernel(const uint64_t *__restrict__ key64, const unsigned long long *__restrict__ range,
+                                   int64_t n, uint32_t *__restrict__ key32, uint32_t *__restrict__ ids) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long lo = range[0], hi = range[1];
+    const unsigned long long span = hi >= lo ? hi - lo : 0ull;
+    const int bits = span ? 64 - __clzll((long long)span) : 0;
+    const int shift = bits > 31 ? bits - 31 : 0;
+    const uint64_t k = key64[i];
+    key32[i] = (k == kInvisibleKey) ? 0xFFFFFFFFu : (uint32_t)((k - lo) >> shift);
+    ids[i] = (uint32_t)i;
+}
+
+// Exact order inside runs of equal 32-bit keys: the thread at a run start
+// insertion-sorts the run by (full f64 key, id).  Runs are rare and short
+// (~1e2 pairs of 2 among 1M visible primitives).
+__global__ void depth_tie_repair_kernel(const uint32_t *__restrict__ key32s, const uint64_t *__restrict__ key64,
+                                        const uint32_t *__restrict__ n_visible, uint32_t *__restrict__ order) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nv = *n_visible;
+    if (r + 1 >= nv) return;
+    const uint32_t k = key32s[r];
+    if (key32s[r + 1] != k || (r > 0 && key32s[r - 1] == k)) return;
+    int64_t e = r + 2;
+    while (e < nv && key32s[e] == k) ++e;
+    for (int64_t i = r + 1; i < e; ++i) {
+        const uint32_t id = order[i];
+        const uint64_t kk = key64[id];
+        int64_t j = i;
+        while (j > r) {
+            const uint32_t pj = order[j - 1];
+            const uint64_t kp = key64[pj];
+            if (kp < kk || (kp == kk && pj < id)) break;
+            order[j] = pj;
+            --j;
+        }
+        order[j] = id;
+    }
 }
 
 // Per-tile [start, end) from the rect-corner difference array (one CTA):
@@ -256,7 +294,9 @@ bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restr
 __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
                       const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
-                      int NB, int nbk, const uint32_t *__restrict__ hist, uint64_t *__restrict__ entries) {
+                      int NB, int nbk, const uint32_t *__restrict__ hist, uint64_t *__restrict__ entries,
+                      const unsigned long long *__restrict__ n_pairs, int64_t capacity, uint32_t *status) {
+    if (pairs_overflow(n_pairs, capacity, status)) return;
     extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int chunk = blockIdx.x * kBinWarps + w;
@@ -303,7 +343,9 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
 constexpr int kListThreads = 256;
 __global__ void __launch_bounds__(kListThreads)
 tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restrict__ bstart,
-                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t *__restrict__ out) {
+                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t *__restrict__ out,
+                  const unsigned long long *__restrict__ n_pairs, int64_t capacity) {
+    if (pairs_overflow(n_pairs, capacity, nullptr)) return;
     __shared__ uint32_t wtot[kListThreads / 32];
     const int tile = blockIdx.x;
     const int ty = tile / TX, tx = tile - ty * TX;
@@ -348,8 +390,8 @@ extern "C" size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n
     (void)n_tiles;
     size_t a = 0;
     const int nn = (int)(n > 0 ? n : 1);
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, nn, 0, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, nn, 0, 32);
     return a + 256;
 }
 
@@ -370,11 +412,14 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
     }
     const int thr = 256;
     const unsigned blocks = (unsigned)((n + thr - 1) / thr);
-    iota_kernel<<<blocks, thr, 0, s>>>(bb->ids_iota, n);
+    uint32_t *k32 = reinterpret_cast<uint32_t *>(bb->keys_sorted);
+    uint32_t *k32s = k32 + n;
+    depth_key32_kernel<<<blocks, thr, 0, s>>>(pb->depth_key, pb->depth_range, n, k32, bb->ids_iota);
     size_t bytes = bb->temp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(bb->temp, bytes, pb->depth_key, bb->keys_sorted, bb->ids_iota,
-                                        bb->order, (int)n, 0, 64, s) != cudaSuccess)
+    if (cub::DeviceRadixSort::SortPairs(bb->temp, bytes, k32, k32s, bb->ids_iota, bb->order, (int)n, 0, 32, s) !=
+        cudaSuccess)
         return UBS_E_CUDA;
+    depth_tie_repair_kernel<<<blocks, thr, 0, s>>>(k32s, pb->depth_key, pb->n_visible, bb->order);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
@@ -388,7 +433,7 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     const int NB = (TX + kBand - 1) / kBand, nbk = TY * NB;
     cudaStream_t s = (cudaStream_t)stream;
     if (n_pairs == 0 || v->n == 0) return UBS_OK;
-    if (n_pairs > bb->pair_capacity || n_pairs >= ((int64_t)1 << 32)) return UBS_E_CAPACITY;
+    if (n_pairs > bb->pair_capacity || bb->pair_capacity >= ((int64_t)1 << 32)) return UBS_E_CAPACITY;
     const int G = bb->chunk_count;
     if (G < 1 || !bb->chunk_hist || !bb->entries || !bb->seg_scratch || !bb->bucket_start || !bb->tile_ids)
         return UBS_E_ARGS;
@@ -411,9 +456,10 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     bucket_start_kernel<<<1, 1024, 0, s>>>(total, nbk, bb->bucket_start);
     bucket_offsets_kernel<<<kg, 256, 0, s>>>(bb->chunk_hist, segbase, bb->bucket_start, nbk, G, off);
     bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count,
-                                                                 pb->n_visible, G, NB, nbk, off, bb->entries);
+                                                                 pb->n_visible, G, NB, nbk, off, bb->entries,
+                                                                 pb->n_pairs, bb->pair_capacity, bb->status);
     tile_lists_kernel<<<n_tiles, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, NB,
-                                                       bb->tile_ids);
+                                                       bb->tile_ids, pb->n_pairs, bb->pair_capacity);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

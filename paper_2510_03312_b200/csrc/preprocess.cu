@@ -25,17 +25,18 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
     constexpr int P = 14 + 6 * C;
     __shared__ PT stage[kPreThreads * P];
     __shared__ uint32_t block_vis;
-    __shared__ unsigned long long block_pairs;
+    __shared__ unsigned long long block_pairs, block_dmin, block_dmax;
     const int64_t base = (int64_t)blockIdx.x * kPreThreads;
     const int64_t n = v.n;
     const int nloc = (int)min((int64_t)kPreThreads, n - base);
     const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
-    if (threadIdx.x == 0) { block_vis = 0; block_pairs = 0; }
+    if (threadIdx.x == 0) { block_vis = 0; block_pairs = 0; block_dmin = ~0ull; block_dmax = 0; }
     for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
     __syncthreads();
     const int t = threadIdx.x;
     bool vis = false;
     uint32_t my_count = 0;
+    unsigned long long my_key = ~0ull;
     if (t < nloc) {
         const int64_t i = base + t;
         PrimGeom<C> g;
@@ -69,6 +70,7 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
             }
         }
         pb.depth_key[i] = vis ? (uint64_t)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
+        my_key = pb.depth_key[i];
         pb.rect[i] = rect;
         pb.tile_count[i] = count;
         my_count = count;
@@ -137,14 +139,27 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
     // block-aggregated visible count and pair total
     unsigned ballot = __ballot_sync(0xffffffffu, vis);
     unsigned long long wsum = my_count;
-    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    unsigned long long kmin = vis ? my_key : ~0ull, kmax = vis ? my_key : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        kmin = min(kmin, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmax, o));
+    }
     if ((threadIdx.x & 31) == 0) {
-        if (ballot) atomicAdd(&block_vis, (uint32_t)__popc(ballot));
+        if (ballot) {
+            atomicAdd(&block_vis, (uint32_t)__popc(ballot));
+            atomicMin(&block_dmin, kmin);
+            atomicMax(&block_dmax, kmax);
+        }
         if (wsum) atomicAdd(&block_pairs, wsum);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (block_vis) atomicAdd(pb.n_visible, block_vis);
+        if (block_vis) {
+            atomicAdd(pb.n_visible, block_vis);
+            atomicMin(pb.depth_range, block_dmin);
+            atomicMax(pb.depth_range + 1, block_dmax);
+        }
         if (block_pairs) atomicAdd(pb.n_pairs, block_pairs);
     }
 }
@@ -172,8 +187,11 @@ extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_
     if (v->n < 0 || (v->n > 0 && !v->params)) return UBS_E_ARGS;
     if (!pb->depth_key || !pb->rect || !pb->tile_count || !pb->flags) return UBS_E_ARGS;
     if (!pb->rec64 && !(want_rec32 && pb->rec32)) return UBS_E_ARGS;
-    if (!pb->tile_grid) return UBS_E_ARGS;
+    if (!pb->tile_grid || !pb->depth_range) return UBS_E_ARGS;
     cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(pb->depth_range, 0xFF, 8, s) != cudaSuccess ||
+        cudaMemsetAsync(pb->depth_range + 1, 0, 8, s) != cudaSuccess)
+        return UBS_E_CUDA;
     {
         const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
         if (cudaMemsetAsync(pb->tile_grid, 0, sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1), s) != cudaSuccess)

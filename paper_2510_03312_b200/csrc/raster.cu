@@ -31,10 +31,14 @@ struct RasterParams {
     int W, H, TX;
     double tau, clamp, tmin;
     double bg[3];
+    const unsigned long long *n_pairs;  // device K, checked against pair_capacity
+    int64_t pair_capacity;
 };
 
-static RasterParams make_params(const UbsView &v) {
+static RasterParams make_params(const UbsView &v, const UbsPrimBuffers &pb, const UbsBinBuffers &bb) {
     RasterParams p;
+    p.n_pairs = pb.n_pairs;
+    p.pair_capacity = bb.pair_capacity;
     p.W = v.cam.width;
     p.H = v.cam.height;
     p.TX = (p.W + kTile - 1) / kTile;
@@ -66,6 +70,7 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     __shared__ Rec64 srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
     __shared__ unsigned long long red[kTileThreads / 32];
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int px = tx * kTile + (threadIdx.x & (kTile - 1));
@@ -169,6 +174,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     __shared__ float4 s0[kTileThreads], s1[kTileThreads], s2[kTileThreads], s3[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
     __shared__ unsigned long long red[kTileThreads / 32];
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int px = tx * kTile + (threadIdx.x & (kTile - 1));
@@ -285,6 +291,7 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const uint32_t *__restrict__ fix_count, float *__restrict__ image, float *__restrict__ asum,
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits) {
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int lane = threadIdx.x & 31;
     const uint32_t nfix = *fix_count;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -415,6 +422,7 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
     __shared__ Rec srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
     __shared__ int smax;
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int px = tx * kTile + (threadIdx.x & (kTile - 1));
@@ -504,7 +512,7 @@ extern "C" int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, co
     if (!v || !pb || !bb || !ib || !ib->image || !ib->alpha_sum || !ib->t_stop || !ib->n_contrib ||
         !ib->hit_clamp || !ib->visits)
         return UBS_E_ARGS;
-    const RasterParams P = make_params(*v);
+    const RasterParams P = make_params(*v, *pb, *bb);
     const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
     cudaStream_t s = (cudaStream_t)stream;
     if (ib->raster_f64) {
@@ -527,7 +535,7 @@ extern "C" int ubs_raster_fixup(const UbsView *v, const UbsPrimBuffers *pb, cons
     if (!v || !pb || !bb || !ib) return UBS_E_ARGS;
     if (ib->raster_f64) return UBS_OK;  // nothing to fix: the fp64 raster is the reference arithmetic
     if (!pb->rec64 || !ib->fix_list || !ib->fix_count) return UBS_E_ARGS;
-    const RasterParams P = make_params(*v);
+    const RasterParams P = make_params(*v, *pb, *bb);
     // one pass over the device-counted list; grid sized for the GPU, not the list
     raster_fixup_kernel<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(
         P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, ib->fix_list, ib->fix_count, (float *)ib->image,
@@ -540,7 +548,7 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
                                    const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t stream) {
     if (!v || !pb || !bb || !ib || !gb || !gb->g_image || !gb->grad2d) return UBS_E_ARGS;
     if ((gb->grad2d_f64 != 0) != (ib->raster_f64 != 0)) return UBS_E_ARGS;
-    const RasterParams P = make_params(*v);
+    const RasterParams P = make_params(*v, *pb, *bb);
     const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
     cudaStream_t s = (cudaStream_t)stream;
     if (ib->raster_f64) {

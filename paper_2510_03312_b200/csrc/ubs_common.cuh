@@ -410,6 +410,17 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
     g.visible = g.in_front && on_screen && g.valid;
 }
 
+// Device-side capacity guard for the pair buffers: true (and the overflow
+// status bit set) when this frame's K exceeds the caller's capacity.
+__device__ __forceinline__ bool pairs_overflow(const unsigned long long *n_pairs, int64_t capacity,
+                                               uint32_t *status) {
+    if (n_pairs && (int64_t)*n_pairs > capacity) {
+        if (status && threadIdx.x == 0) atomicOr(status, (uint32_t)UBS_S_PAIR_OVERFLOW);
+        return true;
+    }
+    return false;
+}
+
 }  // namespace ubs
 
 #define UBS_CUDA_CHECK()                                   \

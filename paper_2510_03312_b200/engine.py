@@ -44,6 +44,8 @@ def _require_cuda(device) -> torch.device:
         raise _lib.UbsError("the UBS engine runs on CUDA devices only (no CPU fallback)")
     if not torch.cuda.is_available():
         raise _lib.UbsError("no CUDA device available: the UBS engine has no CPU fallback")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     return dev
 
 
@@ -127,8 +129,8 @@ class Frame:
     width: int
     height: int
     n: int
-    n_visible: int
-    n_pairs: int
+    n_visible_host: int | None  # known when rendered with sync=True
+    n_pairs_host: int | None
     image: torch.Tensor       # (H, W, 3)
     alpha_sum: torch.Tensor   # (H, W)
     t_stop: torch.Tensor      # (H, W)
@@ -136,6 +138,18 @@ class Frame:
     hit_clamp: torch.Tensor   # (n,) uint8
     ws: "Workspace"
     raster_f64: bool
+
+    @property
+    def n_visible(self) -> int:
+        if self.n_visible_host is None:
+            self.n_visible_host = int(self.ws.counters32[4].item())
+        return self.n_visible_host
+
+    @property
+    def n_pairs(self) -> int:
+        if self.n_pairs_host is None:
+            self.n_pairs_host = int(self.ws.counters[0].item())
+        return self.n_pairs_host
 
     @property
     def processed_pixels(self) -> int:
@@ -161,7 +175,8 @@ class Workspace:
         self.tile_cap = 0
         self.pair_cap = 0
         self.temp_bytes = 0
-        # [0] n_pairs u64 | [1] visits u64 | [2] lo: n_visible u32 | [3] lo: fix_count u32
+        # [0] n_pairs u64 | [1] visits u64 | [2] lo: n_visible u32 | [3] lo: fix_count u32 |
+        # [5] min visible depth key | [6] max visible depth key
         self.counters = torch.zeros(8, dtype=torch.int64, device=self.device)
         self.counters32 = self.counters.view(torch.int32)
         self.debug = None
@@ -174,6 +189,7 @@ class Workspace:
         self.loss_scratch = None
         self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)  # UBS_S_* bits, sticky
 
     # --- allocation -------------------------------------------------------
     def _i(self, n, dtype):
@@ -256,6 +272,7 @@ class Workspace:
         pb.n_visible = _ptr(self.counters) + 16
         pb.n_pairs = _ptr(self.counters)
         pb.tile_grid = _ptr(self.tile_grid)
+        pb.depth_range = _ptr(self.counters) + 40
         return pb
 
     def bin_buffers(self) -> UbsBinBuffers:
@@ -277,6 +294,7 @@ class Workspace:
             bb.seg_scratch = _ptr(self.seg_scratch)
             bb.bucket_start = _ptr(self.bucket_start)
             bb.bucket_capacity = self.bucket_start.numel()
+        bb.status = _ptr(self.status)
         return bb
 
     def image_buffers(self) -> UbsImageBuffers:
@@ -317,11 +335,16 @@ class _Timed:
 
 
 def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS,
-                 want_debug: bool = False, timers: dict | None = None) -> Frame:
+                 want_debug: bool = False, timers: dict | None = None, sync: bool = True) -> Frame:
     """Forward one frame on the current stream; returns device views.
 
-    ``timers``: optional dict collecting per-stage CUDA event pairs
-    ("preprocess", "bin_depth", "bin_tiles", "raster")."""
+    ``sync=True`` reads the frame's tile-pair count K back (one 16-byte copy)
+    and grows the pair buffers to fit before binning.  ``sync=False`` keeps
+    the whole frame asynchronous: the kernels check K against the current
+    capacity on the device and set ``ws.status`` (UBS_S_PAIR_OVERFLOW)
+    instead of overflowing; call :func:`check_status` (or render the frame
+    again with ``sync=True``) before trusting an async frame whose K may have
+    grown.  ``timers``: optional dict collecting per-stage CUDA event pairs."""
     lib = ws.lib
     if ds.device != ws.device:
         raise ValueError("scene and workspace live on different devices")
@@ -342,15 +365,18 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
         check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
     with _Timed(timers, "bin_depth"):
         check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
-    host = ws.counters[:3].cpu()  # the one per-frame sync: K and n_visible
-    k = int(host[0])
-    n_vis = int(host.view(torch.int32)[4])
-    if k >= 2 ** 31:
-        raise _lib.UbsError(f"{k} tile pairs exceed the 2^31 device limit")
-    ws.ensure_pairs(k)
+    if sync or ws.pair_cap == 0:
+        host = ws.counters[:3].cpu()  # K and n_visible (16 bytes)
+        k = int(host[0])
+        n_vis = int(host.view(torch.int32)[4])
+        if k >= 2 ** 32:
+            raise _lib.UbsError(f"{k} tile pairs exceed the 2^32 device limit")
+        ws.ensure_pairs(k)
+    else:
+        k, n_vis = None, None
     bb = ws.bin_buffers()
     with _Timed(timers, "bin_tiles"):
-        check(lib.ubs_bin_tiles(v, pb, bb, k, s), "ubs_bin_tiles")
+        check(lib.ubs_bin_tiles(v, pb, bb, -1 if k is None else k, s), "ubs_bin_tiles")
     ws.hit_clamp[:max(n, 1)].zero_()
     ib = ws.image_buffers()
     with _Timed(timers, "raster"):
@@ -359,10 +385,20 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
         with _Timed(timers, "fixup"):
             check(lib.ubs_raster_fixup(v, pb, bb, ib, s), "ubs_raster_fixup")
     npix = W * H
-    return Frame(view=v, width=W, height=H, n=n, n_visible=n_vis, n_pairs=k,
+    return Frame(view=v, width=W, height=H, n=n, n_visible_host=n_vis, n_pairs_host=k,
                  image=ws.image_buf[:npix * 3].view(H, W, 3), alpha_sum=ws.asum_buf[:npix].view(H, W),
                  t_stop=ws.tstop_buf[:npix].view(H, W), n_contrib=ws.ncontrib_buf[:npix].view(H, W),
                  hit_clamp=ws.hit_clamp[:n], ws=ws, raster_f64=ws.f64)
+
+
+def check_status(ws: Workspace) -> int:
+    """Raise if any asynchronous frame since the last reset overflowed its pair
+    buffers (its outputs are invalid; re-render with sync=True).  Syncs."""
+    st = int(ws.status.item())
+    if st & _lib.S_PAIR_OVERFLOW:
+        ws.status.zero_()
+        raise _lib.UbsError("tile-pair capacity exceeded by an asynchronous frame; re-render with sync=True")
+    return st
 
 
 def loss_image_grad(fr: Frame, target: torch.Tensor, lambda_ssim: float, scale: float):

@@ -243,3 +243,34 @@ def test_binning_large_list_parity():
     ref = O.render_frame(sc, cam, q, DEFAULT_SETTINGS)
     assert np.array_equal(got.tile_ids, ref["tile_ids"])
     assert np.array_equal(got.n_contrib, ref["count"])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_depth_ties_broken_by_id(precision):
+    # triplicated primitives have bit-identical depths: lexsort breaks the tie
+    # by id; the 32-bit-key sort must repair those runs exactly
+    base = quantize_f32(S.random_scene(6, 300, seed=23))
+    sc = base.take(np.concatenate([np.arange(300)] * 3))
+    cam = S.random_camera(96, 24)
+    q = S.random_query(6, 25)
+    assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, precision)
+
+
+def test_async_frames_match_sync():
+    # sync=False keeps K on the device; with adequate capacity the frame is identical
+    from paper_2510_03312_b200 import engine
+    import torch
+    sc = quantize_f32(S.random_scene(7, 5000, seed=31))
+    cam = S.random_camera(128, 32)
+    ws = engine.Workspace("cuda", "fp32")
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    q = S.random_query(7, 33)
+    a = engine.render_frame(ws, ds, cam, q, sync=True).image.clone()
+    b = engine.render_frame(ws, ds, cam, q, sync=False).image.clone()
+    engine.check_status(ws)
+    assert torch.equal(a, b)
+    # shrink capacity below K: the async frame must flag overflow instead of writing out of bounds
+    ws.pair_cap = 16
+    engine.render_frame(ws, ds, cam, q, sync=False)
+    with pytest.raises(Exception):
+        engine.check_status(ws)
