@@ -104,14 +104,12 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
             double eb = in_range ? g.beta_x * E : INFINITY;
             if (!isfinite(eb)) fl |= UBS_F_THIN;
             Rec32 r;
-            r.r0 = make_float4(__int_as_float(in_range ? (int)fxm : 0), __int_as_float(in_range ? (int)fym : 0),
+            r.r0 = make_float4(in_range ? (float)fxm : 0.f, in_range ? (float)fym : 0.f,
                                (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
-            r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)g.og);
+            r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)(v.set.tau_sq + E));
             r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
-            // r3: eb (m-error bound times beta), tau + E (support-edge band),
-            //     qc (lg2/ex2 approximation error of the alpha, relative), log2(og)
             const double qc = 0.6931471805599453 * g.beta_x * 4.76837158203125e-07 + 5.0e-7;
-            r.r3 = make_float4((float)eb, (float)(v.set.tau_sq + E), (float)qc, (float)log2(g.og));
+            r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2(g.og));
             reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
         }
         pb.flags[i] = fl;

@@ -171,7 +171,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits, uint32_t *__restrict__ fix_list,
                     uint32_t *__restrict__ fix_count) {
-    __shared__ float4 s0[kTileThreads], s1[kTileThreads], s2[kTileThreads], s3[kTileThreads];
+    __shared__ Rec32 srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
     __shared__ unsigned long long red[kTileThreads / 32];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
@@ -179,10 +179,15 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int px = tx * kTile + (threadIdx.x & (kTile - 1));
     const int py = ty * kTile + (threadIdx.x >> 4);
+    const float pxf = (float)px, pyf = (float)py;
     const bool inside = px < P.W && py < P.H;
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
     const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    // alpha below clamp_lo cannot be clamp-ambiguous unless its error bound is
+    // so large that err > kImgErrTol flags the pixel anyway: a(1+q) > clamp
+    // with a < clamp_lo implies a q / (1 - a) > clamp - clamp_lo >> kImgErrTol
+    const float clamp_lo = clamp - 0.05f;
     const float tmin = (float)P.tmin;
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
     float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
@@ -196,16 +201,18 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         if (q < end) {
             const uint32_t id = ids[q];
             const float4 *r = reinterpret_cast<const float4 *>(recs + id);
+            float4 *d = reinterpret_cast<float4 *>(srec + threadIdx.x);
             sid[threadIdx.x] = id;
-            s0[threadIdx.x] = __ldg(r);
-            s1[threadIdx.x] = __ldg(r + 1);
-            s2[threadIdx.x] = __ldg(r + 2);
-            s3[threadIdx.x] = __ldg(r + 3);
+            d[0] = __ldg(r);
+            d[1] = __ldg(r + 1);
+            d[2] = __ldg(r + 2);
+            d[3] = __ldg(r + 3);
         }
         __syncthreads();
         const int nb = (int)min((uint32_t)kTileThreads, end - b);
         if (!done) {
-            for (int j = 0; j < nb; ++j) {
+            const float4 *rp = reinterpret_cast<const float4 *>(srec);
+            for (int j = 0; j < nb; ++j, rp += 4) {
                 if (T < tmin_hi) {
                     const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
                     if (T < tmin) {
@@ -216,30 +223,30 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     if (T < tmin * (1.0f + band)) flag = true;
                 }
                 ++cnt;
-                const float4 r0 = s0[j], r1 = s1[j];
-                const float dx = (float)(px - __float_as_int(r0.x)) + r0.z;
-                const float dy = (float)(py - __float_as_int(r0.y)) + r0.w;
+                const float4 r0 = rp[0], r1 = rp[1];
+                const float dx = (pxf - r0.x) + r0.z;
+                const float dy = (pyf - r0.y) + r0.w;
                 const float y0 = fmaf(r1.x, dx, r1.y * dy);
                 const float y1 = r1.z * dy;
                 const float m = fmaf(y0, y0, y1 * y1);
-                const float4 r3 = s3[j];
                 if (m >= tau) {
-                    if (m < r3.y) flag = true;  // support edge within the m-error band
+                    if (m < r1.w) flag = true;  // support edge within the m-error band
                     continue;
                 }
-                const float4 r2 = s2[j];
+                const float4 r2 = rp[2], r3 = rp[3];
                 const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                 float a = ex2_approx(arg);
                 const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 1.2e-7f, r3.z));
-                float om;
-                if (a > clamp) {
-                    if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
-                    else flag = true;
-                    a = clamp;
-                    om = one_minus_clamp;
-                } else {
-                    if (a * (1.0f + qrel) > clamp) flag = true;
-                    om = 1.0f - a;
+                float om = 1.0f - a;
+                if (a > clamp_lo) {
+                    if (a > clamp) {
+                        if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
+                        else flag = true;
+                        a = clamp;
+                        om = one_minus_clamp;
+                    } else if (a * (1.0f + qrel) > clamp) {
+                        flag = true;
+                    }
                 }
                 err = fmaf(a * qrel, rcp_approx(om), err + 6.0e-8f);
                 const float w = a * T;
@@ -394,11 +401,11 @@ __device__ __forceinline__ void eval_splat(const Rec64 &r, int px, int py, doubl
 
 __device__ __forceinline__ void eval_splat(const Rec32 &r, int px, int py, float tau, float clamp,
                                            float one_minus_clamp, SplatEval<float> &e) {
-    e.dx = (float)(px - __float_as_int(r.r0.x)) + r.r0.z;
-    e.dy = (float)(py - __float_as_int(r.r0.y)) + r.r0.w;
+    e.dx = ((float)px - r.r0.x) + r.r0.z;
+    e.dy = ((float)py - r.r0.y) + r.r0.w;
     const float y0 = fmaf(r.r1.x, e.dx, r.r1.y * e.dy), y1 = r.r1.z * e.dy;
     e.m = fmaf(y0, y0, y1 * y1);
-    e.og = r.r1.w; e.bx = r.r2.x; e.c0 = r.r2.y; e.c1 = r.r2.z; e.c2 = r.r2.w;
+    e.og = r.r3.y; e.bx = r.r2.x; e.c0 = r.r2.y; e.c1 = r.r2.z; e.c2 = r.r2.w;
     e.pd0 = r.r1.x * y0;  // P d = U^T (U d)
     e.pd1 = fmaf(r.r1.y, y0, r.r1.z * y1);
     e.a = (e.m < tau) ? e.og * __expf(e.bx * log1pf(-e.m / tau)) : 0.f;

@@ -30,12 +30,13 @@ struct __align__(16) Rec64 {
 static_assert(sizeof(Rec64) == 80, "Rec64 layout");
 
 // fp32 raster record, 64 B = 4 x 16 B vector loads.
-//  r0: ix, iy (floor of mean2, int bits), ox, oy = 0.5 - frac(mean2)
-//      -> dx = float(px - ix) + ox is exact to ~1e-7 px at any image size
-//  r1: u00, u01, u11 (P = U^T U, m = (u00 dx + u01 dy)^2 + (u11 dy)^2), og
+//  r0: fx, fy = floor(mean2) as exact floats, ox, oy = 0.5 - frac(mean2)
+//      -> dx = (px - fx) + ox: the first difference is exact (integers
+//      < 2^24), so dx is accurate to ~1e-7 px at any image size
+//  r1: u00, u01, u11 (P = U^T U, m = (u00 dx + u01 dy)^2 + (u11 dy)^2),
+//      tau + E (E bounds |m32 - m64| over the splat's support)
 //  r2: beta_x, colour
-//  r3: eb = beta_x * E, E a bound on |m32 - m64| over the splat's support;
-//      flags
+//  r3: eb = beta_x * E, og, qc (lg2/ex2 approximation bound), log2(og)
 struct __align__(16) Rec32 {
     float4 r0, r1, r2, r3;
 };

@@ -250,7 +250,8 @@ class Workspace:
 
     def ensure_pairs(self, k: int):
         if k > self.pair_cap:
-            cap = max(k, int(self.pair_cap * 1.3), 1024)
+            # headroom so asynchronous frames of a sweep rarely outgrow it
+            cap = max(int(k * 1.2), int(self.pair_cap * 1.3), 1024)
             self.tile_ids = self._i(cap, torch.int32)
             self.entries = self._i(cap, torch.int64)
             self.pair_cap = cap
