@@ -150,19 +150,57 @@ constexpr int kBand = 8;  // tile columns per bucket band
 constexpr int kChunkRanks = 128;
 constexpr int kBinWarps = 8;
 
-// the buckets of one rank's rect: rows ty0..ty1 x bands b0..b1, row-major
-struct RankBuckets {
-    int ty0, b0, nbw, nb;
-    __device__ __forceinline__ int bucket(int j, int NB) const { return (ty0 + j / nbw) * NB + b0 + j % nbw; }
+// The (rank, bucket) pairs of a batch of 32 consecutive ranks, flattened in
+// rank-major order (and row-major bucket order inside a rank): lane j holds
+// rank j's rect; after a warp inclusive scan of the per-rank bucket counts,
+// flat index f belongs to the rank j with incl[j-1] <= f < incl[j] (found by
+// a 5-step shuffle binary search).  A warp step thus covers 32 pairs instead
+// of one rank's ~9 buckets.
+struct FlatBatch {
+    uint64_t q;      // this lane's rect
+    int nb, incl;    // this lane's bucket count and inclusive prefix
+    int total;       // pairs in the batch
 };
-__device__ __forceinline__ RankBuckets rank_buckets(uint64_t q) {
-    RankBuckets rb;
-    rb.b0 = (int)(q & 0xFFFF) / kBand;
-    rb.ty0 = (int)((q >> 16) & 0xFFFF);
+
+__device__ __forceinline__ int rank_bucket_count(uint64_t q, bool has) {
+    if (!has) return 0;
+    const int b0 = (int)(q & 0xFFFF) / kBand, ty0 = (int)((q >> 16) & 0xFFFF);
     const int b1 = (int)((q >> 32) & 0xFFFF) / kBand, ty1 = (int)((q >> 48) & 0xFFFF);
-    rb.nbw = b1 - rb.b0 + 1;
-    rb.nb = rb.nbw * (ty1 - rb.ty0 + 1);
-    return rb;
+    return (b1 - b0 + 1) * (ty1 - ty0 + 1);
+}
+
+__device__ __forceinline__ FlatBatch flat_batch(uint64_t q, bool has, int lane) {
+    FlatBatch fb;
+    fb.q = q;
+    fb.nb = rank_bucket_count(q, has);
+    int x = fb.nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    fb.incl = x;
+    fb.total = __shfl_sync(0xffffffffu, x, 31);
+    return fb;
+}
+
+// (rank lane j, bucket k) of flat index f (all lanes participate in the shuffles)
+__device__ __forceinline__ int flat_locate(const FlatBatch &fb, int f, int NB, int &j) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const int incl_mid = __shfl_sync(0xffffffffu, fb.incl, lo + step - 1);
+        if (incl_mid <= f) lo += step;
+    }
+    j = lo;  // first lane whose inclusive prefix exceeds f
+    const uint64_t q = __shfl_sync(0xffffffffu, fb.q, j);
+    const int excl = __shfl_sync(0xffffffffu, fb.incl - fb.nb, j);
+    const int b0 = (int)(q & 0xFFFF) / kBand, ty0 = (int)((q >> 16) & 0xFFFF);
+    const int nbw = (int)((q >> 32) & 0xFFFF) / kBand - b0 + 1;
+    const int i = f - excl;
+    // floor((i + 0.5) / nbw) in fp32 is exact for i < 2^16, nbw < 2^12
+    const int r = (int)(((float)i + 0.5f) * __frcp_rn((float)nbw));
+    return (ty0 + r) * NB + b0 + (i - r * nbw);
 }
 
 // (1) per-chunk bucket counts
@@ -188,11 +226,12 @@ bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restric
             has = tile_count[id] != 0;
             if (has) q = rect[id];
         }
-        const int nbatch = (int)min((int64_t)32, r1 - rb);
-        for (int j = 0; j < nbatch; ++j) {
-            if (!__shfl_sync(0xffffffffu, (int)has, j)) continue;
-            const RankBuckets b = rank_buckets(__shfl_sync(0xffffffffu, q, j));
-            for (int i = lane; i < b.nb; i += 32) atomicAdd(&cnt[b.bucket(i, NB)], 1u);
+        const FlatBatch fb = flat_batch(q, has, lane);
+        for (int f0 = 0; f0 < fb.total; f0 += 32) {
+            const int f = f0 + lane;
+            int j;
+            const int k = flat_locate(fb, min(f, fb.total - 1), NB, j);
+            if (f < fb.total) atomicAdd(&cnt[k], 1u);
         }
     }
     __syncwarp();
@@ -289,8 +328,9 @@ bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restr
     }
 }
 
-// (3) ordered scatter: each warp walks its chunk's ranks in order, lanes over
-// the rank's buckets (distinct within a rank), bumping private counters.
+// (3) ordered scatter over the same flattened (rank, bucket) order: lanes of
+// one step that hit the same bucket are ranked with __match_any_sync, so the
+// entries of a bucket are written in rank order.
 __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
                       const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
@@ -308,6 +348,7 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     const uint32_t *h = hist + (int64_t)chunk * nbk;
     for (int k = lane; k < nbk; k += 32) sfill[k] = h[k];
     __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int64_t r = rb + lane;
         uint64_t q = 0;
@@ -318,19 +359,20 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
             has = tile_count[id] != 0;
             if (has) q = rect[id];
         }
-        const int nbatch = (int)min((int64_t)32, r1 - rb);
-        for (int j = 0; j < nbatch; ++j) {
-            if (!__shfl_sync(0xffffffffu, (int)has, j)) continue;
-            const uint64_t qj = __shfl_sync(0xffffffffu, q, j);
-            const uint32_t idj = __shfl_sync(0xffffffffu, id, j);
-            const uint64_t ent = (uint64_t)idj | ((qj & 0xFFFFull) << 32) | (((qj >> 32) & 0xFFFFull) << 48);
-            const RankBuckets b = rank_buckets(qj);
-            for (int i = lane; i < b.nb; i += 32) {
-                const int k = b.bucket(i, NB);
-                const uint32_t pos = sfill[k];
-                entries[pos] = ent;
-                sfill[k] = pos + 1;
-            }
+        const uint64_t ent = (uint64_t)id | ((q & 0xFFFFull) << 32) | (((q >> 32) & 0xFFFFull) << 48);
+        const FlatBatch fb = flat_batch(q, has, lane);
+        for (int f0 = 0; f0 < fb.total; f0 += 32) {
+            const int f = f0 + lane;
+            const bool act = f < fb.total;
+            int j;
+            const int k = flat_locate(fb, act ? f : fb.total - 1, NB, j);
+            const uint64_t e = __shfl_sync(0xffffffffu, ent, j);
+            const unsigned grp = __match_any_sync(0xffffffffu, act ? k : -1);
+            const uint32_t base = sfill[act ? k : 0];
+            if (act) entries[base + __popc(grp & lt)] = e;
+            __syncwarp();
+            // the highest lane of each group publishes the new fill
+            if (act && (grp >> lane) == 1u) sfill[k] = base + __popc(grp);
             __syncwarp();
         }
     }

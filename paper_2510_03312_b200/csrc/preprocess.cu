@@ -20,7 +20,7 @@ namespace ubs {
 constexpr int kPreThreads = 128;
 
 template <int C, typename PT>
-__global__ void __launch_bounds__(kPreThreads)
+__global__ void __launch_bounds__(kPreThreads, 4)
 preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
     constexpr int P = 14 + 6 * C;
     __shared__ PT stage[kPreThreads * P];

@@ -66,14 +66,14 @@ __device__ __forceinline__ bool cholesky(const double (&A)[C][C], double (&L)[C]
 #pragma unroll
         for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
         if (!(s > 0.0)) return false;
-        double d = sqrt(s);
+        const double d = sqrt(s), inv_d = 1.0 / d;
         L[j][j] = d;
 #pragma unroll
         for (int i = j + 1; i < C; ++i) {
             double t = A[i][j];
 #pragma unroll
             for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
-            L[i][j] = t / d;
+            L[i][j] = t * inv_d;
         }
 #pragma unroll
         for (int i = 0; i < j; ++i) L[i][j] = 0.0;
@@ -84,18 +84,20 @@ __device__ __forceinline__ bool cholesky(const double (&A)[C][C], double (&L)[C]
 // inverse from a Cholesky factor: A^-1 = L^-T L^-1
 template <int C>
 __device__ __forceinline__ void chol_inverse(const double (&L)[C][C], double (&M)[C][C]) {
-    double Li[C][C];
+    double Li[C][C], inv[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) inv[j] = 1.0 / L[j][j];
 #pragma unroll
     for (int j = 0; j < C; ++j) {
 #pragma unroll
         for (int i = 0; i < C; ++i) Li[i][j] = 0.0;
-        Li[j][j] = 1.0 / L[j][j];
+        Li[j][j] = inv[j];
 #pragma unroll
         for (int i = j + 1; i < C; ++i) {
             double s = 0.0;
 #pragma unroll
             for (int k = j; k < i; ++k) s += L[i][k] * Li[k][j];
-            Li[i][j] = -s / L[i][i];
+            Li[i][j] = -s * inv[i];
         }
     }
 #pragma unroll
@@ -366,9 +368,10 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
     g.z = g.in_front ? g.tcam[2] : 1.0;
     const double z = g.z, x = g.tcam[0], y = g.tcam[1];
     const double fx = v.cam.fx, fy = v.cam.fy;
-    g.mean2[0] = fx * x / z + v.cam.cx;
-    g.mean2[1] = fy * y / z + v.cam.cy;
-    double J[2][3] = {{fx / z, 0.0, -fx * x / (z * z)}, {0.0, fy / z, -fy * y / (z * z)}};
+    const double iz = 1.0 / z;
+    g.mean2[0] = fx * x * iz + v.cam.cx;
+    g.mean2[1] = fy * y * iz + v.cam.cy;
+    double J[2][3] = {{fx * iz, 0.0, -fx * x * iz * iz}, {0.0, fy * iz, -fy * y * iz * iz}};
     for (int i = 0; i < 2; ++i)
         for (int k = 0; k < 3; ++k) g.V[i][k] = J[i][0] * Rc[k] + J[i][1] * Rc[3 + k] + J[i][2] * Rc[6 + k];
     double VC[2][3];
@@ -398,10 +401,10 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
         }
     }
     const double a = g.cov2[0], b = g.cov2[1], d = g.cov2[2];
-    const double det = a * d - b * b;
-    g.p2[0] = d / det;
-    g.p2[1] = -b / det;
-    g.p2[2] = a / det;
+    const double idet = 1.0 / (a * d - b * b);
+    g.p2[0] = d * idet;
+    g.p2[1] = -b * idet;
+    g.p2[2] = a * idet;
     g.radii[0] = sqrt(v.set.tau_sq * a);
     g.radii[1] = sqrt(v.set.tau_sq * d);
     const double mg = v.set.cull_margin;
