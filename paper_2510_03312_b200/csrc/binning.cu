@@ -147,7 +147,8 @@ constexpr int kBand = 8;  // tile columns per bucket band
 
 // Level-1 work unit: one warp per chunk of kChunkRanks consecutive ranks
 // (8 warps per CTA), each with a private shared-memory counter per bucket.
-constexpr int kChunkRanks = 128;
+constexpr int kChunkRanks = 128;             // ranks per warp slice
+constexpr int kCtaRanks = kChunkRanks * 8;   // ranks per CTA chunk (one histogram row)
 constexpr int kBinWarps = 8;
 
 // The (rank, bucket) pairs of a batch of 32 consecutive ranks, flattened in
@@ -203,20 +204,10 @@ __device__ __forceinline__ int flat_locate(const FlatBatch &fb, int f, int NB, i
     return (ty0 + r) * NB + b0 + (i - r * nbw);
 }
 
-// (1) per-chunk bucket counts
-__global__ void __launch_bounds__(kBinWarps * 32)
-bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
-                   const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G, int NB,
-                   int nbk, uint32_t *__restrict__ hist) {
-    extern __shared__ uint32_t scnt[];  // kBinWarps x nbk
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int chunk = blockIdx.x * kBinWarps + w;
-    uint32_t *cnt = scnt + w * nbk;
-    for (int k = lane; k < nbk; k += 32) cnt[k] = 0;
-    __syncwarp();
-    if (chunk >= G) return;
-    const int64_t nv = *n_visible;
-    const int64_t r0 = (int64_t)chunk * kChunkRanks, r1 = min(r0 + kChunkRanks, nv);
+// count the (rank, bucket) pairs of ranks [r0, r1) into cnt (shared atomics)
+__device__ __forceinline__ void count_slice(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
+                                            const uint32_t *__restrict__ tile_count, int64_t r0, int64_t r1,
+                                            int NB, uint32_t *cnt, int lane) {
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int64_t r = rb + lane;
         uint64_t q = 0;
@@ -234,9 +225,24 @@ bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restric
             if (f < fb.total) atomicAdd(&cnt[k], 1u);
         }
     }
-    __syncwarp();
-    uint32_t *h = hist + (int64_t)chunk * nbk;
-    for (int k = lane; k < nbk; k += 32) h[k] = cnt[k];
+}
+
+// (1) per-CTA-chunk bucket counts (8 warps count 128-rank slices into one array)
+__global__ void __launch_bounds__(kBinWarps * 32)
+bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
+                   const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G, int NB,
+                   int nbk, uint32_t *__restrict__ hist) {
+    extern __shared__ uint32_t scnt[];  // nbk
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) scnt[k] = 0;
+    __syncthreads();
+    const int64_t nv = *n_visible;
+    const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
+    const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
+    count_slice(order, rect, tile_count, r0, r1, NB, scnt, lane);
+    __syncthreads();
+    uint32_t *h = hist + (int64_t)blockIdx.x * nbk;
+    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) h[k] = scnt[k];
 }
 
 // (2) offsets[c][k] = bucket_start[k] + sum_{c' < c} hist[c'][k], in three
@@ -328,26 +334,39 @@ bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restr
     }
 }
 
-// (3) ordered scatter over the same flattened (rank, bucket) order: lanes of
-// one step that hit the same bucket are ranked with __match_any_sync, so the
-// entries of a bucket are written in rank order.
+// (3) ordered scatter.  Each warp recounts its 128-rank slice, a scan over
+// the 8 warps turns the CTA offsets into per-warp start offsets, then each
+// warp walks its slice in the flattened rank-major (rank, bucket) order;
+// lanes of one step that hit the same bucket are ranked with
+// __match_any_sync, so every bucket's entries come out in rank order.
 __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
                       const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
-                      int NB, int nbk, const uint32_t *__restrict__ hist, uint64_t *__restrict__ entries,
+                      int NB, int nbk, const uint32_t *__restrict__ off, uint64_t *__restrict__ entries,
                       const unsigned long long *__restrict__ n_pairs, int64_t capacity, uint32_t *status) {
     if (pairs_overflow(n_pairs, capacity, status)) return;
     extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int chunk = blockIdx.x * kBinWarps + w;
-    if (chunk >= G) return;
     const int64_t nv = *n_visible;
-    const int64_t r0 = (int64_t)chunk * kChunkRanks, r1 = min(r0 + kChunkRanks, nv);
-    if (r0 >= r1) return;
+    const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
+    if (c0 >= nv) return;
+    const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
     uint32_t *sfill = sfill_all + w * nbk;
-    const uint32_t *h = hist + (int64_t)chunk * nbk;
-    for (int k = lane; k < nbk; k += 32) sfill[k] = h[k];
+    for (int k = lane; k < nbk; k += 32) sfill[k] = 0;
     __syncwarp();
+    count_slice(order, rect, tile_count, r0, r1, NB, sfill, lane);
+    __syncthreads();
+    const uint32_t *o = off + (int64_t)blockIdx.x * nbk;
+    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) {
+        uint32_t run = o[k];
+#pragma unroll
+        for (int ww = 0; ww < kBinWarps; ++ww) {
+            const uint32_t c = sfill_all[ww * nbk + k];
+            sfill_all[ww * nbk + k] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int64_t r = rb + lane;
@@ -371,8 +390,7 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
             const uint32_t base = sfill[act ? k : 0];
             if (act) entries[base + __popc(grp & lt)] = e;
             __syncwarp();
-            // the highest lane of each group publishes the new fill
-            if (act && (grp >> lane) == 1u) sfill[k] = base + __popc(grp);
+            if (act && (grp >> lane) == 1u) sfill[k] = base + __popc(grp);  // highest lane of the group
             __syncwarp();
         }
     }
@@ -481,14 +499,14 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
         return UBS_E_ARGS;
     if (2 * (int64_t)G * nbk > bb->chunk_hist_capacity || (int64_t)nbk + 1 > bb->bucket_capacity)
         return UBS_E_CAPACITY;
-    if ((int64_t)G * kChunkRanks < v->n) return UBS_E_ARGS;  // chunk_count must cover n / kChunkRanks
+    if ((int64_t)G * kCtaRanks < v->n) return UBS_E_ARGS;  // chunk_count must cover n / kCtaRanks
     const size_t cnt_bytes = sizeof(uint32_t) * (size_t)kBinWarps * nbk;
     if (cnt_bytes > 200 * 1024) return UBS_E_ARGS;
-    cudaFuncSetAttribute(bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
     cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
-    const unsigned cta = (unsigned)((G + kBinWarps - 1) / kBinWarps);
-    bucket_hist_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count, pb->n_visible, G,
-                                                              NB, nbk, bb->chunk_hist);
+    const unsigned cta = (unsigned)G;
+    bucket_hist_kernel<<<cta, kBinWarps * 32, sizeof(uint32_t) * nbk, s>>>(bb->order, pb->rect, pb->tile_count,
+                                                                           pb->n_visible, G, NB, nbk,
+                                                                           bb->chunk_hist);
     // seg_scratch: segsum (kSegs x nbk) | segbase (kSegs x nbk) | total (nbk)
     uint32_t *segsum = bb->seg_scratch, *segbase = segsum + (size_t)kSegs * nbk, *total = segbase + (size_t)kSegs * nbk;
     uint32_t *off = bb->chunk_hist + (size_t)G * nbk;  // second half of chunk_hist

@@ -234,7 +234,7 @@ class Workspace:
             self.tile_cap = ntiles
             self.temp_bytes = 0
 
-    CHUNK_RANKS = 128   # ranks per level-1 binning chunk (one warp each; csrc/binning.cu kChunkRanks)
+    CHUNK_RANKS = 1024  # ranks per level-1 binning CTA chunk (csrc/binning.cu kCtaRanks)
     BAND = 8            # tile columns per level-1 bucket (csrc/binning.cu kBand)
 
     def ensure_chunks(self, n: int, width: int, height: int):
