@@ -97,10 +97,18 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
             const double u11 = sqrt(fmax(g.p2[2] - u01 * u01, 0.0));
             const double fxm = floor(g.mean2[0]), fym = floor(g.mean2[1]);
             const bool in_range = fabs(g.mean2[0]) < 4.0e6 && fabs(g.mean2[1]) < 4.0e6 && isfinite(u11);
-            const double eps32 = 5.9604644775390625e-08;  // 2^-24
+            // E bounds |m32 - m64| over the support (m < tau => |dx| < rx, |dy| < ry,
+            // |y0|, |y1| < sqrt(tau)), with u = 2^-24 the fp32 unit roundoff:
+            //   dx = (px - fx) + ox        |d dx| <= u (|dx| + 0.5)   (ox rounded, one add)
+            //   y0 = fma(u00, dx, u01 dy)  |d y0| <= u (|u00|(2|dx| + .5) + |u01|(3|dy| + .5) + |y0|)
+            //   y1 = u11 dy                |d y1| <= u (|u11|(2|dy| + .5) + |y1|)
+            //   m  = fma(y0, y0, y1 y1)    |d m|  <= 2|y0||d y0| + 2|y1||d y1| + 2 u tau
+            // (u.. rounded to fp32 included), times a 1.25 safety factor.
+            const double u = 5.9604644775390625e-08;
             const double st = sqrt(v.set.tau_sq);
-            double E = 8.0 * eps32 * (st * (fabs(u00) * (g.radii[0] + 1.0) +
-                                            (fabs(u01) + fabs(u11)) * (g.radii[1] + 1.0)) + v.set.tau_sq);
+            const double rx = g.radii[0], ry = g.radii[1];
+            double E = 1.25 * u * (2.0 * st * (fabs(u00) * (2.0 * rx + 0.5) + fabs(u01) * (3.0 * ry + 0.5) + st) +
+                                   2.0 * st * (fabs(u11) * (2.0 * ry + 0.5) + st) + 2.0 * v.set.tau_sq);
             double eb = in_range ? g.beta_x * E : INFINITY;
             if (!isfinite(eb)) fl |= UBS_F_THIN;
             Rec32 r;
@@ -108,7 +116,10 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
                                (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
             r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)(v.set.tau_sq + E));
             r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
-            const double qc = 0.6931471805599453 * g.beta_x * 4.76837158203125e-07 + 5.0e-7;
+            // qc: lg2.approx absolute error 2^-22.6 (near 1) times ln2 beta, ex2.approx
+            // relative error 2^-22, og / log2(og) representation; the |arg|-relative
+            // parts are added per visit in the raster (2.1e-7 |arg|)
+            const double qc = 0.6931471805599453 * g.beta_x * 1.6e-7 + 4.0e-7;
             r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2(g.og));
             reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
         }

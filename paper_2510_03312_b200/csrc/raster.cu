@@ -158,10 +158,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 // Per visit (in support): alpha = 2^(beta * lg2(1 - m/tau) + log2(og)) with
-// the MUFU lg2/ex2 approximations; their error (qc, and 1.2e-7 per unit of
+// the MUFU lg2/ex2 approximations; their error (qc, and 2.1e-7 per unit of
 // the exponent) is part of the per-visit relative alpha bound
-//     q = eb / (tau - m) + qc + 1.2e-7 |arg|,
-// and err accumulates q * a / (1 - a), the first-order relative error of T.
+//     q = eb / (tau - m) + qc + 2.1e-7 |arg|,
+// and err accumulates q a / (1 - a) + 2u, the first-order relative error of T.
 // Near the cut (T < tmin * (1 + 4e-3)) the exact band test runs; elsewhere a
 // single compare.  A pixel whose bound exceeds kImgErrTol is flagged anyway,
 // so the coarse prefilter width can never hide a needed band test.
@@ -214,7 +214,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             const float4 *rp = reinterpret_cast<const float4 *>(srec);
             for (int j = 0; j < nb; ++j, rp += 4) {
                 if (T < tmin_hi) {
-                    const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
+                    const float band = err + 1.0e-6f;
                     if (T < tmin) {
                         if (T > tmin * (1.0f - band)) flag = true;
                         done = true;
@@ -236,7 +236,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 const float4 r2 = rp[2], r3 = rp[3];
                 const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                 float a = ex2_approx(arg);
-                const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 1.2e-7f, r3.z));
+                const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
                 float om = 1.0f - a;
                 if (a > clamp_lo) {
                     if (a > clamp) {
@@ -248,7 +248,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                         flag = true;
                     }
                 }
-                err = fmaf(a * qrel, rcp_approx(om), err + 6.0e-8f);
+                err = fmaf(a * qrel, rcp_approx(om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
                 const float w = a * T;
                 a0 = fmaf(w, r2.y, a0);
                 a1 = fmaf(w, r2.z, a1);
@@ -258,13 +258,13 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             }
             if (!done && T < tmin) {
                 // crossed on the batch's last splat: the next check would stop
-                const float band = fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f);
+                const float band = err + 1.0e-6f;
                 if (T > tmin * (1.0f - band)) flag = true;
                 done = true;
             }
         }
     }
-    if (inside && !done && T < tmin * (1.0f + fmaf((float)cnt, 6.0e-8f, err + 1.0e-6f))) flag = true;
+    if (inside && !done && T < tmin * (1.0f + err + 1.0e-6f)) flag = true;
     if (err > kImgErrTol) flag = true;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
@@ -289,22 +289,30 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
 }
 
-// fp64 replay of flagged pixels: one warp per pixel.  Lanes evaluate 32
-// splats' alphas in parallel (reference formula and rounding), then the warp
-// blends them sequentially in list order so T matches tile_forward bit for bit.
+// fp64 replay of flagged pixels: one warp per pixel, chunks of 32 splats.
+//  1. lanes evaluate alpha_k (reference formula and rounding, clamp applied)
+//     and 1 - alpha_k in parallel;
+//  2. lane 0 runs the only truly sequential part, T_{k+1} = T_k (1 - alpha_k),
+//     exactly as tile_forward rounds it, finds the early-out index and
+//     publishes T_k through shared memory;
+//  3. lanes accumulate w_k = alpha_k T_k times colour with a warp reduction
+//     (summation order differs from the reference only at the 1e-16 level;
+//     T, the contributor count and the clamp flags are exact).
 __global__ void __launch_bounds__(256)
 raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec64 *__restrict__ recs, const uint32_t *__restrict__ fix_list,
                     const uint32_t *__restrict__ fix_count, float *__restrict__ image, float *__restrict__ asum,
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits) {
+    __shared__ double s_om[8][32], s_T[8][33];
+    __shared__ int s_stop[8];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const uint32_t nfix = *fix_count;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix; w += warps) {
-        const uint32_t pix = fix_list[w];
+    for (uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfix; wi += warps) {
+        const uint32_t pix = fix_list[wi];
         const int py = pix / P.W, px = pix - py * P.W;
         const int tile = (py / kTile) * P.TX + px / kTile;
         const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
@@ -312,12 +320,12 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
         int cnt = 0;
         bool done = false;
+        uint32_t q = start + lane;
+        uint32_t id = q < end ? ids[q] : 0u;
         for (uint32_t b = start; b < end && !done; b += 32) {
-            const uint32_t q = b + lane;
             double a = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
-            uint32_t id = 0;
-            if (q < end) {
-                id = ids[q];
+            const bool valid = q < end;
+            if (valid) {
                 const Rec64 r = recs[id];
                 const double dx = sub(pxc, r.mx), dy = sub(pyc, r.my);
                 const double m = add(add(mul(mul(r.p00, dx), dx), mul(mul(mul(2.0, r.p01), dx), dy)),
@@ -325,26 +333,47 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 if (m < tau) a = mul(r.og, exp(mul(r.bx, log1p(-m / tau))));
                 cr = r.cr; cg = r.cg; cb = r.cb;
             }
+            const uint32_t my_id = id;
+            // prefetch the next chunk's id while the chain runs
+            q += 32;
+            id = q < end ? ids[q] : 0u;
+            const bool clamped = a > clamp;
+            if (clamped) a = clamp;
+            s_om[wl][lane] = sub(1.0, a);
+            __syncwarp();
             const int nb = (int)min(32u, end - b);
-            for (int k = 0; k < nb; ++k) {
-                if (T < tmin) { done = true; break; }
-                ++cnt;
-                double ak = __shfl_sync(0xffffffffu, a, k);
-                const double ck0 = __shfl_sync(0xffffffffu, cr, k);
-                const double ck1 = __shfl_sync(0xffffffffu, cg, k);
-                const double ck2 = __shfl_sync(0xffffffffu, cb, k);
-                if (ak == 0.0) continue;  // m >= tau (or underflow): no-op in tile_forward
-                if (ak > clamp) {
-                    ak = clamp;
-                    if (lane == k) hit[id] = 1;
+            if (lane == 0) {
+                double t = T;
+                int k = 0;
+                for (; k < nb; ++k) {
+                    if (t < tmin) break;
+                    s_T[wl][k] = t;
+                    t = mul(t, s_om[wl][k]);  // 1 - 0 == 1 exactly: a no-op splat leaves t unchanged
                 }
-                const double wgt = mul(ak, T);
-                a0 = add(a0, mul(wgt, ck0));
-                a1 = add(a1, mul(wgt, ck1));
-                a2 = add(a2, mul(wgt, ck2));
-                ws = add(ws, wgt);
-                T = mul(T, sub(1.0, ak));
+                s_T[wl][32] = t;
+                s_stop[wl] = k;
             }
+            __syncwarp();
+            const int stop = s_stop[wl];
+            cnt += stop;
+            done = stop < nb;
+            double w = 0.0;
+            if (lane < stop && a != 0.0) {
+                w = mul(a, s_T[wl][lane]);
+                if (clamped) hit[my_id] = 1;
+            }
+            double v0 = w * cr, v1 = w * cg, v2 = w * cb, v3 = w;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+                v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+                v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+                v3 += __shfl_xor_sync(0xffffffffu, v3, o);
+            }
+            a0 += v0; a1 += v1; a2 += v2; ws += v3;
+            T = s_T[wl][32];
+            if (!done && T < tmin) done = true;  // crossed on the chunk's last splat
+            __syncwarp();
         }
         if (lane == 0) {
             image[3 * (int64_t)pix] = (float)add(a0, mul(T, P.bg[0]));
