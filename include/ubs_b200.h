@@ -66,6 +66,7 @@ enum {
     UBS_F_FLOOR3 = 4,       /* SliceCache.floored (slicing.py:215) */
     UBS_F_FLOOR2 = 8,       /* ProjectionCache.floored (raster.py:116) */
     UBS_F_THIN = 16,        /* fp32 raster guard: pixels touching this splat are re-done in fp64 */
+    UBS_F_GATE_SAT = 32,    /* some d_gate == 1: the gate adjoint is 0 * inf (NaN), gradients.py:225-226 */
 };
 
 /* device status bits (UbsBinBuffers.status) */
@@ -161,6 +162,9 @@ typedef struct UbsGradBuffers {
     double reg_opacity;  /* loss_scale * lambda_o   (0 to skip, gradients.py:120-123) */
     double reg_scale;    /* loss_scale * lambda_sigma */
     uint32_t *nonfinite; /* [1] set to 1 when any gradient is not finite */
+    const uint16_t *flags; /* UbsPrimBuffers.flags of this view (for the skip test), or NULL */
+    uint32_t *active;    /* n scratch: primitives the chain must visit, or NULL (visit all) */
+    uint32_t *active_count; /* [1] scratch counter */
 } UbsGradBuffers;
 
 /* --- entry points --- */
@@ -203,7 +207,10 @@ size_t ubs_loss_scratch_bytes(int32_t height, int32_t width, int32_t f64);
 int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                         const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t s);
 
-/* chain 2D gradients back to raw parameters (fp64), += into grad_params */
+/* chain 2D gradients back to raw parameters (fp64), += into grad_params.
+ * With gb->active set, only primitives with a nonzero screen-space gradient
+ * or a saturated gate are visited (the chain of an all-zero 2D gradient is
+ * exactly zero otherwise, gradients.py:179-280). */
 int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int32_t add_regularisers, ubs_stream_t s);
 
 /* --- training-step epilogue (optim.py:115-135, gradients.py:120-123) --- */

@@ -15,7 +15,7 @@ from . import build as _build
 
 UBS_OK, UBS_E_ARGS, UBS_E_CUDA, UBS_E_CAPACITY = 0, -1, -2, -3
 S_PAIR_OVERFLOW = 1
-F_VISIBLE, F_DEGENERATE, F_FLOOR3, F_FLOOR2, F_THIN = 1, 2, 4, 8, 16
+F_VISIBLE, F_DEGENERATE, F_FLOOR3, F_FLOOR2, F_THIN, F_GATE_SAT = 1, 2, 4, 8, 16, 32
 DEBUG_STRIDE = 32
 GRAD2D_STRIDE = 12
 REC32_BYTES, REC64_BYTES = 64, 80
@@ -67,7 +67,7 @@ class UbsImageBuffers(Structure):
 class UbsGradBuffers(Structure):
     _fields_ = [("g_image", c_void_p), ("grad2d", c_void_p), ("grad_params", c_void_p), ("grad_f64", c_int32),
                 ("grad2d_f64", c_int32), ("reg_opacity", c_double), ("reg_scale", c_double),
-                ("nonfinite", c_void_p)]
+                ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p)]
 
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares

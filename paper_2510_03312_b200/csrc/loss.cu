@@ -26,12 +26,17 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {
     return i >= n ? period - i : i;
 }
 
-// forward blur along an axis of length n with element stride `stride`
+// forward blur along an axis of length n (interior points skip the reflect)
 template <typename T, typename F>
 __device__ __forceinline__ T blur_fwd(const BlurTaps &w, int j, int n, F get) {
     T s = 0;
+    if (j >= 5 && j + 5 < n) {
 #pragma unroll
-    for (int t = 0; t < 11; ++t) s += (T)w.k[t] * get(reflect_idx(j - 5 + t, n));
+        for (int t = 0; t < 11; ++t) s += (T)w.k[t] * get(j - 5 + t);
+    } else {
+#pragma unroll
+        for (int t = 0; t < 11; ++t) s += (T)w.k[t] * get(reflect_idx(j - 5 + t, n));
+    }
     return s;
 }
 
@@ -39,6 +44,12 @@ __device__ __forceinline__ T blur_fwd(const BlurTaps &w, int j, int n, F get) {
 template <typename T, typename F>
 __device__ __forceinline__ T blur_adj(const BlurTaps &w, int j, int n, F get) {
     T s = 0;
+    if (n >= 12 && j >= 6 && j + 7 < n) {
+        // interior: only the direct source p = j contributes, all taps in range
+#pragma unroll
+        for (int t = 0; t < 11; ++t) s += (T)w.k[t] * get(j + 5 - t);
+        return s;
+    }
     if (n < 12) {
         for (int r = 0; r < n; ++r)
 #pragma unroll
@@ -75,9 +86,10 @@ __global__ void ssim_hblur_kernel(const T *__restrict__ a, const T *__restrict__
     const int x = (int)(yx % W);
     const int64_t row = (yx / W) * W;
     T s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+    const bool interior = x >= 5 && x + 5 < W;
 #pragma unroll
     for (int t = 0; t < 11; ++t) {
-        const int64_t q = (row + reflect_idx(x - 5 + t, W)) * 3 + c;
+        const int64_t q = (row + (interior ? x - 5 + t : reflect_idx(x - 5 + t, W))) * 3 + c;
         const T av = a[q], bv = b[q], k = (T)w.k[t];
         s0 += k * av;
         s1 += k * bv;

@@ -17,23 +17,67 @@ struct AdamCols {
     uint64_t frozen_mask;  // columns not updated (freeze_shapes)
 };
 
+// fp32 path: the flat n*P buffer is processed as float4 quads (16 B vector
+// loads of param/grad/m/v); each quad's column comes from one division, the
+// per-column learning rate and clamp/frozen bits from shared memory.
+__global__ void __launch_bounds__(256)
+adam_f32_kernel(float *__restrict__ params, const float *__restrict__ grads, float *__restrict__ m,
+                float *__restrict__ v, int64_t total, int P, AdamCols cols, float b1, float b2, float inv_bc1,
+                float inv_bc2, float eps) {
+    __shared__ float slr[64];
+    __shared__ uint64_t smask[2];
+    if (threadIdx.x < 64) slr[threadIdx.x] = cols.lr[threadIdx.x];
+    if (threadIdx.x == 0) { smask[0] = cols.clamp_mask; smask[1] = cols.frozen_mask; }
+    __syncthreads();
+    const int64_t nq = total / 4;
+    for (int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; qi < nq; qi += (int64_t)gridDim.x * blockDim.x) {
+        float4 pp = reinterpret_cast<float4 *>(params)[qi];
+        const float4 gg = reinterpret_cast<const float4 *>(grads)[qi];
+        float4 mm = reinterpret_cast<float4 *>(m)[qi];
+        float4 vv = reinterpret_cast<float4 *>(v)[qi];
+        int c = (int)((qi * 4) % P);
+        float *pe = &pp.x, *me = &mm.x, *ve = &vv.x;
+        const float *ge = &gg.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if ((smask[1] >> c) & 1ull) {
+                pe[e] = fminf(fmaxf(pe[e], -5.0f), 5.0f);  // frozen: clamp only (optim.py:122-135)
+            } else {
+                const float g = ge[e];
+                const float mi = fmaf(b1, me[e], (1.0f - b1) * g);
+                const float vi = fmaf(b2, ve[e], (1.0f - b2) * g * g);
+                me[e] = mi;
+                ve[e] = vi;
+                float p = pe[e] - __fdividef(slr[c] * mi * inv_bc1, sqrtf(vi * inv_bc2) + eps);
+                if ((smask[0] >> c) & 1ull) p = fminf(fmaxf(p, -5.0f), 5.0f);
+                pe[e] = p;
+            }
+            c = (c + 1 == P) ? 0 : c + 1;
+        }
+        reinterpret_cast<float4 *>(params)[qi] = pp;
+        reinterpret_cast<float4 *>(m)[qi] = mm;
+        reinterpret_cast<float4 *>(v)[qi] = vv;
+    }
+}
+
+// generic path (fp64 parameters or gradients, or a tail): one element per thread
 template <typename PT, typename GT>
 __global__ void adam_kernel(PT *__restrict__ params, const GT *__restrict__ grads, float *__restrict__ m,
-                            float *__restrict__ v, int64_t total, int P, AdamCols cols, float b1, float b2,
-                            float bc1, float bc2, float eps) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+                            float *__restrict__ v, int64_t begin, int64_t total, int P, AdamCols cols, float b1,
+                            float b2, float inv_bc1, float inv_bc2, float eps) {
+    for (int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
         const int c = (int)(i % P);
         if ((cols.frozen_mask >> c) & 1ull) {
-            // frozen shapes are not updated but still clamped (optim.py:122-135)
             params[i] = (PT)fmin(fmax((double)params[i], -5.0), 5.0);
             continue;
         }
-        const float g = (float)grads[i];
-        const float mi = b1 * m[i] + (1.0f - b1) * g;
-        const float vi = b2 * v[i] + (1.0f - b2) * g * g;
+        const double g = (double)grads[i];
+        const float mi = fmaf(b1, m[i], (1.0f - b1) * (float)g);
+        const float vi = fmaf(b2, v[i], (1.0f - b2) * (float)(g * g));
         m[i] = mi;
         v[i] = vi;
-        double p = (double)params[i] - (double)cols.lr[c] * ((double)mi / bc1) / (sqrt((double)vi / bc2) + eps);
+        double p = (double)params[i] - (double)cols.lr[c] * ((double)mi * inv_bc1) / (sqrt((double)vi * inv_bc2) + eps);
         if ((cols.clamp_mask >> c) & 1ull) p = fmin(fmax(p, -5.0), 5.0);
         params[i] = (PT)p;
     }
@@ -68,6 +112,7 @@ extern "C" int ubs_adam_step(void *params, int32_t param_f64, const void *grads,
     if (n == 0) return UBS_OK;
     const int C = n_dims - 3, P = 14 + 6 * C;
     AdamCols cols{};
+    (void)C;
     // column -> learning-rate group, PARAM_FIELDS order
     int c = 0;
     auto put = [&](int count, double lr, bool clampc) {
@@ -91,18 +136,26 @@ extern "C" int ubs_adam_step(void *params, int32_t param_f64, const void *grads,
     put(1, opa, false);      // opacity_raw
     put(3, oth, false);      // color
     const float b1 = 0.9f, b2 = 0.999f;
-    const float bc1 = (float)(1.0 - pow(0.9, step)), bc2 = (float)(1.0 - pow(0.999, step));
+    const float inv_bc1 = (float)(1.0 / (1.0 - pow(0.9, step))), inv_bc2 = (float)(1.0 / (1.0 - pow(0.999, step)));
     const int64_t total = n * P;
-    const int thr = 256;
-    const int64_t want = (total + thr - 1) / thr;
-    const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
     cudaStream_t s = (cudaStream_t)stream;
-    if (param_f64) {
-        if (grad_f64) adam_kernel<double, double><<<blocks, thr, 0, s>>>((double *)params, (const double *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
-        else adam_kernel<double, float><<<blocks, thr, 0, s>>>((double *)params, (const float *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
-    } else {
-        if (grad_f64) adam_kernel<float, double><<<blocks, thr, 0, s>>>((float *)params, (const double *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
-        else adam_kernel<float, float><<<blocks, thr, 0, s>>>((float *)params, (const float *)grads, m, v, total, P, cols, b1, b2, bc1, bc2, 1e-8f);
+    const unsigned grid = 148 * 8;
+    int64_t begin = 0;
+    const bool aligned = ((uintptr_t)params % 16 == 0) && ((uintptr_t)grads % 16 == 0) && ((uintptr_t)m % 16 == 0) &&
+                         ((uintptr_t)v % 16 == 0);
+    if (!param_f64 && !grad_f64 && aligned) {
+        adam_f32_kernel<<<grid, 256, 0, s>>>((float *)params, (const float *)grads, m, v, total, P, cols, b1, b2,
+                                             inv_bc1, inv_bc2, 1e-8f);
+        begin = (total / 4) * 4;
+    }
+    if (begin < total) {
+        if (param_f64) {
+            if (grad_f64) adam_kernel<double, double><<<grid, 256, 0, s>>>((double *)params, (const double *)grads, m, v, begin, total, P, cols, b1, b2, inv_bc1, inv_bc2, 1e-8f);
+            else adam_kernel<double, float><<<grid, 256, 0, s>>>((double *)params, (const float *)grads, m, v, begin, total, P, cols, b1, b2, inv_bc1, inv_bc2, 1e-8f);
+        } else {
+            if (grad_f64) adam_kernel<float, double><<<grid, 256, 0, s>>>((float *)params, (const double *)grads, m, v, begin, total, P, cols, b1, b2, inv_bc1, inv_bc2, 1e-8f);
+            else adam_kernel<float, float><<<grid, 256, 0, s>>>((float *)params, (const float *)grads, m, v, begin, total, P, cols, b1, b2, inv_bc1, inv_bc2, 1e-8f);
+        }
     }
     UBS_CUDA_CHECK();
     return UBS_OK;

@@ -78,7 +78,10 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
                       (g.floored3 ? UBS_F_FLOOR3 : 0) | (g.floored2 ? UBS_F_FLOOR2 : 0);
         if constexpr (C > 0) {
 #pragma unroll
-            for (int k = 0; k < C; ++k) fl |= (g.s_tanh[k] > 0.0 ? 1 : 0) << (8 + k);
+            for (int k = 0; k < C; ++k) {
+                fl |= (g.s_tanh[k] > 0.0 ? 1 : 0) << (8 + k);
+                if (g.d_gate[k] == 1.0) fl |= UBS_F_GATE_SAT;
+            }
         }
 
         // raster records (only read for visible primitives)

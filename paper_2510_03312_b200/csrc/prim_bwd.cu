@@ -57,14 +57,44 @@ __device__ inline void floor_adjoint(const double (&lam)[D], const double (&E)[D
         }
 }
 
+// Compaction: primitives whose chain can be nonzero (any of the 10 screen-space
+// gradients nonzero, a saturated gate, or regularisers requested).
+template <typename GT>
+__global__ void __launch_bounds__(256)
+prim_active_kernel(const GT *__restrict__ grad2d, const uint16_t *__restrict__ flags, int64_t n, int add_reg,
+                   uint32_t *__restrict__ active, uint32_t *__restrict__ count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool need = false;
+    if (i < n) {
+        const GT *q = grad2d + i * kGrad2dStride;
+        bool nz = false;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) nz |= (q[k] != (GT)0);
+        need = nz || add_reg || (flags[i] & UBS_F_GATE_SAT);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(count, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (need) active[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+}
+
 template <int C, typename PT, typename GT, typename OT>
 __global__ void __launch_bounds__(128)
 prim_bwd_kernel(const UbsView v, const GT *__restrict__ grad2d, OT *__restrict__ out, int add_reg,
-                double reg_o, double reg_s, uint32_t *__restrict__ nonfinite) {
+                double reg_o, double reg_s, uint32_t *__restrict__ nonfinite, const uint32_t *__restrict__ active,
+                const uint32_t *__restrict__ active_count) {
     constexpr int P = 14 + 6 * C;
     constexpr int CC = PrimGeom<C>::CC;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= v.n) return;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (active) {
+        if (i >= (int64_t)*active_count) return;
+        i = active[i];
+    } else if (i >= v.n) {
+        return;
+    }
     const PT *rec = reinterpret_cast<const PT *>(v.params) + i * P;
     PrimGeom<C> g;
     double mu_x[3];
@@ -334,20 +364,30 @@ prim_bwd_kernel(const UbsView v, const GT *__restrict__ grad2d, OT *__restrict__
 template <int C, typename PT>
 static void launch_bwd(const UbsView &v, const UbsGradBuffers &gb, int add_reg, bool g2d_f64, cudaStream_t s) {
     const unsigned blocks = (unsigned)((v.n + 127) / 128);
+    if (gb.active) {
+        const unsigned ab = (unsigned)((v.n + 255) / 256);
+        cudaMemsetAsync(gb.active_count, 0, sizeof(uint32_t), s);
+        if (g2d_f64)
+            prim_active_kernel<double><<<ab, 256, 0, s>>>((const double *)gb.grad2d, gb.flags, v.n, add_reg, gb.active,
+                                                          gb.active_count);
+        else
+            prim_active_kernel<float><<<ab, 256, 0, s>>>((const float *)gb.grad2d, gb.flags, v.n, add_reg, gb.active,
+                                                         gb.active_count);
+    }
     if (g2d_f64) {
         if (gb.grad_f64)
             prim_bwd_kernel<C, PT, double, double><<<blocks, 128, 0, s>>>(
-                v, (const double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite);
+                v, (const double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
         else
             prim_bwd_kernel<C, PT, double, float><<<blocks, 128, 0, s>>>(
-                v, (const double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite);
+                v, (const double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
     } else {
         if (gb.grad_f64)
             prim_bwd_kernel<C, PT, float, double><<<blocks, 128, 0, s>>>(
-                v, (const float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite);
+                v, (const float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
         else
             prim_bwd_kernel<C, PT, float, float><<<blocks, 128, 0, s>>>(
-                v, (const float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite);
+                v, (const float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
     }
 }
 
@@ -358,6 +398,7 @@ using namespace ubs;
 extern "C" int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int32_t add_regularisers,
                                  ubs_stream_t stream) {
     if (!v || !gb || !gb->grad2d || !gb->grad_params) return UBS_E_ARGS;
+    if (gb->active && (!gb->flags || !gb->active_count)) return UBS_E_ARGS;
     if (v->n == 0) return UBS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const bool pf64 = v->param_f64 != 0, g64 = gb->grad2d_f64 != 0;

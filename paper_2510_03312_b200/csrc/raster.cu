@@ -437,7 +437,7 @@ __device__ __forceinline__ void eval_splat(const Rec32 &r, int px, int py, float
     e.og = r.r3.y; e.bx = r.r2.x; e.c0 = r.r2.y; e.c1 = r.r2.z; e.c2 = r.r2.w;
     e.pd0 = r.r1.x * y0;  // P d = U^T (U d)
     e.pd1 = fmaf(r.r1.y, y0, r.r1.z * y1);
-    e.a = (e.m < tau) ? e.og * __expf(e.bx * log1pf(-e.m / tau)) : 0.f;
+    e.a = (e.m < tau) ? ex2_approx(fmaf(e.bx, lg2_approx(1.0f - e.m / tau), r.r3.w)) : 0.f;
     if (e.a > clamp) {
         e.a = clamp;
         e.om = one_minus_clamp;  // same factor the forward multiplied T by
@@ -447,7 +447,31 @@ __device__ __forceinline__ void eval_splat(const Rec32 &r, int px, int py, float
 }
 
 __device__ __forceinline__ double log1p_(double x) { return log1p(x); }
-__device__ __forceinline__ float log1p_(float x) { return log1pf(x); }
+__device__ __forceinline__ float log1p_(float x) { return 0.69314718f * lg2_approx(1.0f + x); }
+__device__ __forceinline__ double rcp_(double x) { return 1.0 / x; }
+__device__ __forceinline__ float rcp_(float x) { return __frcp_rn(x); }
+
+// Reduce-scatter of 16 per-lane values over the warp in 16 shuffles (instead
+// of 16 x 5 for 16 all-reduces): at each level a lane keeps the half of its
+// vector selected by its lane bit and adds the partner's copy of that half.
+// Returns the full warp sum of component idx(lane), idx = bits 4..1 of lane;
+// lanes 2i and 2i+1 hold component i.
+template <typename T>
+__device__ __forceinline__ T warp_reduce_scatter16(T (&v)[16], int lane, int &idx) {
+#pragma unroll
+    for (int lvl = 0; lvl < 4; ++lvl) {
+        const int half = 8 >> lvl, off = 16 >> lvl;
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const T send = upper ? v[i] : v[i + half];
+            const T keep = upper ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
 
 template <typename Real>
 __global__ void __launch_bounds__(kTileThreads)
@@ -480,6 +504,9 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
     }
     __syncthreads();
     const int max_cnt = smax;
+    int warp_cnt = my_cnt;  // this warp's largest contributor count: splats beyond it are skipped
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) warp_cnt = max(warp_cnt, __shfl_xor_sync(0xffffffffu, warp_cnt, o));
     const Real tau = (Real)P.tau, clamp = (Real)P.clamp, one_minus_clamp = (Real)(1.0 - P.clamp);
     Real suffix = (g0 * (Real)P.bg[0] + g1 * (Real)P.bg[1] + g2 * (Real)P.bg[2]) * T;
     const int lane = threadIdx.x & 31;
@@ -493,8 +520,8 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
             srec[threadIdx.x] = recs[id];
         }
         __syncthreads();
-        for (int j = hi - 1; j >= lo; --j) {
-            Real v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = min(hi, warp_cnt) - 1; j >= lo; --j) {
+            Real v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             bool contrib = false;
             if (j < my_cnt) {
                 SplatEval<Real> e;
@@ -502,19 +529,20 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
                 if (e.a != (Real)0) {
                     // _tiles.py:97-127, T_i rebuilt by division from T_final
                     contrib = true;
-                    const Real ti = T / e.om;
+                    const Real iom = rcp_(e.om);
+                    const Real ti = T * iom;
                     const Real w = e.a * ti;
                     v[7] = w * g0;
                     v[8] = w * g1;
                     v[9] = w * g2;
                     const Real gc = g0 * e.c0 + g1 * e.c1 + g2 * e.c2;
-                    const Real ga = gc * ti - suffix / e.om;
+                    const Real ga = gc * ti - suffix * iom;
                     suffix += gc * w;
                     T = ti;
                     if (e.a < clamp) {
                         const Real x = e.m / tau;
                         const Real gaa = ga * e.a;
-                        v[5] = ga * (e.a / e.og);
+                        v[5] = ga * e.a * rcp_(e.og);
                         v[6] = gaa * log1p_(-x);
                         const Real gm = gaa * (-e.bx / ((Real)1 - x)) / tau;
                         v[0] = (Real)-2 * gm * e.pd0;
@@ -526,14 +554,10 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
                 }
             }
             if (__any_sync(0xffffffffu, contrib)) {
-#pragma unroll
-                for (int k = 0; k < 10; ++k) v[k] = warp_sum(v[k]);
-                Real mine = v[0];
-#pragma unroll
-                for (int k = 1; k < 10; ++k)
-                    if (lane == k) mine = v[k];
-                if (lane < 10 && mine != (Real)0)
-                    atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + lane, mine);
+                int idx;
+                const Real mine = warp_reduce_scatter16(v, lane, idx);
+                if ((lane & 1) == 0 && idx < 10 && mine != (Real)0)
+                    atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + idx, mine);
             }
         }
     }

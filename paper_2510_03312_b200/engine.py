@@ -190,6 +190,8 @@ class Workspace:
         self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)  # UBS_S_* bits, sticky
+        self.active = None
+        self.active_count = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     # --- allocation -------------------------------------------------------
     def _i(self, n, dtype):
@@ -444,6 +446,11 @@ def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_param
     gb.reg_opacity = float(reg_opacity)
     gb.reg_scale = float(reg_scale)
     gb.nonfinite = _ptr(ws.nonfinite)
+    if ws.active is None or ws.active.numel() < n:
+        ws.active = torch.empty(ws.n_cap, dtype=torch.int32, device=ws.device)
+    gb.flags = _ptr(ws.flags)
+    gb.active = _ptr(ws.active)
+    gb.active_count = _ptr(ws.active_count)
     s = _stream_ptr()
     check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb, s),
           "ubs_raster_backward")

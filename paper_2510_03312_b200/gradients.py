@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import engine
+from . import _lib, engine
 from .raster import _device_scene, workspace
 from .types import DEFAULT_SETTINGS, LossConfig, SceneGrads, sigmoid
 
@@ -39,13 +39,17 @@ def backward(scene, frames, cfg: LossConfig = LossConfig(), settings=DEFAULT_SET
         ws.loss_parts.zero_()
         tgt = torch.as_tensor(np.ascontiguousarray(target, dtype=np.float64))
         g_img, parts = engine.loss_image_grad(fr, tgt, cfg.lambda_ssim, scale)
-        engine.backward_frame(fr, ds, g_img, grads, add_regularisers=(k == 0),
-                              reg_opacity=cfg.loss_scale * cfg.lambda_o,
-                              reg_scale=cfg.loss_scale * cfg.lambda_sigma)
+        engine.backward_frame(fr, ds, g_img, grads)
         l1_sum, ssim_sum = parts.cpu().tolist()
         size = fr.width * fr.height * 3
         rec += (1.0 - cfg.lambda_ssim) * (l1_sum / size) + cfg.lambda_ssim * (1.0 - ssim_sum / size)
     rec /= len(frames)
+    # regulariser gradients once per step (gradients.py:120-123)
+    lib = _lib.load()
+    _lib.check(lib.ubs_add_regularisers(ds.params.data_ptr(), int(ds.params.dtype == torch.float64),
+                                        grads.data_ptr(), 1, ds.n, ds.n_dims, cfg.loss_scale * cfg.lambda_o,
+                                        cfg.loss_scale * cfg.lambda_sigma, torch.cuda.current_stream().cuda_stream),
+               "ubs_add_regularisers")
     out = SceneGrads.from_records(scene.n_dims, grads.cpu().numpy())
     out.check_finite()
     total = cfg.loss_scale * (rec + _regularizers(scene, cfg))

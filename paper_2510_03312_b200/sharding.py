@@ -60,15 +60,24 @@ class GpuViewBackend:
         return torch.zeros(self.ds.params.shape, dtype=self.grad_dtype, device=self.ds.device)
 
     def view_loss_grad(self, cam, query, target: torch.Tensor, cfg: LossConfig, scale: float,
-                       grad: torch.Tensor) -> torch.Tensor:
+                       grad: torch.Tensor, sync: bool = False) -> torch.Tensor:
         """Adds this view's d(loss)/d(params) into ``grad``; returns the view's
-        reconstruction term (1-l) L1 + l (1 - SSIM) as a 0-d device tensor."""
-        fr = engine.render_frame(self.ws, self.ds, cam, query, self.settings)
+        reconstruction term (1-l) L1 + l (1 - SSIM) as a 0-d device tensor.
+        Frames are asynchronous unless ``sync`` (see :meth:`status`)."""
+        fr = engine.render_frame(self.ws, self.ds, cam, query, self.settings,
+                                 sync=sync or self.ws.pair_cap == 0)
         self.ws.loss_parts.zero_()
         g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
         engine.backward_frame(fr, self.ds, g_img, grad)
         size = fr.width * fr.height * 3
         return (1.0 - cfg.lambda_ssim) * parts[0] / size + cfg.lambda_ssim * (1.0 - parts[1] / size)
+
+    def status(self) -> torch.Tensor:
+        """Device flag, nonzero when an asynchronous view outgrew the pair buffers."""
+        return self.ws.status
+
+    def clear_status(self):
+        self.ws.status.zero_()
 
     def add_regularisers(self, grad: torch.Tensor, cfg: LossConfig):
         lib = _lib.load()
@@ -79,10 +88,11 @@ class GpuViewBackend:
                                             torch.cuda.current_stream().cuda_stream), "ubs_add_regularisers")
 
     def regulariser_value(self, cfg: LossConfig) -> torch.Tensor:
+        # only the opacity and scale columns, summed in fp64
         sl = engine.field_slices(self.ds.n_dims)
-        p = self.ds.params.double()
-        o = torch.sigmoid(p[:, sl["opacity_raw"][0]]).sum()
-        sc = torch.exp(p[:, sl["s_x_raw"][0]]).sum() + torch.exp(p[:, sl["s_q_raw"][0]]).sum()
+        p = self.ds.params
+        o = torch.sigmoid(p[:, sl["opacity_raw"][0]].double()).sum()
+        sc = torch.exp(p[:, sl["s_x_raw"][0]].double()).sum() + torch.exp(p[:, sl["s_q_raw"][0]].double()).sum()
         return cfg.lambda_o * o + cfg.lambda_sigma * sc
 
 
@@ -98,16 +108,23 @@ class ViewShardedStep:
             raise ValueError("empty batch")
         rank, world = dist_rank_world(self.group)
         b = self.backend
-        grad = b.new_grad() if grad is None else grad.zero_()
         scale = cfg.loss_scale / len(views)
-        rec = torch.zeros((), dtype=torch.float64, device=grad.device)
-        for cam, query, target in shard(views, rank, world):
-            rec = rec + b.view_loss_grad(cam, query, target, cfg, scale, grad)
+        for attempt in range(2):
+            sync = attempt > 0  # retry with synchronous frames if a view outgrew the pair buffers
+            grad = b.new_grad() if grad is None else grad.zero_()
+            rec = torch.zeros(2, dtype=torch.float64, device=grad.device)
+            for cam, query, target in shard(views, rank, world):
+                rec[0] += b.view_loss_grad(cam, query, target, cfg, scale, grad, sync=sync)
+            if hasattr(b, "status"):
+                rec[1] = b.status().to(torch.float64)[0]
+            allreduce_sum_(rec, self.group)  # loss term and overflow flag in one collective
+            if float(rec[1]) == 0.0:
+                break
+            b.clear_status()
         if rank == 0:
             b.add_regularisers(grad, cfg)
         allreduce_sum_(grad, self.group)
-        rec = allreduce_sum_(rec.reshape(1), self.group)[0]
-        loss = cfg.loss_scale * (rec / len(views) + b.regulariser_value(cfg))
+        loss = cfg.loss_scale * (rec[0] / len(views) + b.regulariser_value(cfg))
         return loss, grad
 
 

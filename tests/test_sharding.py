@@ -30,7 +30,7 @@ class OracleBackend:
     def new_grad(self):
         return torch.zeros((self.scene.n_primitives, 14 + 6 * (self.scene.n_dims - 3)), dtype=torch.float64)
 
-    def view_loss_grad(self, cam, q, target, cfg, scale, grad):
+    def view_loss_grad(self, cam, q, target, cfg, scale, grad, sync=False):
         fr = O.render_frame(self.scene, cam, q, DEFAULT_SETTINGS)
         tgt = target.numpy()
         diff = fr["image"] - tgt
