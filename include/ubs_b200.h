@@ -70,7 +70,10 @@ enum {
 };
 
 /* device status bits (UbsBinBuffers.status) */
-enum { UBS_S_PAIR_OVERFLOW = 1 };
+enum {
+    UBS_S_PAIR_OVERFLOW = 1, /* K exceeded the pair capacity */
+    UBS_S_LIST_TRUNC = 2,    /* a tile exhausted its capped list with unsaturated pixels */
+};
 
 /* Camera (camera.py:15-51): intrinsics + rigid world_to_cam. */
 typedef struct UbsCamera {
@@ -136,7 +139,11 @@ typedef struct UbsBinBuffers {
     uint32_t *seg_scratch; /* (2 x 128 + 1) x n_buckets */
     uint32_t *bucket_start;/* n_buckets + 1 */
     int64_t bucket_capacity; /* elements of bucket_start */
-    uint32_t *status;      /* [1] |= UBS_S_PAIR_OVERFLOW when K > pair_capacity (frame must be re-run) */
+    uint32_t *status;      /* [1] |= UBS_S_* (frame must be re-run with more capacity) */
+    uint32_t list_cap;     /* per-tile list cap: only the first list_cap ids of each tile are
+                              materialised (0xFFFFFFFF = full lists).  Tiles saturate long before
+                              their lists end; a raster CTA that runs out of a capped list with
+                              unsaturated pixels sets UBS_S_LIST_TRUNC. */
 } UbsBinBuffers;
 
 /* Forward outputs.  Image/alpha/T are f32, or f64 in the fp64 raster. */

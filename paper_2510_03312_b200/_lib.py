@@ -14,7 +14,8 @@ from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_u
 from . import build as _build
 
 UBS_OK, UBS_E_ARGS, UBS_E_CUDA, UBS_E_CAPACITY = 0, -1, -2, -3
-S_PAIR_OVERFLOW = 1
+S_PAIR_OVERFLOW, S_LIST_TRUNC = 1, 2
+FULL_LISTS = 0xFFFFFFFF
 F_VISIBLE, F_DEGENERATE, F_FLOOR3, F_FLOOR2, F_THIN, F_GATE_SAT = 1, 2, 4, 8, 16, 32
 DEBUG_STRIDE = 32
 GRAD2D_STRIDE = 12
@@ -55,7 +56,7 @@ class UbsBinBuffers(Structure):
                 ("temp", c_void_p), ("temp_bytes", c_size_t), ("chunk_hist", c_void_p),
                 ("chunk_hist_capacity", c_int64), ("chunk_count", c_int32), ("entries", c_void_p),
                 ("seg_scratch", c_void_p), ("bucket_start", c_void_p), ("bucket_capacity", c_int64),
-                ("status", c_void_p)]
+                ("status", c_void_p), ("list_cap", c_uint32)]
 
 
 class UbsImageBuffers(Structure):

@@ -396,48 +396,49 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     }
 }
 
-// (4) per-tile lists: one CTA per tile; each warp owns a contiguous segment
-// of the tile's bucket.  Phase 1 counts matches per warp (no barriers inside
-// the scan), one block scan of the 8 warp totals, phase 2 re-reads the
-// (L2-resident) segment and writes the ids in order.
+// (4) per-tile lists: one CTA per tile scans its bucket in rounds of 256
+// entries (one per thread) with a block-ordered compaction of the entries
+// whose [tx0, tx1] contains the tile, and stops once `cap` ids are written:
+// only the prefix of each list a tile can consume is materialised.
 constexpr int kListThreads = 256;
 __global__ void __launch_bounds__(kListThreads)
 tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restrict__ bstart,
-                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t *__restrict__ out,
+                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t cap, uint32_t *__restrict__ out,
                   const unsigned long long *__restrict__ n_pairs, int64_t capacity) {
+    __shared__ uint32_t wcount[kListThreads / 32];
     if (pairs_overflow(n_pairs, capacity, nullptr)) return;
-    __shared__ uint32_t wtot[kListThreads / 32];
     const int tile = blockIdx.x;
     const int ty = tile / TX, tx = tile - ty * TX;
     const int k = ty * NB + tx / kBand;
     const uint32_t e0 = bstart[k], e1 = bstart[k + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kListThreads / 32;
-    const uint32_t len = e1 - e0;
-    const uint32_t per = ((len + nw - 1) / nw + 31) & ~31u;  // warp segment, multiple of 32
-    const uint32_t s0 = e0 + min(len, per * wid), s1 = e0 + min(len, per * (wid + 1));
-    auto hit = [&](uint32_t i, uint32_t &id) {
-        const uint64_t e = entries[i];
-        const int tx0 = (int)((e >> 32) & 0xFFFF), tx1 = (int)(e >> 48);
-        id = (uint32_t)e;
-        return tx0 <= tx && tx <= tx1;
-    };
-    uint32_t c = 0;
-    for (uint32_t i = s0 + lane; i < s1; i += 32) {
-        uint32_t id;
-        c += hit(i, id) ? 1u : 0u;
-    }
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) wtot[wid] = c;
-    __syncthreads();
-    uint32_t w = ranges[2 * tile];
-    for (int j = 0; j < wid; ++j) w += wtot[j];
-    for (uint32_t base = s0; base < s1; base += 32) {
-        const uint32_t i = base + lane;
+    const uint32_t t0 = ranges[2 * tile], t1 = ranges[2 * tile + 1];
+    const uint32_t want = min(cap, t1 - t0);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t written = 0;
+    for (uint32_t base = e0; base < e1 && written < want; base += kListThreads) {
+        const uint32_t i = base + threadIdx.x;
+        bool p = false;
         uint32_t id = 0;
-        const bool p = i < s1 && hit(i, id);
+        if (i < e1) {
+            const uint64_t e = entries[i];
+            const int tx0 = (int)((e >> 32) & 0xFFFF), tx1 = (int)(e >> 48);
+            p = tx0 <= tx && tx <= tx1;
+            id = (uint32_t)e;
+        }
         const unsigned m = __ballot_sync(0xffffffffu, p);
-        if (p) out[w + __popc(m & ((1u << lane) - 1u))] = id;
-        w += __popc(m);
+        if (lane == 0) wcount[wid] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+#pragma unroll
+        for (int j = 0; j < kListThreads / 32; ++j) {
+            const uint32_t c = wcount[j];
+            before += (j < wid) ? c : 0u;
+            tot += c;
+        }
+        const uint32_t pos = written + before + __popc(m & ((1u << lane) - 1u));
+        if (p && pos < want) out[t0 + pos] = id;
+        written += tot;
+        __syncthreads();
     }
 }
 
@@ -519,7 +520,8 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
                                                                  pb->n_visible, G, NB, nbk, off, bb->entries,
                                                                  pb->n_pairs, bb->pair_capacity, bb->status);
     tile_lists_kernel<<<n_tiles, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, NB,
-                                                       bb->tile_ids, pb->n_pairs, bb->pair_capacity);
+                                                       bb->list_cap ? bb->list_cap : 0xFFFFFFFFu, bb->tile_ids,
+                                                       pb->n_pairs, bb->pair_capacity);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

@@ -33,12 +33,26 @@ struct RasterParams {
     double bg[3];
     const unsigned long long *n_pairs;  // device K, checked against pair_capacity
     int64_t pair_capacity;
+    uint32_t list_cap;                  // per-tile list cap (binning materialised only this prefix)
+    uint32_t *status;                   // UBS_S_LIST_TRUNC when a capped list ran out too early
 };
+
+// [start, end) of the materialised part of a tile's list; `capped` when the
+// real list is longer (running out of it with unsaturated pixels is an error)
+__device__ __forceinline__ void tile_span(const RasterParams &P, const uint32_t *ranges, int tile, uint32_t &start,
+                                          uint32_t &end, bool &capped) {
+    start = ranges[2 * tile];
+    const uint32_t len = ranges[2 * tile + 1] - start;
+    capped = len > P.list_cap;
+    end = start + (capped ? P.list_cap : len);
+}
 
 static RasterParams make_params(const UbsView &v, const UbsPrimBuffers &pb, const UbsBinBuffers &bb) {
     RasterParams p;
     p.n_pairs = pb.n_pairs;
     p.pair_capacity = bb.pair_capacity;
+    p.list_cap = bb.list_cap ? bb.list_cap : 0xFFFFFFFFu;
+    p.status = bb.status;
     p.W = v.cam.width;
     p.H = v.cam.height;
     p.TX = (p.W + kTile - 1) / kTile;
@@ -76,7 +90,9 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const int px = tx * kTile + (threadIdx.x & (kTile - 1));
     const int py = ty * kTile + (threadIdx.x >> 4);
     const bool inside = px < P.W && py < P.H;
-    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    uint32_t start, end;
+    bool capped;
+    tile_span(P, ranges, tile, start, end, capped);
     const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
     const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
     double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
@@ -116,6 +132,7 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             done = done || (T < tmin);
         }
     }
+    if (capped && inside && !(T < tmin)) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = add(a0, mul(T, P.bg[0]));
@@ -181,7 +198,9 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const int py = ty * kTile + (threadIdx.x >> 4);
     const float pxf = (float)px, pyf = (float)py;
     const bool inside = px < P.W && py < P.H;
-    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    uint32_t start, end;
+    bool capped;
+    tile_span(P, ranges, tile, start, end, capped);
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
     const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
     // alpha below clamp_lo cannot be clamp-ambiguous unless its error bound is
@@ -265,6 +284,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         }
     }
     if (inside && !done && T < tmin * (1.0f + err + 1.0e-6f)) flag = true;
+    if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
     if (err > kImgErrTol) flag = true;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
@@ -315,7 +335,9 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         const uint32_t pix = fix_list[wi];
         const int py = pix / P.W, px = pix - py * P.W;
         const int tile = (py / kTile) * P.TX + px / kTile;
-        const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+        uint32_t start, end;
+        bool capped;
+        tile_span(P, ranges, tile, start, end, capped);
         const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
         double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
         int cnt = 0;
@@ -375,6 +397,7 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             if (!done && T < tmin) done = true;  // crossed on the chunk's last splat
             __syncwarp();
         }
+        if (lane == 0 && capped && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
         if (lane == 0) {
             image[3 * (int64_t)pix] = (float)add(a0, mul(T, P.bg[0]));
             image[3 * (int64_t)pix + 1] = (float)add(a1, mul(T, P.bg[1]));

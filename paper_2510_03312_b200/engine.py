@@ -192,6 +192,9 @@ class Workspace:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)  # UBS_S_* bits, sticky
         self.active = None
         self.active_count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # materialised prefix of each tile list (grows x2 when a frame needs more)
+        self.list_cap = 1024
+        self.frame_list_cap = self.list_cap
 
     # --- allocation -------------------------------------------------------
     def _i(self, n, dtype):
@@ -298,6 +301,7 @@ class Workspace:
             bb.bucket_start = _ptr(self.bucket_start)
             bb.bucket_capacity = self.bucket_start.numel()
         bb.status = _ptr(self.status)
+        bb.list_cap = self.frame_list_cap
         return bb
 
     def image_buffers(self) -> UbsImageBuffers:
@@ -338,7 +342,8 @@ class _Timed:
 
 
 def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS,
-                 want_debug: bool = False, timers: dict | None = None, sync: bool = True) -> Frame:
+                 want_debug: bool = False, timers: dict | None = None, sync: bool = True,
+                 full_lists: bool = False) -> Frame:
     """Forward one frame on the current stream; returns device views.
 
     ``sync=True`` reads the frame's tile-pair count K back (one 16-byte copy)
@@ -347,7 +352,13 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     capacity on the device and set ``ws.status`` (UBS_S_PAIR_OVERFLOW)
     instead of overflowing; call :func:`check_status` (or render the frame
     again with ``sync=True``) before trusting an async frame whose K may have
-    grown.  ``timers``: optional dict collecting per-stage CUDA event pairs."""
+    grown.  ``timers``: optional dict collecting per-stage CUDA event pairs.
+
+    Tile lists are materialised only up to ``ws.list_cap`` ids per tile (the
+    rasterizer stops long before; ``full_lists=True`` materialises them all,
+    e.g. for FrameCache.tiles).  A frame that needed more sets
+    UBS_S_LIST_TRUNC: synchronous frames then double the cap and re-render,
+    asynchronous ones leave it to :func:`check_status`."""
     lib = ws.lib
     if ds.device != ws.device:
         raise ValueError("scene and workspace live on different devices")
@@ -377,6 +388,7 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
         ws.ensure_pairs(k)
     else:
         k, n_vis = None, None
+    ws.frame_list_cap = _lib.FULL_LISTS if full_lists else ws.list_cap
     bb = ws.bin_buffers()
     with _Timed(timers, "bin_tiles"):
         check(lib.ubs_bin_tiles(v, pb, bb, -1 if k is None else k, s), "ubs_bin_tiles")
@@ -387,6 +399,12 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     if not ws.f64:
         with _Timed(timers, "fixup"):
             check(lib.ubs_raster_fixup(v, pb, bb, ib, s), "ubs_raster_fixup")
+    if sync and not full_lists:
+        st = int(ws.status.item())
+        if st & _lib.S_LIST_TRUNC:
+            ws.status.zero_()
+            ws.list_cap *= 2
+            return render_frame(ws, ds, cam, query, settings, want_debug, timers, sync, full_lists)
     npix = W * H
     return Frame(view=v, width=W, height=H, n=n, n_visible_host=n_vis, n_pairs_host=k,
                  image=ws.image_buf[:npix * 3].view(H, W, 3), alpha_sum=ws.asum_buf[:npix].view(H, W),
@@ -398,9 +416,12 @@ def check_status(ws: Workspace) -> int:
     """Raise if any asynchronous frame since the last reset overflowed its pair
     buffers (its outputs are invalid; re-render with sync=True).  Syncs."""
     st = int(ws.status.item())
-    if st & _lib.S_PAIR_OVERFLOW:
+    if st & (_lib.S_PAIR_OVERFLOW | _lib.S_LIST_TRUNC):
         ws.status.zero_()
-        raise _lib.UbsError("tile-pair capacity exceeded by an asynchronous frame; re-render with sync=True")
+        if st & _lib.S_LIST_TRUNC:
+            ws.list_cap *= 2
+        raise _lib.UbsError("an asynchronous frame outgrew its pair buffers or tile-list cap (capacity grown); "
+                            "re-render it")
     return st
 
 

@@ -108,7 +108,8 @@ class FrameCache:
         if self._debug is None:
             ws = workspace(self.precision)
             ds = _device_scene(self.scene, ws)
-            fr = engine.render_frame(ws, ds, self.camera, self.query, self.settings, want_debug=True)
+            fr = engine.render_frame(ws, ds, self.camera, self.query, self.settings, want_debug=True,
+                                     full_lists=True)
             self._debug = ws.debug[:fr.n * DEBUG_STRIDE].view(fr.n, DEBUG_STRIDE).cpu().numpy().copy()
         return self._debug
 
@@ -150,7 +151,7 @@ def render_with_cache(scene, cam, query, settings=DEFAULT_SETTINGS, *, precision
         raise ValueError(f"query has {np.asarray(query.dims).size} dims, scene expects {c}")
     ws = workspace(precision, device)
     ds = _device_scene(scene, ws)
-    fr = engine.render_frame(ws, ds, cam, query, settings)
+    fr = engine.render_frame(ws, ds, cam, query, settings, full_lists=True)
     return FrameCache(scene, cam, query, settings, ws.precision, fr)
 
 

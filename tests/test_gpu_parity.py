@@ -274,3 +274,26 @@ def test_async_frames_match_sync():
     engine.render_frame(ws, ds, cam, q, sync=False)
     with pytest.raises(Exception):
         engine.check_status(ws)
+
+
+def test_capped_tile_lists_match_full():
+    # a tiny cap forces truncation: the frame must detect it, grow the cap and
+    # re-render to exactly the full-list result
+    from paper_2510_03312_b200 import engine
+    import torch
+    sc = quantize_f32(S.random_scene(7, 4000, seed=41))
+    cam = S.random_camera(96, 42)
+    q = S.random_query(7, 43)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    full = engine.render_frame(ws, ds, cam, q, full_lists=True)
+    ref_img, ref_cnt = full.image.clone(), full.n_contrib.clone()
+    ws.list_cap = 4
+    capped = engine.render_frame(ws, ds, cam, q)  # sync: grows the cap until no tile runs out
+    assert ws.list_cap > 4
+    assert torch.equal(capped.n_contrib, ref_cnt) and torch.equal(capped.image, ref_img)
+    # asynchronous frame with a cap that is too small: flagged, not silently wrong
+    ws.list_cap = 4
+    engine.render_frame(ws, ds, cam, q, sync=False)
+    with pytest.raises(Exception):
+        engine.check_status(ws)
