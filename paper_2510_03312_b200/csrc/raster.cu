@@ -179,9 +179,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // the exponent) is part of the per-visit relative alpha bound
 //     q = eb / (tau - m) + qc + 2.1e-7 |arg|,
 // and err accumulates q a / (1 - a) + 2u, the first-order relative error of T.
-// Near the cut (T < tmin * (1 + 4e-3)) the exact band test runs; elsewhere a
-// single compare.  A pixel whose bound exceeds kImgErrTol is flagged anyway,
-// so the coarse prefilter width can never hide a needed band test.
+// T and err change only on in-support visits, so the reference's cut test
+// (T < t_min before each splat) and its certification band are evaluated
+// right after each update: the next splat is iterated iff T >= t_min, exactly
+// as in tile_forward, and out-of-support visits carry no cut logic at all.
+// The contributor count is the number of splats the loop pointer passed.
 __global__ void __launch_bounds__(kTileThreads)
 raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, float *__restrict__ image, float *__restrict__ asum,
@@ -212,8 +214,9 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
     float err = 0.f;  // bound on |T32 - T64| / T
     int cnt = 0;
-    bool flag = false;
+    int flag = 0;
     bool done = !inside;
+    const float4 *rbase = reinterpret_cast<const float4 *>(srec);
     for (uint32_t b = start; b < end; b += kTileThreads) {
         if (__syncthreads_count(done) == kTileThreads) break;
         const uint32_t q = b + threadIdx.x;
@@ -228,20 +231,10 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             d[3] = __ldg(r + 3);
         }
         __syncthreads();
-        const int nb = (int)min((uint32_t)kTileThreads, end - b);
         if (!done) {
-            const float4 *rp = reinterpret_cast<const float4 *>(srec);
-            for (int j = 0; j < nb; ++j, rp += 4) {
-                if (T < tmin_hi) {
-                    const float band = err + 1.0e-6f;
-                    if (T < tmin) {
-                        if (T > tmin * (1.0f - band)) flag = true;
-                        done = true;
-                        break;
-                    }
-                    if (T < tmin * (1.0f + band)) flag = true;
-                }
-                ++cnt;
+            const float4 *rend = rbase + 4 * (int)min((uint32_t)kTileThreads, end - b);
+            const float4 *rp = rbase;
+            for (; rp < rend; rp += 4) {
                 const float4 r0 = rp[0], r1 = rp[1];
                 const float dx = (pxf - r0.x) + r0.z;
                 const float dy = (pyf - r0.y) + r0.w;
@@ -249,7 +242,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 const float y1 = r1.z * dy;
                 const float m = fmaf(y0, y0, y1 * y1);
                 if (m >= tau) {
-                    if (m < r1.w) flag = true;  // support edge within the m-error band
+                    flag |= (m < r1.w);  // support edge within the m-error band
                     continue;
                 }
                 const float4 r2 = rp[2], r3 = rp[3];
@@ -259,12 +252,12 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 float om = 1.0f - a;
                 if (a > clamp_lo) {
                     if (a > clamp) {
-                        if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
-                        else flag = true;
+                        if (a * (1.0f - qrel) > clamp) hit[sid[(rp - rbase) >> 2]] = 1;
+                        else flag = 1;
                         a = clamp;
                         om = one_minus_clamp;
-                    } else if (a * (1.0f + qrel) > clamp) {
-                        flag = true;
+                    } else {
+                        flag |= (a * (1.0f + qrel) > clamp);
                     }
                 }
                 err = fmaf(a * qrel, rcp_approx(om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
@@ -274,18 +267,23 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 a2 = fmaf(w, r2.w, a2);
                 ws += w;
                 T *= om;
+                if (T < tmin_hi) {
+                    const float band = err + 1.0e-6f;
+                    if (T < tmin) {
+                        // the reference stops before the next splat
+                        flag |= (T > tmin * (1.0f - band));
+                        done = true;
+                        rp += 4;
+                        break;
+                    }
+                    flag |= (T < tmin * (1.0f + band));
+                }
             }
-            if (!done && T < tmin) {
-                // crossed on the batch's last splat: the next check would stop
-                const float band = err + 1.0e-6f;
-                if (T > tmin * (1.0f - band)) flag = true;
-                done = true;
-            }
+            cnt += (int)((rp - rbase) >> 2);
         }
     }
-    if (inside && !done && T < tmin * (1.0f + err + 1.0e-6f)) flag = true;
     if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
-    if (err > kImgErrTol) flag = true;
+    if (err > kImgErrTol) flag = 1;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
@@ -295,14 +293,14 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         tstop[pix] = T;
         ncontrib[pix] = cnt;
     }
-    flag = flag && inside;
-    const unsigned fb = __ballot_sync(0xffffffffu, flag);
+    const bool fl = flag && inside;
+    const unsigned fb = __ballot_sync(0xffffffffu, fl);
     if (fb) {
         uint32_t base = 0;
         const int lane = threadIdx.x & 31;
         if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (flag) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
+        if (fl) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
     }
     __syncthreads();
     const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
