@@ -174,6 +174,47 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Warp cover mask of one splat over a 16x16 tile whose warps are 8x4 pixel
+// blocks (warp w covers columns 8 (w & 1) .. +7, rows 4 (w >> 1) .. +3).
+// The conic factor maps a pixel offset to y0 = u00 dx + u01 dy, y1 = u11 dy
+// (u00, u11 >= 0) and m = y0^2 + y1^2; over a warp's box both are linear, so
+// their ranges come from the box corners and z0^2 + z1^2 (z = distance of
+// each range from 0) is a lower bound of m over the box.  Bit w is clear only
+// when that bound, less a 1e-5 relative slack in y0 (a hundred ulp of the
+// terms, above the fp32 rounding of this test and of the per-pixel m), is
+// still >= (tau + E)(1 + 1e-4): every pixel of the warp would have skipped
+// the splat without raising its edge flag, so culling never changes a bit.
+__device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float4 r1, int tx, int ty) {
+    const float u00 = r1.x, u01 = r1.y, u11 = r1.z;
+    const float thr = r1.w * (1.0f + 1.0e-4f);
+    const float xa0 = ((float)(tx * kTile) - r0.x) + r0.z;
+    const float ya0 = ((float)(ty * kTile) - r0.y) + r0.w;
+    if (!isfinite(u00 + u01 + u11 + thr + xa0 + ya0)) return 0xffu;  // fmaxf would drop a NaN
+    float clo[2], chi[2], cs[2];
+#pragma unroll
+    for (int wx = 0; wx < 2; ++wx) {
+        clo[wx] = u00 * (xa0 + (float)(8 * wx));
+        chi[wx] = u00 * (xa0 + (float)(8 * wx + 7));
+        cs[wx] = fmaf(1.0e-5f, fabsf(clo[wx]) + fabsf(chi[wx]), 1.0e-6f);
+    }
+    uint32_t mask = 0;
+#pragma unroll
+    for (int wy = 0; wy < 4; ++wy) {
+        const float ya = ya0 + (float)(4 * wy), yb = ya + 3.0f;
+        const float z1 = fmaxf(0.0f, fmaxf(u11 * ya, -(u11 * yb)));
+        const float z1sq = z1 * z1;
+        const float ua = u01 * ya, ub = u01 * yb;
+        const float umin = fminf(ua, ub), umax = fmaxf(ua, ub);
+        const float us = 1.0e-5f * (fabsf(ua) + fabsf(ub));
+#pragma unroll
+        for (int wx = 0; wx < 2; ++wx) {
+            const float z0 = fmaxf(fmaxf(clo[wx] + umin, -(chi[wx] + umax)) - (cs[wx] + us), 0.0f);
+            if (fmaf(z0, z0, z1sq) < thr) mask |= 1u << (2 * wy + wx);
+        }
+    }
+    return mask;
+}
+
 // Per visit (in support): alpha = 2^(beta * lg2(1 - m/tau) + log2(og)) with
 // the MUFU lg2/ex2 approximations; their error (qc, and 2.1e-7 per unit of
 // the exponent) is part of the per-visit relative alpha bound
@@ -182,22 +223,26 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // T and err change only on in-support visits, so the reference's cut test
 // (T < t_min before each splat) and its certification band are evaluated
 // right after each update: the next splat is iterated iff T >= t_min, exactly
-// as in tile_forward, and out-of-support visits carry no cut logic at all.
-// The contributor count is the number of splats the loop pointer passed.
+// as in tile_forward.  Each warp walks only the splats whose cover mask has
+// its bit (per-warp ballot words), and the contributor count is the list
+// position where the pixel stopped (tile_forward counts every iterated splat).
 __global__ void __launch_bounds__(kTileThreads)
 raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, float *__restrict__ image, float *__restrict__ asum,
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits, uint32_t *__restrict__ fix_list,
                     uint32_t *__restrict__ fix_count) {
+    constexpr int kWarps = kTileThreads / 32;
     __shared__ Rec32 srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
-    __shared__ unsigned long long red[kTileThreads / 32];
+    __shared__ uint32_t swm[kWarps][kWarps];  // [walking warp][loading warp] ballot words
+    __shared__ unsigned long long red[kWarps];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
-    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty * kTile + (threadIdx.x >> 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
     const float pxf = (float)px, pyf = (float)py;
     const bool inside = px < P.W && py < P.H;
     uint32_t start, end;
@@ -213,73 +258,85 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
     float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
     float err = 0.f;  // bound on |T32 - T64| / T
-    int cnt = 0;
+    uint32_t cnt = inside ? end - start : 0u;
     int flag = 0;
     bool done = !inside;
     const float4 *rbase = reinterpret_cast<const float4 *>(srec);
     for (uint32_t b = start; b < end; b += kTileThreads) {
         if (__syncthreads_count(done) == kTileThreads) break;
         const uint32_t q = b + threadIdx.x;
+        uint32_t cover = 0;
         if (q < end) {
             const uint32_t id = ids[q];
             const float4 *r = reinterpret_cast<const float4 *>(recs + id);
             float4 *d = reinterpret_cast<float4 *>(srec + threadIdx.x);
             sid[threadIdx.x] = id;
-            d[0] = __ldg(r);
-            d[1] = __ldg(r + 1);
+            const float4 r0 = __ldg(r), r1 = __ldg(r + 1);
+            d[0] = r0;
+            d[1] = r1;
             d[2] = __ldg(r + 2);
             d[3] = __ldg(r + 3);
+            cover = warp_cover_mask(r0, r1, tx, ty);
+        }
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
+            if (lane == 0) swm[w][warp] = word;
         }
         __syncthreads();
         if (!done) {
-            const float4 *rend = rbase + 4 * (int)min((uint32_t)kTileThreads, end - b);
-            const float4 *rp = rbase;
-            for (; rp < rend; rp += 4) {
-                const float4 r0 = rp[0], r1 = rp[1];
-                const float dx = (pxf - r0.x) + r0.z;
-                const float dy = (pyf - r0.y) + r0.w;
-                const float y0 = fmaf(r1.x, dx, r1.y * dy);
-                const float y1 = r1.z * dy;
-                const float m = fmaf(y0, y0, y1 * y1);
-                if (m >= tau) {
-                    flag |= (m < r1.w);  // support edge within the m-error band
-                    continue;
-                }
-                const float4 r2 = rp[2], r3 = rp[3];
-                const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
-                float a = ex2_approx(arg);
-                const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
-                float om = 1.0f - a;
-                if (a > clamp_lo) {
-                    if (a > clamp) {
-                        if (a * (1.0f - qrel) > clamp) hit[sid[(rp - rbase) >> 2]] = 1;
-                        else flag = 1;
-                        a = clamp;
-                        om = one_minus_clamp;
-                    } else {
-                        flag |= (a * (1.0f + qrel) > clamp);
+            const int nw = (int)((min((uint32_t)kTileThreads, end - b) + 31u) >> 5);
+            for (int k = 0; k < nw && !done; ++k) {
+                uint32_t bits = swm[warp][k];
+                while (bits) {
+                    const int j = (k << 5) + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    const float4 *rp = rbase + 4 * j;
+                    const float4 r0 = rp[0], r1 = rp[1];
+                    const float dx = (pxf - r0.x) + r0.z;
+                    const float dy = (pyf - r0.y) + r0.w;
+                    const float y0 = fmaf(r1.x, dx, r1.y * dy);
+                    const float y1 = r1.z * dy;
+                    const float m = fmaf(y0, y0, y1 * y1);
+                    if (m >= tau) {
+                        flag |= (m < r1.w);  // support edge within the m-error band
+                        continue;
                     }
-                }
-                err = fmaf(a * qrel, rcp_approx(om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
-                const float w = a * T;
-                a0 = fmaf(w, r2.y, a0);
-                a1 = fmaf(w, r2.z, a1);
-                a2 = fmaf(w, r2.w, a2);
-                ws += w;
-                T *= om;
-                if (T < tmin_hi) {
-                    const float band = err + 1.0e-6f;
-                    if (T < tmin) {
-                        // the reference stops before the next splat
-                        flag |= (T > tmin * (1.0f - band));
-                        done = true;
-                        rp += 4;
-                        break;
+                    const float4 r2 = rp[2], r3 = rp[3];
+                    const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
+                    float a = ex2_approx(arg);
+                    const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
+                    float om = 1.0f - a;
+                    if (a > clamp_lo) {
+                        if (a > clamp) {
+                            if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
+                            else flag = 1;
+                            a = clamp;
+                            om = one_minus_clamp;
+                        } else {
+                            flag |= (a * (1.0f + qrel) > clamp);
+                        }
                     }
-                    flag |= (T < tmin * (1.0f + band));
+                    err = fmaf(a * qrel, rcp_approx(om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
+                    const float w = a * T;
+                    a0 = fmaf(w, r2.y, a0);
+                    a1 = fmaf(w, r2.z, a1);
+                    a2 = fmaf(w, r2.w, a2);
+                    ws += w;
+                    T *= om;
+                    if (T < tmin_hi) {
+                        const float band = err + 1.0e-6f;
+                        if (T < tmin) {
+                            // the reference stops before the next splat
+                            flag |= (T > tmin * (1.0f - band));
+                            done = true;
+                            cnt = b - start + (uint32_t)j + 1u;
+                            break;
+                        }
+                        flag |= (T < tmin * (1.0f + band));
+                    }
                 }
             }
-            cnt += (int)((rp - rbase) >> 2);
         }
     }
     if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
@@ -291,13 +348,12 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         image[3 * pix + 2] = fmaf(T, (float)P.bg[2], a2);
         asum[pix] = ws;
         tstop[pix] = T;
-        ncontrib[pix] = cnt;
+        ncontrib[pix] = (int32_t)cnt;
     }
     const bool fl = flag && inside;
     const unsigned fb = __ballot_sync(0xffffffffu, fl);
     if (fb) {
         uint32_t base = 0;
-        const int lane = threadIdx.x & 31;
         if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (fl) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
