@@ -256,7 +256,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const float clamp_lo = clamp - 0.05f;
     const float tmin = (float)P.tmin;
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
-    float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f, ws = 0.f;
+    float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f;
     float err = 0.f;  // bound on |T32 - T64| / T
     uint32_t cnt = inside ? end - start : 0u;
     int flag = 0;
@@ -281,17 +281,18 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
-            if (lane == 0) swm[w][warp] = word;
+            if (lane == 0) swm[w][warp] = __brev(word);  // splat order from the MSB down
         }
         __syncthreads();
         if (!done) {
             const int nw = (int)((min((uint32_t)kTileThreads, end - b) + 31u) >> 5);
             for (int k = 0; k < nw && !done; ++k) {
                 uint32_t bits = swm[warp][k];
+                const float4 *rk = rbase + 128 * k;
                 while (bits) {
-                    const int j = (k << 5) + __ffs(bits) - 1;
-                    bits &= bits - 1u;
-                    const float4 *rp = rbase + 4 * j;
+                    const int o = __clz(bits);
+                    bits ^= 0x80000000u >> o;
+                    const float4 *rp = rk + 4 * o;
                     const float4 r0 = rp[0], r1 = rp[1];
                     const float dx = (pxf - r0.x) + r0.z;
                     const float dy = (pyf - r0.y) + r0.w;
@@ -305,11 +306,14 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const float4 r2 = rp[2], r3 = rp[3];
                     const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                     float a = ex2_approx(arg);
-                    const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
+                    // q = num / d; the T-error term a q / (1 - a) takes one reciprocal
+                    const float d = tau - m;
+                    const float num = fmaf(fmaf(fabsf(arg), 2.1e-7f, r3.z), d, r3.x);
                     float om = 1.0f - a;
                     if (a > clamp_lo) {
+                        const float qrel = num * rcp_approx(d);
                         if (a > clamp) {
-                            if (a * (1.0f - qrel) > clamp) hit[sid[j]] = 1;
+                            if (a * (1.0f - qrel) > clamp) hit[sid[(k << 5) + (int)((rp - rk) >> 2)]] = 1;
                             else flag = 1;
                             a = clamp;
                             om = one_minus_clamp;
@@ -317,12 +321,11 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                             flag |= (a * (1.0f + qrel) > clamp);
                         }
                     }
-                    err = fmaf(a * qrel, rcp_approx(om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
+                    err = fmaf(a * num, rcp_approx(d * om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
                     const float w = a * T;
                     a0 = fmaf(w, r2.y, a0);
                     a1 = fmaf(w, r2.z, a1);
                     a2 = fmaf(w, r2.w, a2);
-                    ws += w;
                     T *= om;
                     if (T < tmin_hi) {
                         const float band = err + 1.0e-6f;
@@ -330,7 +333,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                             // the reference stops before the next splat
                             flag |= (T > tmin * (1.0f - band));
                             done = true;
-                            cnt = b - start + (uint32_t)j + 1u;
+                            cnt = b - start + (uint32_t)((k << 5) + (int)((rp - rk) >> 2)) + 1u;
                             break;
                         }
                         flag |= (T < tmin * (1.0f + band));
@@ -346,7 +349,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
         image[3 * pix + 1] = fmaf(T, (float)P.bg[1], a1);
         image[3 * pix + 2] = fmaf(T, (float)P.bg[2], a2);
-        asum[pix] = ws;
+        asum[pix] = 1.0f - T;  // sum_i a_i T_i telescopes to 1 - T
         tstop[pix] = T;
         ncontrib[pix] = (int32_t)cnt;
     }
