@@ -18,7 +18,9 @@
  *
  * Stage map (reference function -> entry point here):
  *   slice_scene + project_scene        slicing.py:185-235, raster.py:95-134
- *                                      -> ubs_preprocess
+ *                                      -> ubs_scene_statics (query-invariant
+ *                                         half, once per parameter version)
+ *                                         + ubs_preprocess
  *   order = lexsort((ids, depth))      raster.py:274-275
  *   build_tiles                        raster.py:252-266
  *                                      -> ubs_bin_depth + ubs_bin_tiles
@@ -49,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 1
+#define UBS_ABI_VERSION 2
 #define UBS_TILE 16
 
 enum {
@@ -100,6 +102,9 @@ typedef struct UbsView {
     double query[4];
     UbsCamera cam;
     UbsSettings set;
+    /* Optional scene statics from ubs_scene_statics for these params and
+     * settings.psd_floor_scale (NULL: ubs_preprocess derives them inline). */
+    const void *statics;
 } UbsView;
 
 /* Per-primitive preprocess outputs (all length n unless noted). */
@@ -177,6 +182,15 @@ typedef struct UbsGradBuffers {
 /* --- entry points --- */
 int ubs_abi_version(void);
 const char *ubs_build_info(void);
+
+/* Query-invariant half of slice_scene (slicing.py:185-235 minus the
+ * conditional mean and gate): activations, Sx, the query-block inverse, Sxq,
+ * conditional covariance with its PSD floor, opacity, beta_x.  Written to a
+ * caller buffer of ubs_statics_bytes(n, n_dims, param_f64) bytes; valid while
+ * params and settings.psd_floor_scale are unchanged.  Set UbsView.statics to
+ * it and ubs_preprocess only runs the per-view half (same bits either way). */
+size_t ubs_statics_bytes(int64_t n, int32_t n_dims, int32_t param_f64);
+int ubs_scene_statics(const UbsView *v, void *statics, ubs_stream_t s);
 
 /* slice + project + tile rects (fp64 arithmetic, one thread per primitive) */
 int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32, ubs_stream_t s);

@@ -40,7 +40,7 @@ class UbsSettings(Structure):
 class UbsView(Structure):
     _fields_ = [("params", c_void_p), ("n", c_int64), ("n_dims", c_int32), ("param_f64", c_int32),
                 ("background", c_double * 3), ("query", c_double * 4), ("cam", UbsCamera),
-                ("set", UbsSettings)]
+                ("set", UbsSettings), ("statics", c_void_p)]
 
 
 class UbsPrimBuffers(Structure):
@@ -71,10 +71,14 @@ class UbsGradBuffers(Structure):
                 ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p)]
 
 
+ABI_VERSION = 2  # UBS_ABI_VERSION in include/ubs_b200.h
+
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares
 SIGNATURES = [
     ("ubs_abi_version", c_int32, []),
     ("ubs_build_info", ctypes.c_char_p, []),
+    ("ubs_statics_bytes", c_size_t, [c_int64, c_int32, c_int32]),
+    ("ubs_scene_statics", c_int32, [POINTER(UbsView), c_void_p, c_void_p]),
     ("ubs_preprocess", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), c_int32, c_void_p]),
     ("ubs_bin_temp_bytes", c_size_t, [c_int64, c_int64, c_int32]),
     ("ubs_bin_depth", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers), c_void_p]),
@@ -113,7 +117,7 @@ def load(build_if_needed: bool = True):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ubs_abi_version() != 1:
+    if lib.ubs_abi_version() != ABI_VERSION:
         raise UbsError("libubs_b200 ABI version mismatch")
     _LIB = lib
     return lib

@@ -19,19 +19,44 @@ namespace ubs {
 
 constexpr int kPreThreads = 128;
 
+// Scene statics: the query-invariant half of slice_scene for every primitive
+// (prim_static), written field-major (StaticLayout) for coalesced reads.
 template <int C, typename PT>
-__global__ void __launch_bounds__(kPreThreads, 4)
-preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
+__global__ void __launch_bounds__(kPreThreads)
+statics_kernel(const UbsView v, void *out) {
     constexpr int P = 14 + 6 * C;
     __shared__ PT stage[kPreThreads * P];
+    const int64_t base = (int64_t)blockIdx.x * kPreThreads;
+    const int64_t n = v.n;
+    const int nloc = (int)min((int64_t)kPreThreads, n - base);
+    const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
+    for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t >= nloc) return;
+    PrimGeom<C> g;
+    double mu_x[3], mu_q[PrimGeom<C>::CC];
+    prim_static<C, PT>(stage + t * P, v.set, g, mu_x, mu_q);
+    store_statics<C, PT>(out, base + t, n, g, mu_x, mu_q);
+}
+
+// kStatic: the query-invariant half comes from v.statics (ubs_scene_statics)
+// and only prim_view runs here; otherwise the whole of prim_geom.
+template <int C, typename PT, bool kStatic>
+__global__ void __launch_bounds__(kPreThreads, kStatic ? 5 : 4)
+preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
+    constexpr int P = 14 + 6 * C;
+    __shared__ PT stage[kStatic ? 1 : kPreThreads * P];
     __shared__ uint32_t block_vis;
     __shared__ unsigned long long block_pairs, block_dmin, block_dmax;
     const int64_t base = (int64_t)blockIdx.x * kPreThreads;
     const int64_t n = v.n;
     const int nloc = (int)min((int64_t)kPreThreads, n - base);
-    const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
     if (threadIdx.x == 0) { block_vis = 0; block_pairs = 0; block_dmin = ~0ull; block_dmax = 0; }
-    for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
+    if constexpr (!kStatic) {
+        const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
+        for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
+    }
     __syncthreads();
     const int t = threadIdx.x;
     bool vis = false;
@@ -41,7 +66,13 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
         const int64_t i = base + t;
         PrimGeom<C> g;
         double mu_x[3];
-        prim_geom<C, PT>(stage + t * P, v, g, mu_x);
+        if constexpr (kStatic) {
+            double mu_q[PrimGeom<C>::CC];
+            load_statics<C, PT>(v.statics, i, n, g, mu_x, mu_q);
+            prim_view<C>(g, mu_x, mu_q, v);
+        } else {
+            prim_geom<C, PT>(stage + t * P, v, g, mu_x);
+        }
 
         const int W = v.cam.width, H = v.cam.height;
         const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
@@ -180,7 +211,16 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
 template <int C, typename PT>
 static void launch_pre(const UbsView &v, const UbsPrimBuffers &pb, int want32, cudaStream_t s) {
     const int64_t blocks = (v.n + kPreThreads - 1) / kPreThreads;
-    preprocess_kernel<C, PT><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, pb, want32);
+    if (v.statics)
+        preprocess_kernel<C, PT, true><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, pb, want32);
+    else
+        preprocess_kernel<C, PT, false><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, pb, want32);
+}
+
+template <int C, typename PT>
+static void launch_statics(const UbsView &v, void *out, cudaStream_t s) {
+    const int64_t blocks = (v.n + kPreThreads - 1) / kPreThreads;
+    statics_kernel<C, PT><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, out);
 }
 
 }  // namespace ubs
@@ -219,6 +259,26 @@ extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_
                     : launch_pre<3, float>(*v, *pb, want_rec32, s); break;
         case 7: f64 ? launch_pre<4, double>(*v, *pb, want_rec32, s)
                     : launch_pre<4, float>(*v, *pb, want_rec32, s); break;
+        default: return UBS_E_ARGS;
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" size_t ubs_statics_bytes(int64_t n, int32_t n_dims, int32_t param_f64) {
+    if (n < 0 || (n_dims != 3 && n_dims != 6 && n_dims != 7)) return 0;
+    return statics_bytes(n, n_dims, param_f64);
+}
+
+extern "C" int ubs_scene_statics(const UbsView *v, void *statics, ubs_stream_t stream) {
+    if (!v || v->n < 0 || (v->n > 0 && (!v->params || !statics))) return UBS_E_ARGS;
+    if (v->n == 0) return UBS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool f64 = v->param_f64 != 0;
+    switch (v->n_dims) {
+        case 3: f64 ? launch_statics<0, double>(*v, statics, s) : launch_statics<0, float>(*v, statics, s); break;
+        case 6: f64 ? launch_statics<3, double>(*v, statics, s) : launch_statics<3, float>(*v, statics, s); break;
+        case 7: f64 ? launch_statics<4, double>(*v, statics, s) : launch_statics<4, float>(*v, statics, s); break;
         default: return UBS_E_ARGS;
     }
     UBS_CUDA_CHECK();

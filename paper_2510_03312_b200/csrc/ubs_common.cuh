@@ -228,10 +228,17 @@ __device__ __forceinline__ double sigmoid64(double x) {
     return e / (1.0 + e);
 }
 
+// Query-invariant half of slice_scene (slicing.py:185-235): activations,
+// Sx, the query block inverse M, Sxq, the conditional covariance with its PSD
+// floor, opacity and beta_x.  Depends on the parameters and psd_floor_scale
+// only, so a scene's statics are computed once per parameter version
+// (ubs_scene_statics) and shared by every view; prim_view does the rest with
+// the same operations in the same order, so both routes give identical bits.
 template <int C, typename PT>
-__device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g, double (&mu_x)[3]) {
+__device__ inline void prim_static(const PT *rec, const UbsSettings &set, PrimGeom<C> &g, double (&mu_x)[3],
+                                   double (&mu_q)[PrimGeom<C>::CC]) {
     constexpr int CC = PrimGeom<C>::CC;
-    double mu_q[CC], rot[3], sxr[3], lq[CC * 3], sqr[CC], bxr, bqr[CC], oraw;
+    double rot[3], sxr[3], lq[CC * 3], sqr[CC], bxr, bqr[CC], oraw;
     load_params<C>(rec, mu_x, mu_q, rot, sxr, lq, sqr, bxr, bqr, oraw, g.color);
 
     for (int k = 0; k < 3; ++k) g.sx[k] = exp(sxr[k]);
@@ -249,11 +256,9 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
     g.beta_x = 4.0 * exp(bxr);
     g.opacity = sigmoid64(oraw);
     g.valid = true;
-    double mean3[3] = {mu_x[0], mu_x[1], mu_x[2]};
     double raw[3][3];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) raw[i][j] = Sx[i][j];
-    g.gate = 1.0;
 
     if constexpr (C > 0) {
         for (int k = 0; k < C; ++k) {
@@ -288,21 +293,6 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
             for (int i = 0; i < C; ++i)
                 for (int j = 0; j < C; ++j) g.M[i][j] = (i == j) ? 1.0 : 0.0;
         }
-        // conditional mean (slicing.py:205-208)
-        for (int k = 0; k < C; ++k) {
-            g.delta[k] = v.query[k] - mu_q[k];
-            g.u[k] = g.beta_q[k] * g.delta[k];
-        }
-        for (int i = 0; i < C; ++i) {
-            double s = 0.0;
-            for (int k = 0; k < C; ++k) s += g.M[i][k] * g.u[k];
-            g.v[i] = s;
-        }
-        for (int i = 0; i < 3; ++i) {
-            double s = 0.0;
-            for (int k = 0; k < C; ++k) s += g.Sxq[i][k] * g.v[k];
-            mean3[i] = mu_x[i] + s;
-        }
         // conditional covariance: Sx - Sxq M diag(beta_q) Sqx (slicing.py:210-211)
         double H[3][C];  // Sxq M
         for (int i = 0; i < 3; ++i)
@@ -317,26 +307,12 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
                 for (int k = 0; k < C; ++k) s += H[i][k] * g.beta_q[k] * g.Sxq[j][k];
                 raw[i][j] = Sx[i][j] - s;
             }
-        // opacity gate (slicing.py:224-228)
-        double lsum = 0.0;
-        for (int i = 0; i < C; ++i) {
-            double dr = 0.0;
-            for (int k = 0; k < C; ++k) dr += g.M[i][k] * g.delta[k];
-            double s = tanh(0.5 * dr);
-            g.s_tanh[i] = s;
-            double d = v.set.gate_symmetric ? fabs(s) : fmax(s, 0.0);
-            g.d_gate[i] = d;
-            lsum += 4.0 * g.beta_q[i] * log1p(-d);
-        }
-        g.gate = exp(lsum);
     }
-    for (int i = 0; i < 3; ++i) g.mean3[i] = mean3[i];
-    g.og = g.opacity * g.gate;
 
     // symmetrise + PSD eigen floor (slicing.py:212-222)
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) g.sym3[i][j] = 0.5 * (raw[i][j] + raw[j][i]);
-    g.floor_eps = v.set.psd_floor_scale * (Sx[0][0] + Sx[1][1] + Sx[2][2]) / 3.0;
+    g.floor_eps = set.psd_floor_scale * (Sx[0][0] + Sx[1][1] + Sx[2][2]) / 3.0;
     {
         // cheap test first: sym - eps I positive definite <=> lambda_min > eps
         double T[3][3], L3[3][3];
@@ -359,6 +335,46 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
             }
         }
     }
+}
+
+// Per-view half of slice_scene (conditional mean slicing.py:205-208, opacity
+// gate :224-228) and project_scene (raster.py:99-131) on top of prim_static.
+template <int C>
+__device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const double (&mu_q)[PrimGeom<C>::CC],
+                                 const UbsView &v) {
+    double mean3[3] = {mu_x[0], mu_x[1], mu_x[2]};
+    g.gate = 1.0;
+    if constexpr (C > 0) {
+        // conditional mean (slicing.py:205-208)
+        for (int k = 0; k < C; ++k) {
+            g.delta[k] = v.query[k] - mu_q[k];
+            g.u[k] = g.beta_q[k] * g.delta[k];
+        }
+        for (int i = 0; i < C; ++i) {
+            double s = 0.0;
+            for (int k = 0; k < C; ++k) s += g.M[i][k] * g.u[k];
+            g.v[i] = s;
+        }
+        for (int i = 0; i < 3; ++i) {
+            double s = 0.0;
+            for (int k = 0; k < C; ++k) s += g.Sxq[i][k] * g.v[k];
+            mean3[i] = mu_x[i] + s;
+        }
+        // opacity gate (slicing.py:224-228)
+        double lsum = 0.0;
+        for (int i = 0; i < C; ++i) {
+            double dr = 0.0;
+            for (int k = 0; k < C; ++k) dr += g.M[i][k] * g.delta[k];
+            double s = tanh(0.5 * dr);
+            g.s_tanh[i] = s;
+            double d = v.set.gate_symmetric ? fabs(s) : fmax(s, 0.0);
+            g.d_gate[i] = d;
+            lsum += 4.0 * g.beta_q[i] * log1p(-d);
+        }
+        g.gate = exp(lsum);
+    }
+    for (int i = 0; i < 3; ++i) g.mean3[i] = mean3[i];
+    g.og = g.opacity * g.gate;
 
     // projection (raster.py:99-131)
     const double *Rc = v.cam.rot;
@@ -412,6 +428,92 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
     const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
     bool on_screen = (hix >= -mg) && (lox <= v.cam.width + mg) && (hiy >= -mg) && (loy <= v.cam.height + mg);
     g.visible = g.in_front && on_screen && g.valid;
+}
+
+template <int C, typename PT>
+__device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g, double (&mu_x)[3]) {
+    double mu_q[PrimGeom<C>::CC];
+    prim_static<C, PT>(rec, v.set, g, mu_x, mu_q);
+    prim_view<C>(g, mu_x, mu_q, v);
+}
+
+// Scene statics, structure of arrays (field-major, n per field): D fp64
+// fields then R raw fields at parameter precision.
+//   fp64: beta_q[C] | M upper triangle, row-major [C(C+1)/2] | Sxq[3][C] |
+//         cov3[3][3] | opacity | beta_x | floor_eps | flags
+//   raw:  mu_x[3] | mu_q[C] | color[3]
+// flags: 1 = valid (query block invertible), 2 = PSD-floored.
+template <int C>
+struct StaticLayout {
+    static constexpr int kBetaQ = 0;
+    static constexpr int kM = kBetaQ + C;
+    static constexpr int kSxq = kM + C * (C + 1) / 2;
+    static constexpr int kCov3 = kSxq + 3 * C;
+    static constexpr int kOpacity = kCov3 + 9;
+    static constexpr int kBetaX = kOpacity + 1;
+    static constexpr int kFloorEps = kBetaX + 1;
+    static constexpr int kFlags = kFloorEps + 1;
+    static constexpr int D = kFlags + 1;
+    static constexpr int R = 6 + C;
+};
+
+__host__ __device__ inline size_t statics_bytes(int64_t n, int n_dims, int param_f64) {
+    const int C = n_dims - 3;
+    const int D = C + C * (C + 1) / 2 + 3 * C + 13;
+    const int R = 6 + C;
+    return (size_t)n * (size_t)(8 * D + (param_f64 ? 8 : 4) * R);
+}
+
+template <int C, typename PT>
+__device__ inline void store_statics(void *buf, int64_t i, int64_t n, const PrimGeom<C> &g, const double (&mu_x)[3],
+                                     const double (&mu_q)[PrimGeom<C>::CC]) {
+    using L = StaticLayout<C>;
+    double *d = reinterpret_cast<double *>(buf);
+    PT *r = reinterpret_cast<PT *>(d + (size_t)L::D * n);
+    for (int k = 0; k < C; ++k) d[(L::kBetaQ + k) * n + i] = g.beta_q[k];
+    int o = L::kM;
+    for (int a = 0; a < C; ++a)
+        for (int b = a; b < C; ++b) d[(o++) * n + i] = g.M[a][b];
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < C; ++k) d[(L::kSxq + a * C + k) * n + i] = g.Sxq[a][k];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) d[(L::kCov3 + 3 * a + b) * n + i] = g.cov3[a][b];
+    d[L::kOpacity * n + i] = g.opacity;
+    d[L::kBetaX * n + i] = g.beta_x;
+    d[L::kFloorEps * n + i] = g.floor_eps;
+    d[L::kFlags * n + i] = (double)((g.valid ? 1 : 0) | (g.floored3 ? 2 : 0));
+    for (int k = 0; k < 3; ++k) r[k * n + i] = (PT)mu_x[k];
+    for (int k = 0; k < C; ++k) r[(3 + k) * n + i] = (PT)mu_q[k];
+    for (int k = 0; k < 3; ++k) r[(3 + C + k) * n + i] = (PT)g.color[k];
+}
+
+// M is symmetric bit for bit (chol_inverse sums Li[k][i] Li[k][j] in the same
+// k order for (i, j) and (j, i)), so its upper triangle restores it exactly;
+// the floored cov3 (V w V^T with left-to-right products) is not, so all nine
+// entries are kept.
+template <int C, typename PT>
+__device__ inline void load_statics(const void *buf, int64_t i, int64_t n, PrimGeom<C> &g, double (&mu_x)[3],
+                                    double (&mu_q)[PrimGeom<C>::CC]) {
+    using L = StaticLayout<C>;
+    const double *d = reinterpret_cast<const double *>(buf);
+    const PT *r = reinterpret_cast<const PT *>(d + (size_t)L::D * n);
+    for (int k = 0; k < C; ++k) g.beta_q[k] = __ldg(d + (L::kBetaQ + k) * n + i);
+    int o = L::kM;
+    for (int a = 0; a < C; ++a)
+        for (int b = a; b < C; ++b) g.M[a][b] = g.M[b][a] = __ldg(d + (o++) * n + i);
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < C; ++k) g.Sxq[a][k] = __ldg(d + (L::kSxq + a * C + k) * n + i);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) g.cov3[a][b] = __ldg(d + (L::kCov3 + 3 * a + b) * n + i);
+    g.opacity = __ldg(d + L::kOpacity * n + i);
+    g.beta_x = __ldg(d + L::kBetaX * n + i);
+    g.floor_eps = __ldg(d + L::kFloorEps * n + i);
+    const int fl = (int)__ldg(d + L::kFlags * n + i);
+    g.valid = (fl & 1) != 0;
+    g.floored3 = (fl & 2) != 0;
+    for (int k = 0; k < 3; ++k) mu_x[k] = (double)__ldg(r + k * n + i);
+    for (int k = 0; k < C; ++k) mu_q[k] = (double)__ldg(r + (3 + k) * n + i);
+    for (int k = 0; k < 3; ++k) g.color[k] = (double)__ldg(r + (3 + C + k) * n + i);
 }
 
 // Device-side capacity guard for the pair buffers: true (and the overflow

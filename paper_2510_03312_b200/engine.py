@@ -50,16 +50,61 @@ def _require_cuda(device) -> torch.device:
 
 
 class DeviceScene:
-    """A scene resident in HBM as packed UBS1 records (n x (14+6C))."""
+    """A scene resident in HBM as packed UBS1 records (n x (14+6C)).
 
-    def __init__(self, params: torch.Tensor, n_dims: int, background):
+    Also caches the scene statics (ubs_scene_statics: the query-invariant
+    half of slice_scene) for the current parameter version; every view of
+    the same parameters reuses them.  The cache key is the params tensor's
+    storage and in-place version counter (code that writes the records
+    behind torch's back, like DeviceAdam, bumps it) plus psd_floor_scale.
+    ``use_statics=False`` makes every preprocess derive them inline."""
+
+    def __init__(self, params: torch.Tensor, n_dims: int, background, use_statics: bool = True):
         if params.dim() != 2 or params.shape[1] != record_width(n_dims):
             raise ValueError("params must be (n, 14+6C)")
         if params.dtype not in (torch.float32, torch.float64):
             raise ValueError("params must be float32 or float64")
-        self.params = params.contiguous()
         self.n_dims = int(n_dims)
         self.background = tuple(float(b) for b in np.asarray(background, dtype=np.float64).reshape(3))
+        self.use_statics = bool(use_statics)
+        self._statics = None
+        self._statics_key = None
+        self.params = params.contiguous()
+
+    @property
+    def params(self) -> torch.Tensor:
+        return self._params
+
+    @params.setter
+    def params(self, t: torch.Tensor):
+        self._params = t
+        self._statics_key = None
+
+    def invalidate_statics(self):
+        self._statics_key = None
+
+    def statics_ptr(self, settings) -> int:
+        """Device pointer of up-to-date scene statics (recomputed on the
+        current stream when the parameters changed), or 0 when disabled."""
+        if not self.use_statics or self.n == 0:
+            return 0
+        p = self._params
+        key = (p.data_ptr(), p._version, float(settings.psd_floor_scale))
+        if key != self._statics_key:
+            lib = _lib.load()
+            f64 = 1 if p.dtype == torch.float64 else 0
+            nbytes = int(lib.ubs_statics_bytes(self.n, self.n_dims, f64))
+            if self._statics is None or self._statics.numel() < nbytes:
+                self._statics = torch.empty(nbytes, dtype=torch.uint8, device=p.device)
+            v = UbsView()
+            v.params = _ptr(p)
+            v.n = self.n
+            v.n_dims = self.n_dims
+            v.param_f64 = f64
+            v.set.psd_floor_scale = float(settings.psd_floor_scale)
+            check(lib.ubs_scene_statics(v, _ptr(self._statics), _stream_ptr()), "ubs_scene_statics")
+            self._statics_key = key
+        return _ptr(self._statics)
 
     @classmethod
     def from_scene(cls, scene, dtype=torch.float32, device="cuda") -> "DeviceScene":
@@ -114,6 +159,7 @@ def make_view(ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS) -> UbsView
     st.gate_symmetric = 1 if settings.gate_symmetric else 0
     st.tile_size = TILE
     v.set = st
+    v.statics = ds.statics_ptr(settings)
     return v
 
 

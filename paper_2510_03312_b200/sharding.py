@@ -149,6 +149,9 @@ class DeviceAdam:
                                      self.v.data_ptr(), int(self.params.shape[0]), self.n_dims, self.lr,
                                      self.step_count, self.freeze, torch.cuda.current_stream().cuda_stream),
                    "ubs_adam_step")
+        # the records changed behind torch's back: bump the version counter so
+        # DeviceScene's statics cache sees new parameters
+        torch.autograd.graph.increment_version(self.params)
 
 
 def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=DEFAULT_SETTINGS, group=None,

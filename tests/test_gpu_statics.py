@@ -1,0 +1,86 @@
+"""Scene statics (ubs_scene_statics): the preprocess that reads the cached
+query-invariant half must produce exactly the bits of the preprocess that
+derives it inline -- depth keys, tile rects, flags, fp64/fp32 raster records
+and the debug dump of intermediates -- for every dimensionality, parameter
+precision and the branch-coverage scene (PSD floor, screen floor, degenerate
+query blocks, gate saturation)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2510_03312_b200 import engine, synthetic as S
+from paper_2510_03312_b200.types import DEFAULT_SETTINGS, Query
+
+from .helpers import branch_scene, screen_floor_case
+
+pytestmark = pytest.mark.gpu
+
+
+def _prims(scene, cam, q, dtype, precision, use_statics):
+    ds = engine.DeviceScene.from_scene(scene, dtype=dtype, device="cuda")
+    ds.use_statics = use_statics
+    ws = engine.Workspace("cuda", precision)
+    engine.render_frame(ws, ds, cam, q, DEFAULT_SETTINGS, want_debug=True, sync=True)
+    n = ds.n
+    out = {"depth_key": ws.depth_key[:n], "rect": ws.rect[:n], "flags": ws.flags[:n],
+           "rec64": ws.rec64[:n * 10], "debug": ws.debug[:n * 32]}
+    if ws.rec32 is not None:
+        out["rec32"] = ws.rec32[:n * 16]
+    return {k: v.clone().cpu() for k, v in out.items()}, ws
+
+
+def _cases():
+    out = []
+    for nd in (3, 6, 7):
+        sc = S.synth(nd, 3000, seed=11 + nd)
+        cam = S.bench_camera(320, 240)
+        out.append((f"synth{nd}", sc, cam, S.bench_query(nd, cam, 0.3)))
+    sc = branch_scene(seed=5, n=400)
+    cam = S.bench_camera(256, 192)
+    out.append(("branch", sc, cam, S.bench_query(7, cam, 0.5)))
+    sc, cam = screen_floor_case()[:2]
+    out.append(("screen_floor", sc, cam, Query.static()))
+    return out
+
+
+@pytest.mark.parametrize("precision,dtype", [("fp32", torch.float32), ("fp64", torch.float64),
+                                             ("fp32", torch.float64)])
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
+def test_statics_route_is_bit_identical(case, precision, dtype):
+    _, sc, cam, q = case
+    a, _ = _prims(sc, cam, q, dtype, precision, use_statics=False)
+    b, _ = _prims(sc, cam, q, dtype, precision, use_statics=True)
+    for k in a:
+        x, y = a[k], b[k]
+        if x.dtype.is_floating_point:
+            x, y = x.view(torch.int32 if x.dtype == torch.float32 else torch.int64), \
+                y.view(torch.int32 if y.dtype == torch.float32 else torch.int64)
+        assert torch.equal(x, y), f"{k} differs between the statics and inline preprocess"
+
+
+def test_statics_follow_parameter_updates():
+    """In-place parameter writes (torch ops or DeviceAdam's ctypes update,
+    which bumps the version counter) invalidate the cached statics."""
+    from paper_2510_03312_b200.sharding import DeviceAdam
+    sc = S.synth(7, 2000, seed=3)
+    cam = S.bench_camera(320, 240)
+    q = S.bench_query(7, cam, 0.5)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    engine.render_frame(ws, ds, cam, q, sync=True)
+    k0 = ds._statics_key
+    opt = DeviceAdam(ds.params, 7)
+    g = torch.randn(ds.params.shape, device="cuda")
+    opt.step(g)
+    engine.render_frame(ws, ds, cam, q, want_debug=True, sync=True)
+    assert ds._statics_key != k0
+    got = ws.debug[:ds.n * 32].clone()
+    ref = engine.DeviceScene(ds.params.clone(), 7, sc.background, use_statics=False)
+    ws2 = engine.Workspace("cuda", "fp32")
+    engine.render_frame(ws2, ref, cam, q, want_debug=True, sync=True)
+    assert torch.equal(got.view(torch.int64), ws2.debug[:ds.n * 32].view(torch.int64))
+    ds.params.mul_(1.0)  # torch in-place op: version bump
+    assert ds.statics_ptr(DEFAULT_SETTINGS) and ds._statics_key[1] == ds.params._version
