@@ -4,10 +4,9 @@
 // raster.py:252-266 (build_tiles, an O(tiles x N) mask loop on the CPU).
 //
 // Device algorithm:
-//   1. stable LSD radix sort (CUB) of (f64 depth bits, id) over all n
-//      primitives; invisible primitives carry an all-ones key and sort to the
-//      back.  With values emitted in id order the stable sort reproduces
-//      lexsort.
+//   1. bucket sort of the visible primitives by (f64 depth bits, id): range-
+//      normalised key histogram, scan, scatter, exact rank inside each bucket
+//      (reproduces lexsort, ties by id).
 //   2. per-tile [start, end): the preprocess kernel adds each visible rect's
 //      corners to a 2D difference array whose prefix sums are the per-tile
 //      counts (tile_scan_kernel); no pass over the K pairs.
@@ -15,53 +14,87 @@
 //      "Sort-free stable binning" block below.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "ubs_common.cuh"
 
 namespace ubs {
 
-// 32-bit sort keys: (depth bits - min) >> shift with shift chosen so every
-// visible key is < 2^31 (strictly below the invisible key 0xFFFFFFFF); ids in
-// id order so the stable sort breaks ties by id.
-__global__ void depth_key32_kernel(const uint64_t *__restrict__ key64, const unsigned long long *__restrict__ range,
-                                   int64_t n, uint32_t *__restrict__ key32, uint32_t *__restrict__ ids) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned long long lo = range[0], hi = range[1];
-    const unsigned long long span = hi >= lo ? hi - lo : 0ull;
-    const int bits = span ? 64 - __clzll((long long)span) : 0;
-    const int shift = bits > 31 ? bits - 31 : 0;
-    const uint64_t k = key64[i];
-    key32[i] = (k == kInvisibleKey) ? 0xFFFFFFFFu : (uint32_t)((k - lo) >> shift);
-    ids[i] = (uint32_t)i;
+// Depth order = lexsort((ids, depth)) (raster.py:274-275) as a bucket sort.
+// key32 = (f64 depth bits - min) >> shift (< 2^31, monotone in depth); its top
+// log2(B) bits pick one of B ~ n/4 buckets.  (1) histogram, (2) exclusive
+// scan (CUB), (3) scatter of (f64 bits, id) into bucket slots in arrival
+// order, (4) inside each bucket every element counts the elements that
+// precede it by (f64 bits, id) -- the exact lexsort order, ties by id -- and
+// writes its id there.  O(n) traffic in four light passes; the rank step is
+// O(s) per element for a bucket of s elements (a few on average; thousands
+// only if that many primitives share nearly the same depth bits).
+__host__ __device__ inline int sort_log_buckets(int64_t n) {
+    int l = 12;
+    while (l < 24 && ((int64_t)4 << l) < n) ++l;
+    return l;
 }
 
-// Exact order inside runs of equal 32-bit keys: the thread at a run start
-// insertion-sorts the run by (full f64 key, id).  Runs are rare and short
-// (~1e2 pairs of 2 among 1M visible primitives).
-__global__ void depth_tie_repair_kernel(const uint32_t *__restrict__ key32s, const uint64_t *__restrict__ key64,
-                                        const uint32_t *__restrict__ n_visible, uint32_t *__restrict__ order) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nv = *n_visible;
-    if (r + 1 >= nv) return;
-    const uint32_t k = key32s[r];
-    if (key32s[r + 1] != k || (r > 0 && key32s[r - 1] == k)) return;
-    int64_t e = r + 2;
-    while (e < nv && key32s[e] == k) ++e;
-    for (int64_t i = r + 1; i < e; ++i) {
-        const uint32_t id = order[i];
-        const uint64_t kk = key64[id];
-        int64_t j = i;
-        while (j > r) {
-            const uint32_t pj = order[j - 1];
-            const uint64_t kp = key64[pj];
-            if (kp < kk || (kp == kk && pj < id)) break;
-            order[j] = pj;
-            --j;
-        }
-        order[j] = id;
+struct DepthBuckets {
+    unsigned long long lo;
+    int shift, bshift;
+};
+
+__device__ __forceinline__ DepthBuckets depth_buckets(const unsigned long long *range, int logB) {
+    DepthBuckets d;
+    d.lo = range[0];
+    const unsigned long long hi = range[1];
+    const unsigned long long span = hi >= d.lo ? hi - d.lo : 0ull;
+    const int bits = span ? 64 - __clzll((long long)span) : 0;
+    d.shift = bits > 31 ? bits - 31 : 0;
+    d.bshift = 31 - logB;
+    return d;
+}
+
+__device__ __forceinline__ uint32_t depth_bucket(const DepthBuckets &d, uint64_t k) {
+    return (uint32_t)((k - d.lo) >> d.shift) >> d.bshift;
+}
+
+__global__ void depth_hist_kernel(const uint64_t *__restrict__ key64, const unsigned long long *__restrict__ range,
+                                  int64_t n, int logB, uint32_t *__restrict__ hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = key64[i];
+    if (k == kInvisibleKey) return;
+    atomicAdd(hist + depth_bucket(depth_buckets(range, logB), k), 1u);
+}
+
+// hist[b] counts down to 0 while slots [start[b], start[b] + count) fill
+__global__ void depth_scatter_kernel(const uint64_t *__restrict__ key64, const unsigned long long *__restrict__ range,
+                                     int64_t n, int logB, const uint32_t *__restrict__ start,
+                                     uint32_t *__restrict__ hist, uint64_t *__restrict__ tkey,
+                                     uint32_t *__restrict__ tid) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = key64[i];
+    if (k == kInvisibleKey) return;
+    const uint32_t b = depth_bucket(depth_buckets(range, logB), k);
+    const uint32_t pos = start[b] + atomicSub(hist + b, 1u) - 1u;
+    tkey[pos] = k;
+    tid[pos] = (uint32_t)i;
+}
+
+__global__ void depth_rank_kernel(const unsigned long long *__restrict__ range, int logB,
+                                  const uint32_t *__restrict__ start, const uint64_t *__restrict__ tkey,
+                                  const uint32_t *__restrict__ tid, const uint32_t *__restrict__ n_visible,
+                                  uint32_t *__restrict__ order) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (int64_t)*n_visible) return;
+    const uint64_t k = tkey[p];
+    const uint32_t id = tid[p];
+    const uint32_t b = depth_bucket(depth_buckets(range, logB), k);
+    const uint32_t s0 = start[b], s1 = start[b + 1];
+    uint32_t rank = 0;
+    for (uint32_t q = s0; q < s1; ++q) {
+        const uint64_t kq = tkey[q];
+        rank += (kq < k || (kq == k && tid[q] < id)) ? 1u : 0u;
     }
+    order[s0 + rank] = id;
 }
 
 // Per-tile [start, end) from the rect-corner difference array (one CTA):
@@ -446,14 +479,19 @@ tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restri
 
 using namespace ubs;
 
+// temp: hist (B + 1) | start (B + 1) | CUB scan scratch
+static size_t depth_scan_bytes(int64_t n) {
+    const int B = 1 << sort_log_buckets(n);
+    size_t a = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (const uint32_t *)nullptr, (uint32_t *)nullptr, B + 1);
+    return a;
+}
+
 extern "C" size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles) {
     (void)pair_capacity;
     (void)n_tiles;
-    size_t a = 0;
-    const int nn = (int)(n > 0 ? n : 1);
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, nn, 0, 32);
-    return a + 256;
+    const size_t B = (size_t)1 << sort_log_buckets(n);
+    return 2 * ((B + 1) * sizeof(uint32_t) + 256) + depth_scan_bytes(n) + 256;
 }
 
 extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
@@ -471,16 +509,25 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
         UBS_CUDA_CHECK();
         return UBS_OK;
     }
+    const int logB = sort_log_buckets(n);
+    const size_t B = (size_t)1 << logB;
+    const size_t arr = ((B + 1) * sizeof(uint32_t) + 255) & ~(size_t)255;
+    size_t scan_bytes = depth_scan_bytes(n);
+    if (bb->temp_bytes < 2 * arr + scan_bytes) return UBS_E_CAPACITY;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(bb->temp);
+    uint32_t *start = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(bb->temp) + arr);
+    void *scan_tmp = reinterpret_cast<char *>(bb->temp) + 2 * arr;
+    uint64_t *tkey = reinterpret_cast<uint64_t *>(bb->keys_sorted);
     const int thr = 256;
     const unsigned blocks = (unsigned)((n + thr - 1) / thr);
-    uint32_t *k32 = reinterpret_cast<uint32_t *>(bb->keys_sorted);
-    uint32_t *k32s = k32 + n;
-    depth_key32_kernel<<<blocks, thr, 0, s>>>(pb->depth_key, pb->depth_range, n, k32, bb->ids_iota);
-    size_t bytes = bb->temp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(bb->temp, bytes, k32, k32s, bb->ids_iota, bb->order, (int)n, 0, 32, s) !=
-        cudaSuccess)
+    if (cudaMemsetAsync(hist, 0, (B + 1) * sizeof(uint32_t), s) != cudaSuccess) return UBS_E_CUDA;
+    depth_hist_kernel<<<blocks, thr, 0, s>>>(pb->depth_key, pb->depth_range, n, logB, hist);
+    if (cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, hist, start, (int)(B + 1), s) != cudaSuccess)
         return UBS_E_CUDA;
-    depth_tie_repair_kernel<<<blocks, thr, 0, s>>>(k32s, pb->depth_key, pb->n_visible, bb->order);
+    depth_scatter_kernel<<<blocks, thr, 0, s>>>(pb->depth_key, pb->depth_range, n, logB, start, hist, tkey,
+                                                bb->ids_iota);
+    depth_rank_kernel<<<blocks, thr, 0, s>>>(pb->depth_range, logB, start, tkey, bb->ids_iota, pb->n_visible,
+                                             bb->order);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
