@@ -37,7 +37,7 @@ statics_kernel(const UbsView v, void *out) {
     PrimGeom<C> g;
     double mu_x[3], mu_q[PrimGeom<C>::CC];
     prim_static<C, PT>(stage + t * P, v.set, g, mu_x, mu_q);
-    store_statics<C, PT>(out, base + t, n, g, mu_x, mu_q);
+    store_statics<C, PT>(out, base + t, g, mu_x, mu_q);
 }
 
 // kStatic: the query-invariant half comes from v.statics (ubs_scene_statics)
@@ -68,7 +68,7 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
         double mu_x[3];
         if constexpr (kStatic) {
             double mu_q[PrimGeom<C>::CC];
-            load_statics<C, PT>(v.statics, i, n, g, mu_x, mu_q);
+            load_statics<C, PT>(v.statics, i, g, mu_x, mu_q);
             prim_view<C>(g, mu_x, mu_q, v);
         } else {
             prim_geom<C, PT>(stage + t * P, v, g, mu_x);

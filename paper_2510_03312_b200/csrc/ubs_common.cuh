@@ -437,12 +437,16 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
     prim_view<C>(g, mu_x, mu_q, v);
 }
 
-// Scene statics, structure of arrays (field-major, n per field): D fp64
-// fields then R raw fields at parameter precision.
+// Scene statics, tiled structure of arrays: blocks of kStaticBlock
+// primitives, each block holding D fp64 fields then R raw fields at parameter
+// precision, field-major inside the block (every field load of a warp is one
+// coalesced access at a constant offset from the block base).
 //   fp64: beta_q[C] | M upper triangle, row-major [C(C+1)/2] | Sxq[3][C] |
 //         cov3[3][3] | opacity | beta_x | floor_eps | flags
 //   raw:  mu_x[3] | mu_q[C] | color[3]
 // flags: 1 = valid (query block invertible), 2 = PSD-floored.
+constexpr int kStaticBlock = 128;
+
 template <int C>
 struct StaticLayout {
     static constexpr int kBetaQ = 0;
@@ -457,34 +461,51 @@ struct StaticLayout {
     static constexpr int R = 6 + C;
 };
 
-__host__ __device__ inline size_t statics_bytes(int64_t n, int n_dims, int param_f64) {
+__host__ __device__ inline size_t static_block_bytes(int n_dims, int param_f64) {
     const int C = n_dims - 3;
     const int D = C + C * (C + 1) / 2 + 3 * C + 13;
     const int R = 6 + C;
-    return (size_t)n * (size_t)(8 * D + (param_f64 ? 8 : 4) * R);
+    return (size_t)kStaticBlock * (size_t)(8 * D + (param_f64 ? 8 : 4) * R);
+}
+
+__host__ __device__ inline size_t statics_bytes(int64_t n, int n_dims, int param_f64) {
+    return (size_t)((n + kStaticBlock - 1) / kStaticBlock) * static_block_bytes(n_dims, param_f64);
+}
+
+// fp64 and raw field bases of primitive i (field f at [f * kStaticBlock])
+template <int C, typename PT>
+__device__ __forceinline__ void static_slot(void *buf, int64_t i, double *&d, PT *&r) {
+    using L = StaticLayout<C>;
+    constexpr size_t kBlock = (size_t)kStaticBlock * (8 * L::D + sizeof(PT) * L::R);
+    char *blk = reinterpret_cast<char *>(buf) + (size_t)(i / kStaticBlock) * kBlock;
+    const int t = (int)(i % kStaticBlock);
+    d = reinterpret_cast<double *>(blk) + t;
+    r = reinterpret_cast<PT *>(blk + (size_t)kStaticBlock * 8 * L::D) + t;
 }
 
 template <int C, typename PT>
-__device__ inline void store_statics(void *buf, int64_t i, int64_t n, const PrimGeom<C> &g, const double (&mu_x)[3],
+__device__ inline void store_statics(void *buf, int64_t i, const PrimGeom<C> &g, const double (&mu_x)[3],
                                      const double (&mu_q)[PrimGeom<C>::CC]) {
     using L = StaticLayout<C>;
-    double *d = reinterpret_cast<double *>(buf);
-    PT *r = reinterpret_cast<PT *>(d + (size_t)L::D * n);
-    for (int k = 0; k < C; ++k) d[(L::kBetaQ + k) * n + i] = g.beta_q[k];
+    constexpr int S = kStaticBlock;
+    double *d;
+    PT *r;
+    static_slot<C, PT>(buf, i, d, r);
+    for (int k = 0; k < C; ++k) d[(L::kBetaQ + k) * S] = g.beta_q[k];
     int o = L::kM;
     for (int a = 0; a < C; ++a)
-        for (int b = a; b < C; ++b) d[(o++) * n + i] = g.M[a][b];
+        for (int b = a; b < C; ++b) d[(o++) * S] = g.M[a][b];
     for (int a = 0; a < 3; ++a)
-        for (int k = 0; k < C; ++k) d[(L::kSxq + a * C + k) * n + i] = g.Sxq[a][k];
+        for (int k = 0; k < C; ++k) d[(L::kSxq + a * C + k) * S] = g.Sxq[a][k];
     for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) d[(L::kCov3 + 3 * a + b) * n + i] = g.cov3[a][b];
-    d[L::kOpacity * n + i] = g.opacity;
-    d[L::kBetaX * n + i] = g.beta_x;
-    d[L::kFloorEps * n + i] = g.floor_eps;
-    d[L::kFlags * n + i] = (double)((g.valid ? 1 : 0) | (g.floored3 ? 2 : 0));
-    for (int k = 0; k < 3; ++k) r[k * n + i] = (PT)mu_x[k];
-    for (int k = 0; k < C; ++k) r[(3 + k) * n + i] = (PT)mu_q[k];
-    for (int k = 0; k < 3; ++k) r[(3 + C + k) * n + i] = (PT)g.color[k];
+        for (int b = 0; b < 3; ++b) d[(L::kCov3 + 3 * a + b) * S] = g.cov3[a][b];
+    d[L::kOpacity * S] = g.opacity;
+    d[L::kBetaX * S] = g.beta_x;
+    d[L::kFloorEps * S] = g.floor_eps;
+    d[L::kFlags * S] = (double)((g.valid ? 1 : 0) | (g.floored3 ? 2 : 0));
+    for (int k = 0; k < 3; ++k) r[k * S] = (PT)mu_x[k];
+    for (int k = 0; k < C; ++k) r[(3 + k) * S] = (PT)mu_q[k];
+    for (int k = 0; k < 3; ++k) r[(3 + C + k) * S] = (PT)g.color[k];
 }
 
 // M is symmetric bit for bit (chol_inverse sums Li[k][i] Li[k][j] in the same
@@ -492,28 +513,30 @@ __device__ inline void store_statics(void *buf, int64_t i, int64_t n, const Prim
 // the floored cov3 (V w V^T with left-to-right products) is not, so all nine
 // entries are kept.
 template <int C, typename PT>
-__device__ inline void load_statics(const void *buf, int64_t i, int64_t n, PrimGeom<C> &g, double (&mu_x)[3],
+__device__ inline void load_statics(const void *buf, int64_t i, PrimGeom<C> &g, double (&mu_x)[3],
                                     double (&mu_q)[PrimGeom<C>::CC]) {
     using L = StaticLayout<C>;
-    const double *d = reinterpret_cast<const double *>(buf);
-    const PT *r = reinterpret_cast<const PT *>(d + (size_t)L::D * n);
-    for (int k = 0; k < C; ++k) g.beta_q[k] = __ldg(d + (L::kBetaQ + k) * n + i);
+    constexpr int S = kStaticBlock;
+    double *d;
+    PT *r;
+    static_slot<C, PT>(const_cast<void *>(buf), i, d, r);
+    for (int k = 0; k < C; ++k) g.beta_q[k] = __ldg(d + (L::kBetaQ + k) * S);
     int o = L::kM;
     for (int a = 0; a < C; ++a)
-        for (int b = a; b < C; ++b) g.M[a][b] = g.M[b][a] = __ldg(d + (o++) * n + i);
+        for (int b = a; b < C; ++b) g.M[a][b] = g.M[b][a] = __ldg(d + (o++) * S);
     for (int a = 0; a < 3; ++a)
-        for (int k = 0; k < C; ++k) g.Sxq[a][k] = __ldg(d + (L::kSxq + a * C + k) * n + i);
+        for (int k = 0; k < C; ++k) g.Sxq[a][k] = __ldg(d + (L::kSxq + a * C + k) * S);
     for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) g.cov3[a][b] = __ldg(d + (L::kCov3 + 3 * a + b) * n + i);
-    g.opacity = __ldg(d + L::kOpacity * n + i);
-    g.beta_x = __ldg(d + L::kBetaX * n + i);
-    g.floor_eps = __ldg(d + L::kFloorEps * n + i);
-    const int fl = (int)__ldg(d + L::kFlags * n + i);
+        for (int b = 0; b < 3; ++b) g.cov3[a][b] = __ldg(d + (L::kCov3 + 3 * a + b) * S);
+    g.opacity = __ldg(d + L::kOpacity * S);
+    g.beta_x = __ldg(d + L::kBetaX * S);
+    g.floor_eps = __ldg(d + L::kFloorEps * S);
+    const int fl = (int)__ldg(d + L::kFlags * S);
     g.valid = (fl & 1) != 0;
     g.floored3 = (fl & 2) != 0;
-    for (int k = 0; k < 3; ++k) mu_x[k] = (double)__ldg(r + k * n + i);
-    for (int k = 0; k < C; ++k) mu_q[k] = (double)__ldg(r + (3 + k) * n + i);
-    for (int k = 0; k < 3; ++k) g.color[k] = (double)__ldg(r + (3 + C + k) * n + i);
+    for (int k = 0; k < 3; ++k) mu_x[k] = (double)__ldg(r + k * S);
+    for (int k = 0; k < C; ++k) mu_q[k] = (double)__ldg(r + (3 + k) * S);
+    for (int k = 0; k < 3; ++k) g.color[k] = (double)__ldg(r + (3 + C + k) * S);
 }
 
 // Device-side capacity guard for the pair buffers: true (and the overflow
