@@ -186,17 +186,22 @@ def run_reference(a, rank, world):
 # ---------------------------------------------------------------------------
 # ours
 # ---------------------------------------------------------------------------
-def algorithmic_bytes(stage, n, P, n_vis, k, npix, ntiles):
-    """Algorithmic HBM bytes of one launch of each stage."""
+def algorithmic_bytes(stage, n, statics_per_prim, n_vis, entries, ids, npix, ntiles):
+    """Algorithmic HBM bytes of one launch of each stage.
+
+    entries: level-1 bucket entries of the frame; ids: tile-list ids
+    materialised (list prefixes up to the cap)."""
     return {
-        # read params, write key 8 + rect 8 + count 4 + flags 2 + rec32 64 + rec64 80
-        "preprocess": n * (4 * P + 166),
-        # radix sort (key 8 + id 4, one read+write pass), count gather 12, scan 8
-        "bin_depth": n * (24 + 12 + 8),
-        # emit 8 per pair (+ order/offset/rect/count reads 24 per visible), sort pass 16, ranges 4, 8/tile
-        "bin_tiles": k * (8 + 16 + 4) + n_vis * 24 + ntiles * 8,
-        # tile ranges 8/tile, ids 4 per pair, each visible record 64 once, outputs 20 per pixel
-        "raster": ntiles * 8 + 4 * k + 64 * n_vis + 20 * npix,
+        # read the scene statics, write key 8 + rect 8 + count 4 + flags 2 + rec32 64 + rec64 80
+        "preprocess": n * (statics_per_prim + 166),
+        # tile ranges 8/tile; depth keys read twice (histogram, scatter), (key, id) 12 written
+        # and read back, order 4 written
+        "bin_depth": ntiles * 8 + n * 16 + n_vis * (12 + 12 + 4),
+        # order 4 + rect 8 + count 4 per visible rank (histogram and scatter passes), entries
+        # 8 written + 8 read, ids 4 written, ranges 8 per tile
+        "bin_tiles": n_vis * 32 + entries * 16 + ids * 4 + ntiles * 8,
+        # ranges 8/tile, the consumed ids 4 each, every visible record 64 once, outputs 24 per pixel
+        "raster": ntiles * 8 + 4 * ids + 64 * n_vis + 24 * npix,
         "fixup": 0,
     }[stage]
 
@@ -279,12 +284,15 @@ def run_ours(a, rank, world, local_rank):
     # (capacity grows by 1.3x), the timed frames are fully asynchronous
     for k in range(max(a.warmup, 0)):
         frame(k, sync=True)
-    stats = {"n_vis": 0, "k": 0, "frames": 0}
+    stats = {"n_vis": 0, "k": 0, "frames": 0, "entries": 0, "ids": 0}
     for k in range(0, SWEEP, 25):
         fr = frame(k, sync=True)
         stats["n_vis"] += fr.n_visible
         stats["k"] += fr.n_pairs
         stats["frames"] += 1
+        e, i = engine.list_stats(ws, fr)
+        stats["entries"] += e
+        stats["ids"] += i
     torch.cuda.synchronize()
 
     # --- device-resident throughput -------------------------------------
@@ -295,6 +303,7 @@ def run_ours(a, rank, world, local_rank):
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ds.invalidate_statics()  # the sweep pays its one scene-statics pass
         e0.record()
         for k in range(a.steps):
             fr = frame(k, timers)
@@ -333,7 +342,10 @@ def run_ours(a, rank, world, local_rank):
     ntiles = -(-a.width // 16) * -(-a.height // 16)
     n_vis = stats["n_vis"] / stats["frames"]  # sweep average over 12 sampled frames
     kk = stats["k"] / stats["frames"]
-    b_dom = algorithmic_bytes(dominant, n, P, n_vis, kk, npix, ntiles)
+    ent = stats["entries"] / stats["frames"]
+    nids = stats["ids"] / stats["frames"]
+    spp = ds.statics_bytes_per_prim()
+    b_dom = algorithmic_bytes(dominant, n, spp, n_vis, ent, nids, npix, ntiles)
     peak, peak_src = measured_peak()
     achieved = b_dom / (stage_ms[dominant] / 1e3) / 1e9
     b_frame = n * (4 * P + 64) + 72 * n_vis + 48 * kk + 20 * npix  # SURVEY §8(d) B_fwd
@@ -347,6 +359,7 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ds.invalidate_statics()
     f0.record()
     for k in range(a.steps):
         sink.submit(frame(k))
@@ -380,9 +393,10 @@ def run_ours(a, rank, world, local_rank):
     if rank != 0:
         return None
     # kernels of libubs_b200.so per frame (ncu launch list, profiles/): preprocess, tile_scan,
-    # depth_key32, CUB radix sort (histogram + exclusive sum + 4 onesweep), tie repair,
-    # bucket hist / segsum / segscan / start / offsets / scatter, tile_lists, raster, fixup
-    per_frame_launches = 19
+    # depth hist, CUB scan (init + scan), depth scatter, depth rank, bucket hist / segsum /
+    # segscan / start / offsets / scatter, tile_lists, raster, fixup; plus one scene-statics
+    # pass per sweep
+    per_frame_launches = 16
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -404,7 +418,7 @@ def run_ours(a, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": sink.bytes_per_frame,
                 "path": "engine.render_frame + HostFrameSink (fp32 image -> pinned host, copy stream)"},
-        "gpu_launches": per_frame_launches * a.steps,
+        "gpu_launches": per_frame_launches * a.steps + 1,
         "clocks": clocks,
         "train": train,
     }

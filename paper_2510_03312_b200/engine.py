@@ -83,6 +83,10 @@ class DeviceScene:
     def invalidate_statics(self):
         self._statics_key = None
 
+    def statics_bytes_per_prim(self) -> float:
+        f64 = 1 if self._params.dtype == torch.float64 else 0
+        return _lib.load().ubs_statics_bytes(1 << 20, self.n_dims, f64) / float(1 << 20)
+
     def statics_ptr(self, settings) -> int:
         """Device pointer of up-to-date scene statics (recomputed on the
         current stream when the parameters changed), or 0 when disabled."""
@@ -456,6 +460,22 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
                  image=ws.image_buf[:npix * 3].view(H, W, 3), alpha_sum=ws.asum_buf[:npix].view(H, W),
                  t_stop=ws.tstop_buf[:npix].view(H, W), n_contrib=ws.ncontrib_buf[:npix].view(H, W),
                  hit_clamp=ws.hit_clamp[:n], ws=ws, raster_f64=ws.f64)
+
+
+def list_stats(ws: "Workspace", fr: "Frame") -> tuple[int, int]:
+    """(level-1 bucket entries, tile-list ids materialised) of the last frame
+    rendered with ``ws`` (synchronises; for reporting only)."""
+    W, H = fr.width, fr.height
+    TX, TY = -(-W // TILE), -(-H // TILE)
+    NB = -(-TX // 8)
+    nbk = TY * NB
+    entries = int(ws.bucket_start[nbk].item()) & 0xFFFFFFFF if ws.bucket_start is not None else 0
+    rng = ws.tile_ranges[:2 * TX * TY].view(-1, 2).long()
+    lens = (rng[:, 1] - rng[:, 0]).clamp_(min=0)
+    cap = ws.frame_list_cap
+    if 0 < cap < (1 << 31):
+        lens = lens.clamp_(max=cap)
+    return entries, int(lens.sum().item())
 
 
 def check_status(ws: Workspace) -> int:
