@@ -291,10 +291,11 @@ class Workspace:
 
     CHUNK_RANKS = 1024  # ranks per level-1 binning CTA chunk (csrc/binning.cu kCtaRanks)
     BAND = 8            # tile columns per level-1 bucket (csrc/binning.cu kBand)
+    ROWS = 4            # tile rows per level-1 bucket (csrc/binning.cu kRows)
 
     def ensure_chunks(self, n: int, width: int, height: int):
         tx, ty = math.ceil(width / TILE), math.ceil(height / TILE)
-        nbk = ty * math.ceil(tx / self.BAND)
+        nbk = math.ceil(ty / self.ROWS) * math.ceil(tx / self.BAND)
         g = max(1, -(-n // self.CHUNK_RANKS))
         self.chunk_count = g
         if self.chunk_hist is None or self.chunk_hist.numel() < 2 * g * nbk:
@@ -467,8 +468,7 @@ def list_stats(ws: "Workspace", fr: "Frame") -> tuple[int, int]:
     rendered with ``ws`` (synchronises; for reporting only)."""
     W, H = fr.width, fr.height
     TX, TY = -(-W // TILE), -(-H // TILE)
-    NB = -(-TX // 8)
-    nbk = TY * NB
+    nbk = -(-TY // Workspace.ROWS) * -(-TX // Workspace.BAND)
     entries = int(ws.bucket_start[nbk].item()) & 0xFFFFFFFF if ws.bucket_start is not None else 0
     rng = ws.tile_ranges[:2 * TX * TY].view(-1, 2).long()
     lens = (rng[:, 1] - rng[:, 0]).clamp_(min=0)
