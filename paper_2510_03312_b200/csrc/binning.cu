@@ -444,50 +444,70 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     }
 }
 
-// (4) per-tile lists: one CTA per tile scans its bucket in rounds of 256
-// entries (one per thread) with a block-ordered compaction of the entries
-// whose [tx0, tx1] contains the tile, and stops once `cap` ids are written:
-// only the prefix of each list a tile can consume is materialised.
-constexpr int kListThreads = 256;
+// (4) per-tile lists: one CTA per (bucket, tile row), one warp per tile of
+// that row (kBand tiles).  Each round stages kListRound bucket entries in
+// shared memory once; every warp scans them in order, keeps the entries whose
+// clipped rect contains its tile (warp ballot compaction, so the list stays
+// in rank order) and stops once `cap` ids are written: only the prefix of
+// each list a tile can consume is materialised.  The round loop ends when
+// every warp is done or the bucket is exhausted.
+constexpr int kListThreads = kBand * 32;
+constexpr int kListRound = 1024;
 __global__ void __launch_bounds__(kListThreads)
 tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restrict__ bstart,
-                  const uint32_t *__restrict__ ranges, int TX, int NB, uint32_t cap, uint32_t *__restrict__ out,
-                  const unsigned long long *__restrict__ n_pairs, int64_t capacity) {
-    __shared__ uint32_t wcount[kListThreads / 32];
+                  const uint32_t *__restrict__ ranges, int TX, int TY, int NB, uint32_t cap,
+                  uint32_t *__restrict__ out, const unsigned long long *__restrict__ n_pairs, int64_t capacity) {
+    __shared__ uint64_t sbuf[kListRound];
     if (pairs_overflow(n_pairs, capacity, nullptr)) return;
-    const int tile = blockIdx.x;
-    const int ty = tile / TX, tx = tile - ty * TX;
-    const int k = (ty / kRows) * NB + tx / kBand;
-    const int lx = tx % kBand, ly = ty % kRows;
+    const int k = blockIdx.x / kRows, ly = blockIdx.x % kRows;
+    const int grp = k / NB, band = k - grp * NB;
+    const int lane = threadIdx.x & 31, lx = threadIdx.x >> 5;
+    const int tx = band * kBand + lx, ty = grp * kRows + ly;
+    uint32_t t0 = 0, want = 0;
+    if (tx < TX && ty < TY) {
+        const int tile = ty * TX + tx;
+        t0 = ranges[2 * tile];
+        want = min(cap, ranges[2 * tile + 1] - t0);
+    }
     const uint32_t e0 = bstart[k], e1 = bstart[k + 1];
-    const uint32_t t0 = ranges[2 * tile], t1 = ranges[2 * tile + 1];
-    const uint32_t want = min(cap, t1 - t0);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     uint32_t written = 0;
-    for (uint32_t base = e0; base < e1 && written < want; base += kListThreads) {
-        const uint32_t i = base + threadIdx.x;
-        bool p = false;
-        uint32_t id = 0;
-        if (i < e1) {
-            const uint64_t e = entries[i];
-            const int c = (int)(e >> 32);
-            p = (c & 15) <= lx && lx <= ((c >> 4) & 15) && ((c >> 8) & 15) <= ly && ly <= ((c >> 12) & 15);
-            id = (uint32_t)e;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, p);
-        if (lane == 0) wcount[wid] = __popc(m);
-        __syncthreads();
-        uint32_t before = 0, tot = 0;
+    for (uint32_t base = e0; base < e1; base += kListRound) {
+        if (__syncthreads_count(written < want) == 0) break;
 #pragma unroll
-        for (int j = 0; j < kListThreads / 32; ++j) {
-            const uint32_t c = wcount[j];
-            before += (j < wid) ? c : 0u;
-            tot += c;
+        for (int r = 0; r < kListRound / kListThreads; ++r) {
+            const uint32_t i = base + r * kListThreads + threadIdx.x;
+            if (i < e1) sbuf[r * kListThreads + threadIdx.x] = entries[i];
         }
-        const uint32_t pos = written + before + __popc(m & ((1u << lane) - 1u));
-        if (p && pos < want) out[t0 + pos] = id;
-        written += tot;
         __syncthreads();
+        const int m = (int)min((uint32_t)kListRound, e1 - base);
+        // 4 x 32 entries per step: independent loads / tests / ballots, then
+        // the ordered appends
+        for (int j0 = 0; j0 < m && written < want; j0 += 128) {
+            bool p[4];
+            uint32_t id[4];
+            unsigned bal[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + 32 * u + lane;
+                p[u] = false;
+                id[u] = 0;
+                if (j < m) {
+                    const uint64_t e = sbuf[j];
+                    const int c = (int)(e >> 32);
+                    p[u] = (c & 15) <= lx && lx <= ((c >> 4) & 15) && ((c >> 8) & 15) <= ly &&
+                           ly <= ((c >> 12) & 15);
+                    id[u] = (uint32_t)e;
+                }
+                bal[u] = __ballot_sync(0xffffffffu, p[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t pos = written + __popc(bal[u] & lt);
+                if (p[u] && pos < want) out[t0 + pos] = id[u];
+                written += __popc(bal[u]);
+            }
+        }
     }
 }
 
@@ -582,9 +602,9 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count,
                                                                  pb->n_visible, G, NB, nbk, off, bb->entries,
                                                                  pb->n_pairs, bb->pair_capacity, bb->status);
-    tile_lists_kernel<<<n_tiles, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, NB,
-                                                       bb->list_cap ? bb->list_cap : 0xFFFFFFFFu, bb->tile_ids,
-                                                       pb->n_pairs, bb->pair_capacity);
+    tile_lists_kernel<<<nbk * kRows, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, TY, NB,
+                                                   bb->list_cap ? bb->list_cap : 0xFFFFFFFFu, bb->tile_ids,
+                                                   pb->n_pairs, bb->pair_capacity);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
