@@ -158,6 +158,21 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 // edge), the image tolerance itself is asserted by the parity tests.
 constexpr float kImgErrTol = 1.0e-3f;
 
+// 16 B shared-memory load at a 32-bit shared address (keeps the splat walk
+// in 32-bit shared offsets instead of generic 64-bit pointers)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
+// position of the most significant set bit (x != 0)
+__device__ __forceinline__ uint32_t msb_pos(uint32_t x) {
+    uint32_t p;
+    asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(x));
+    return p;
+}
+
 __device__ __forceinline__ float lg2_approx(float x) {
     float y;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -260,8 +275,9 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     float err = 0.f;  // bound on |T32 - T64| / T
     uint32_t cnt = inside ? end - start : 0u;
     int flag = 0;
+    float edge = 1.0f;  // min over out-of-support visits of m - (tau + E): < 0 flags the pixel
     bool done = !inside;
-    const float4 *rbase = reinterpret_cast<const float4 *>(srec);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
     for (uint32_t b = start; b < end; b += kTileThreads) {
         if (__syncthreads_count(done) == kTileThreads) break;
         const uint32_t q = b + threadIdx.x;
@@ -281,29 +297,30 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
-            if (lane == 0) swm[w][warp] = __brev(word);  // splat order from the MSB down
+            if (lane == 0) swm[w][warp] = __brev(word);  // splat order from the highest bit down
         }
         __syncthreads();
         if (!done) {
             const int nw = (int)((min((uint32_t)kTileThreads, end - b) + 31u) >> 5);
             for (int k = 0; k < nw && !done; ++k) {
                 uint32_t bits = swm[warp][k];
-                const float4 *rk = rbase + 128 * k;
+                // bit p of the reversed word is splat 32 k + 31 - p, at stop - 64 p
+                const uint32_t stop = sbase + (uint32_t)(32 * k + 31) * (uint32_t)sizeof(Rec32);
                 while (bits) {
-                    const int o = __clz(bits);
-                    bits ^= 0x80000000u >> o;
-                    const float4 *rp = rk + 4 * o;
-                    const float4 r0 = rp[0], r1 = rp[1];
+                    const uint32_t p = msb_pos(bits);
+                    bits ^= 1u << p;
+                    const uint32_t ra = stop - (p << 6);
+                    const float4 r0 = lds128(ra), r1 = lds128(ra + 16);
                     const float dx = (pxf - r0.x) + r0.z;
                     const float dy = (pyf - r0.y) + r0.w;
                     const float y0 = fmaf(r1.x, dx, r1.y * dy);
                     const float y1 = r1.z * dy;
                     const float m = fmaf(y0, y0, y1 * y1);
                     if (m >= tau) {
-                        flag |= (m < r1.w);  // support edge within the m-error band
+                        edge = fminf(edge, m - r1.w);  // support edge within the m-error band
                         continue;
                     }
-                    const float4 r2 = rp[2], r3 = rp[3];
+                    const float4 r2 = lds128(ra + 32), r3 = lds128(ra + 48);
                     const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                     float a = ex2_approx(arg);
                     // q = num / d; the T-error term a q / (1 - a) takes one reciprocal
@@ -313,7 +330,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     if (a > clamp_lo) {
                         const float qrel = num * rcp_approx(d);
                         if (a > clamp) {
-                            if (a * (1.0f - qrel) > clamp) hit[sid[(k << 5) + (int)((rp - rk) >> 2)]] = 1;
+                            if (a * (1.0f - qrel) > clamp) hit[sid[32 * k + 31 - (int)p]] = 1;
                             else flag = 1;
                             a = clamp;
                             om = one_minus_clamp;
@@ -333,7 +350,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                             // the reference stops before the next splat
                             flag |= (T > tmin * (1.0f - band));
                             done = true;
-                            cnt = b - start + (uint32_t)((k << 5) + (int)((rp - rk) >> 2)) + 1u;
+                            cnt = b - start + (uint32_t)(32 * k + 31) - p + 1u;
                             break;
                         }
                         flag |= (T < tmin * (1.0f + band));
@@ -343,7 +360,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         }
     }
     if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
-    if (err > kImgErrTol) flag = 1;
+    if (err > kImgErrTol || edge < 0.0f) flag = 1;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
