@@ -387,11 +387,12 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 //  1. lanes evaluate alpha_k (reference formula and rounding, clamp applied)
 //     and 1 - alpha_k in parallel;
 //  2. lane 0 runs the only truly sequential part, T_{k+1} = T_k (1 - alpha_k),
-//     exactly as tile_forward rounds it, finds the early-out index and
-//     publishes T_k through shared memory;
-//  3. lanes accumulate w_k = alpha_k T_k times colour with a warp reduction
-//     (summation order differs from the reference only at the 1e-16 level;
-//     T, the contributor count and the clamp flags are exact).
+//     exactly as tile_forward rounds it, straight through the chunk (T is
+//     non-increasing, so the early-out index is a ballot count of T_k >= t_min)
+//     and publishes T_k through shared memory;
+//  3. lanes accumulate w_k = alpha_k T_k times colour in per-lane sums, reduced
+//     once per pixel (summation order differs from the reference only at the
+//     1e-16 level; T, the contributor count and the clamp flags are exact).
 __global__ void __launch_bounds__(256)
 raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec64 *__restrict__ recs, const uint32_t *__restrict__ fix_list,
@@ -399,7 +400,6 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits) {
     __shared__ double s_om[8][32], s_T[8][33];
-    __shared__ int s_stop[8];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const uint32_t nfix = *fix_count;
@@ -414,6 +414,7 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         tile_span(P, ranges, tile, start, end, capped);
         const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
         double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
+        double l0 = 0.0, l1 = 0.0, l2 = 0.0, lw = 0.0;
         int cnt = 0;
         bool done = false;
         uint32_t q = start + lane;
@@ -439,38 +440,44 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             __syncwarp();
             const int nb = (int)min(32u, end - b);
             if (lane == 0) {
+                // T_k = T_{k-1} (1 - a_{k-1}) for the whole chunk, unconditionally:
+                // T is non-increasing, so the reference's stop (first T_k < t_min)
+                // is the count of T_k >= t_min; lanes past the list have 1 - 0 == 1
                 double t = T;
-                int k = 0;
-                for (; k < nb; ++k) {
-                    if (t < tmin) break;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
                     s_T[wl][k] = t;
-                    t = mul(t, s_om[wl][k]);  // 1 - 0 == 1 exactly: a no-op splat leaves t unchanged
+                    t = mul(t, s_om[wl][k]);
                 }
                 s_T[wl][32] = t;
-                s_stop[wl] = k;
             }
             __syncwarp();
-            const int stop = s_stop[wl];
+            const double Tk = s_T[wl][lane];
+            const int stop = __popc(__ballot_sync(0xffffffffu, lane < nb && Tk >= tmin));
             cnt += stop;
             done = stop < nb;
-            double w = 0.0;
             if (lane < stop && a != 0.0) {
-                w = mul(a, s_T[wl][lane]);
+                const double w = mul(a, Tk);
+                l0 += w * cr;
+                l1 += w * cg;
+                l2 += w * cb;
+                lw += w;
                 if (clamped) hit[my_id] = 1;
             }
-            double v0 = w * cr, v1 = w * cg, v2 = w * cb, v3 = w;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-                v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-                v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-                v3 += __shfl_xor_sync(0xffffffffu, v3, o);
-            }
-            a0 += v0; a1 += v1; a2 += v2; ws += v3;
-            T = s_T[wl][32];
+            T = s_T[wl][stop];
             if (!done && T < tmin) done = true;  // crossed on the chunk's last splat
             __syncwarp();
         }
+        // per-lane partial sums, reduced once (summation order differs from the
+        // reference's sequential sum only at the 1e-16 level)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+            l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+            lw += __shfl_xor_sync(0xffffffffu, lw, o);
+        }
+        a0 = l0; a1 = l1; a2 = l2; ws = lw;
         if (lane == 0 && capped && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
         if (lane == 0) {
             image[3 * (int64_t)pix] = (float)add(a0, mul(T, P.bg[0]));
