@@ -69,7 +69,7 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
         if constexpr (kStatic) {
             double mu_q[PrimGeom<C>::CC];
             load_statics<C, PT>(v.statics, i, g, mu_x, mu_q);
-            prim_view<C>(g, mu_x, mu_q, v);
+            prim_view<C>(g, mu_x, mu_q, v, pb.debug != nullptr);
         } else {
             prim_geom<C, PT>(stage + t * P, v, g, mu_x);
         }

@@ -339,9 +339,14 @@ __device__ inline void prim_static(const PT *rec, const UbsSettings &set, PrimGe
 
 // Per-view half of slice_scene (conditional mean slicing.py:205-208, opacity
 // gate :224-228) and project_scene (raster.py:99-131) on top of prim_static.
+// exact_s: always evaluate s_tanh (the debug dump and the backward read it);
+// otherwise an asymmetric-gate dimension with 0.5 dr <= 0 skips tanh and
+// log1p: there s = tanh(0.5 dr) <= 0, d = max(s, 0) = 0 and 4 beta log1p(-0)
+// adds a signed zero, so lsum and the gate are bit-identical (s_tanh is then
+// only known to be <= 0, all the flags use).
 template <int C>
 __device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const double (&mu_q)[PrimGeom<C>::CC],
-                                 const UbsView &v) {
+                                 const UbsView &v, bool exact_s = true) {
     double mean3[3] = {mu_x[0], mu_x[1], mu_x[2]};
     g.gate = 1.0;
     if constexpr (C > 0) {
@@ -365,7 +370,13 @@ __device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const 
         for (int i = 0; i < C; ++i) {
             double dr = 0.0;
             for (int k = 0; k < C; ++k) dr += g.M[i][k] * g.delta[k];
-            double s = tanh(0.5 * dr);
+            const double h = 0.5 * dr;
+            if (!exact_s && !v.set.gate_symmetric && !(h > 0.0)) {
+                g.s_tanh[i] = h;  // <= 0 (or NaN, as tanh would give)
+                g.d_gate[i] = 0.0;
+                continue;
+            }
+            double s = tanh(h);
             g.s_tanh[i] = s;
             double d = v.set.gate_symmetric ? fabs(s) : fmax(s, 0.0);
             g.d_gate[i] = d;
