@@ -300,92 +300,71 @@ bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restric
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) h[k] = scnt[k];
 }
 
-// (2) offsets[c][k] = bucket_start[k] + sum_{c' < c} hist[c'][k], in three
-// well-parallel passes over S = kSegs segments of chunks:
-//   a) segsum[s][k]  = sum of hist over segment s            (grid: k x s)
-//   b) per bucket k: exclusive scan of segsum over s -> segbase, total[k];
-//      then one CTA scans total -> bucket_start               (grid: k; 1 CTA)
-//   c) offsets over each segment, read hist, write off        (grid: k x s)
-constexpr int kSegs = 128;
+// (2) one kernel, one CTA per bucket k: off[c][k] = sum_{c' < c} hist[c'][k]
+// (a block scan down the chunk column) and total[k]; the last CTA to finish
+// (atomic ticket, reset for the next frame) scans the totals into
+// bucket_start.  The scatter adds bucket_start[k] to its chunk offsets.
+constexpr int kOffThreads = 256;
 
-__global__ void __launch_bounds__(256)
-bucket_segsum_kernel(const uint32_t *__restrict__ hist, int nbk, int G, uint32_t *__restrict__ segsum) {
-    const int k = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int sg = blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (k >= nbk) return;
-    const int L = (G + kSegs - 1) / kSegs;
-    const int c0 = sg * L, c1 = min(G, c0 + L);
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    uint32_t before = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < kOffThreads / 32; ++w) {
+        const uint32_t t = warp_tot[w];
+        before += w < wid ? t : 0u;
+        total += t;
+    }
+    __syncthreads();
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(kOffThreads)
+bucket_offsets_kernel(const uint32_t *__restrict__ hist, int G, int nbk, uint32_t *__restrict__ off,
+                      uint32_t *__restrict__ total, uint32_t *__restrict__ bstart, uint32_t *__restrict__ ticket) {
+    __shared__ uint32_t warp_tot[kOffThreads / 32];
+    __shared__ bool last;
+    const int k = blockIdx.x;
+    const int L = (G + kOffThreads - 1) / kOffThreads;
+    const int c0 = min(G, (int)threadIdx.x * L), c1 = min(G, c0 + L);
     uint32_t sum = 0;
     for (int c = c0; c < c1; ++c) sum += hist[(int64_t)c * nbk + k];
-    segsum[(int64_t)sg * nbk + k] = sum;
-}
-
-__global__ void __launch_bounds__(256)
-bucket_segscan_kernel(const uint32_t *__restrict__ segsum, int nbk, uint32_t *__restrict__ segbase,
-                      uint32_t *__restrict__ total) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= nbk) return;
-    uint32_t v[kSegs];
-#pragma unroll
-    for (int j = 0; j < kSegs; ++j) v[j] = segsum[(int64_t)j * nbk + k];
-    uint32_t acc = 0;
-#pragma unroll
-    for (int j = 0; j < kSegs; ++j) {
-        segbase[(int64_t)j * nbk + k] = acc;
-        acc += v[j];
-    }
-    total[k] = acc;
-}
-
-// one CTA: bucket_start = exclusive scan of bucket totals (nbk + 1 entries)
-__global__ void __launch_bounds__(1024)
-bucket_start_kernel(const uint32_t *__restrict__ total, int nbk, uint32_t *__restrict__ bstart) {
-    __shared__ uint32_t warp_tot[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = 0; base < nbk; base += 1024) {
-        const int k = base + threadIdx.x;
-        const uint32_t c = k < nbk ? total[k] : 0u;
-        uint32_t x = c;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_tot[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = warp_tot[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            warp_tot[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - c;
-        if (k < nbk) bstart[k] = excl;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = excl + c;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) bstart[nbk] = carry;
-}
-
-__global__ void __launch_bounds__(256)
-bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restrict__ segbase,
-                      const uint32_t *__restrict__ bstart, int nbk, int G, uint32_t *__restrict__ off) {
-    const int k = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int sg = blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (k >= nbk) return;
-    const int L = (G + kSegs - 1) / kSegs;
-    const int c0 = sg * L, c1 = min(G, c0 + L);
-    uint32_t acc = bstart[k] + segbase[(int64_t)sg * nbk + k];
+    uint32_t col_total;
+    uint32_t run = block_excl_scan(sum, warp_tot, col_total);
     for (int c = c0; c < c1; ++c) {
         const uint32_t v = hist[(int64_t)c * nbk + k];
-        off[(int64_t)c * nbk + k] = acc;
-        acc += v;
+        off[(int64_t)c * nbk + k] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) {
+        total[k] = col_total;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (uint32_t)nbk - 1u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    uint32_t carry = 0;
+    for (int base = 0; base < nbk; base += kOffThreads) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nbk ? __ldcg(total + i) : 0u;
+        uint32_t chunk_total;
+        const uint32_t ex = block_excl_scan(v, warp_tot, chunk_total);
+        if (i < nbk) bstart[i] = carry + ex;
+        carry += chunk_total;
+    }
+    if (threadIdx.x == 0) {
+        bstart[nbk] = carry;
+        *ticket = 0u;
     }
 }
 
@@ -397,7 +376,8 @@ bucket_offsets_kernel(const uint32_t *__restrict__ hist, const uint32_t *__restr
 __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
                       const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
-                      int NB, int nbk, const uint32_t *__restrict__ off, uint64_t *__restrict__ entries,
+                      int NB, int nbk, const uint32_t *__restrict__ off, const uint32_t *__restrict__ bstart,
+                      uint64_t *__restrict__ entries,
                       const unsigned long long *__restrict__ n_pairs, int64_t capacity, uint32_t *status) {
     if (pairs_overflow(n_pairs, capacity, status)) return;
     extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
@@ -413,7 +393,7 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     __syncthreads();
     const uint32_t *o = off + (int64_t)blockIdx.x * nbk;
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) {
-        uint32_t run = o[k];
+        uint32_t run = bstart[k] + o[k];
 #pragma unroll
         for (int ww = 0; ww < kBinWarps; ++ww) {
             const uint32_t c = sfill_all[ww * nbk + k];
@@ -597,16 +577,14 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     bucket_hist_kernel<<<cta, kBinWarps * 32, sizeof(uint32_t) * nbk, s>>>(bb->order, pb->rect, pb->tile_count,
                                                                            pb->n_visible, G, NB, nbk,
                                                                            bb->chunk_hist);
-    // seg_scratch: segsum (kSegs x nbk) | segbase (kSegs x nbk) | total (nbk)
-    uint32_t *segsum = bb->seg_scratch, *segbase = segsum + (size_t)kSegs * nbk, *total = segbase + (size_t)kSegs * nbk;
+    // seg_scratch: bucket totals (nbk) | ticket (1)
+    uint32_t *total = bb->seg_scratch, *ticket = total + nbk;
     uint32_t *off = bb->chunk_hist + (size_t)G * nbk;  // second half of chunk_hist
-    const dim3 kg((unsigned)((nbk + 31) / 32), kSegs / 8);
-    bucket_segsum_kernel<<<kg, 256, 0, s>>>(bb->chunk_hist, nbk, G, segsum);
-    bucket_segscan_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(segsum, nbk, segbase, total);
-    bucket_start_kernel<<<1, 1024, 0, s>>>(total, nbk, bb->bucket_start);
-    bucket_offsets_kernel<<<kg, 256, 0, s>>>(bb->chunk_hist, segbase, bb->bucket_start, nbk, G, off);
+    if (cudaMemsetAsync(ticket, 0, sizeof(uint32_t), s) != cudaSuccess) return UBS_E_CUDA;
+    bucket_offsets_kernel<<<nbk, kOffThreads, 0, s>>>(bb->chunk_hist, G, nbk, off, total, bb->bucket_start, ticket);
     bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count,
-                                                                 pb->n_visible, G, NB, nbk, off, bb->entries,
+                                                                 pb->n_visible, G, NB, nbk, off, bb->bucket_start,
+                                                                 bb->entries,
                                                                  pb->n_pairs, bb->pair_capacity, bb->status);
     tile_lists_kernel<<<nbk * kRows, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, TY, NB,
                                                    bb->list_cap ? bb->list_cap : 0xFFFFFFFFu, bb->tile_ids,

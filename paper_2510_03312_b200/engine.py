@@ -300,8 +300,8 @@ class Workspace:
         self.chunk_count = g
         if self.chunk_hist is None or self.chunk_hist.numel() < 2 * g * nbk:
             self.chunk_hist = self._i(2 * g * nbk, torch.int32)
-        if self.seg_scratch is None or self.seg_scratch.numel() < 257 * nbk:
-            self.seg_scratch = self._i(257 * nbk, torch.int32)
+        if self.seg_scratch is None or self.seg_scratch.numel() < nbk + 1:
+            self.seg_scratch = self._i(nbk + 1, torch.int32)  # bucket totals | ticket
             self.bucket_start = self._i(nbk + 1, torch.int32)
 
     def ensure_pairs(self, k: int):
