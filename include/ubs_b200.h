@@ -129,19 +129,20 @@ typedef struct UbsPrimBuffers {
 
 /* Binning buffers. */
 typedef struct UbsBinBuffers {
-    uint64_t *keys_sorted; /* n x 8 B scratch: 32-bit sort keys in / out */
-    uint32_t *ids_iota;    /* n: scratch (0..n-1) */
+    uint64_t *keys_sorted; /* n x 8 B scratch: depth keys scattered into their sort buckets */
+    uint32_t *ids_iota;    /* n: scratch (ids scattered alongside) */
     uint32_t *order;       /* n: ids by (depth, id); first n_vis are visible */
     uint32_t *tile_ids;    /* pair_capacity: primitive ids grouped by tile, depth ordered */
     uint32_t *tile_ranges; /* 2 x n_tiles: [start, end) into tile_ids */
     int64_t pair_capacity;
-    void *temp;            /* CUB scratch */
+    void *temp;            /* ubs_bin_temp_bytes: depth-bucket histogram, starts, CUB scan scratch */
     size_t temp_bytes;
     uint32_t *chunk_hist;  /* 2 x chunk_count x n_buckets: per-chunk bucket counts, then offsets */
     int64_t chunk_hist_capacity; /* elements */
     int32_t chunk_count;   /* G rank chunks */
-    uint64_t *entries;     /* pair_capacity: bucket entries (id | tx0 << 32 | tx1 << 48) */
-    uint32_t *seg_scratch; /* (2 x 128 + 1) x n_buckets */
+    uint64_t *entries;     /* pair_capacity: bucket entries (id | covered-tile mask of the 8 x 4
+                              tile bucket << 32) */
+    uint32_t *seg_scratch; /* n_buckets + 1: bucket totals, completion ticket */
     uint32_t *bucket_start;/* n_buckets + 1 */
     int64_t bucket_capacity; /* elements of bucket_start */
     uint32_t *status;      /* [1] |= UBS_S_* (frame must be re-run with more capacity) */
@@ -195,15 +196,16 @@ int ubs_scene_statics(const UbsView *v, void *statics, ubs_stream_t s);
 /* slice + project + tile rects (fp64 arithmetic, one thread per primitive) */
 int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32, ubs_stream_t s);
 
-/* CUB scratch bytes needed for n primitives, pair capacity and tile count */
+/* scratch bytes (UbsBinBuffers.temp) needed for n primitives */
 size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
-/* depth order = lexsort((ids, depth)): stable radix sort of 32-bit keys
- * ((depth bits - min) >> shift) with ids in id order, then an exact repair of
- * the rare runs of equal 32-bit keys by (f64 depth bits, id); plus the per-tile
+/* depth order = lexsort((ids, depth)) (raster.py:274-275): bucket sort of the
+ * visible primitives on the top bits of (depth bits - min) >> shift, then an
+ * exact rank by (f64 depth bits, id) inside each bucket; plus the per-tile
  * [start, end) ranges from the rect-corner difference array */
 int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb, ubs_stream_t s);
-/* per-tile depth-ordered id lists (sort-free two-level stable bucketing);
- * n_buckets = TY * ceil(TX / 8).  n_pairs >= 0: K as read by the host
+/* per-tile depth-ordered id lists (sort-free two-level stable bucketing over
+ * buckets of 8 x 4 tiles); n_buckets = ceil(TY / 4) * ceil(TX / 8).
+ * n_pairs >= 0: K as read by the host
  * (checked against pair_capacity); n_pairs < 0: K stays on the device, every
  * kernel that touches the pair buffers checks it against pair_capacity and
  * sets UBS_S_PAIR_OVERFLOW instead of writing out of bounds (no host sync). */
