@@ -165,3 +165,73 @@ def render(scene, cam, query, settings=DEFAULT_SETTINGS, *, precision: str | Non
     ds = _device_scene(scene, ws)
     fr = engine.render_frame(ws, ds, cam, query, settings)
     return _host_image(fr, scene.background)
+
+
+# ---------------------------------------------------------------------------
+# render_decomposition (reference raster.py:355-422)
+# ---------------------------------------------------------------------------
+DECOMPOSITION_CHANNELS = ("b_x", "b_d", "b_t", "opacity")
+
+
+def channel_values(params: torch.Tensor, n_dims: int, channel: str) -> torch.Tensor:
+    """Per-primitive scalar of ``channel`` from the packed records, fp64 on the
+    records' device (raster.py:397-410, same error messages)."""
+    from .types import field_offsets
+    c = n_dims - 3
+    off = field_offsets(n_dims)
+    p = params.double()
+    if channel == "b_x":
+        return (p[:, off["b_x"][0]] + 5.0) / 10.0
+    if channel == "opacity":
+        return torch.sigmoid(p[:, off["opacity_raw"][0]])
+    if channel == "b_d":
+        if c < 3:
+            raise ValueError("b_d channel needs direction dimensions (6D or 7D scene)")
+        o = off["b_q"][0]
+        bq = p[:, o + c - 3:o + c]
+        return ((((bq[:, 0] + bq[:, 1]) + bq[:, 2]) / 3.0) + 5.0) / 10.0  # numpy's mean of 3, in order
+    if channel == "b_t":
+        if n_dims != 7:
+            raise ValueError("b_t channel is only available for 7D scenes")
+        return (p[:, off["b_q"][0]] + 5.0) / 10.0
+    raise ValueError(f"unknown channel {channel!r}; expected one of {DECOMPOSITION_CHANNELS}")
+
+
+def diverging_colormap(t: torch.Tensor) -> torch.Tensor:
+    """Blue -> white -> red over t in [0, 1] (raster.py:413-422)."""
+    t = t.double().clamp(0.0, 1.0)
+    lo = t.new_tensor([0.15, 0.25, 0.85])
+    mid = t.new_tensor([0.95, 0.95, 0.95])
+    hi = t.new_tensor([0.85, 0.20, 0.15])
+    u = (t * 2.0).clamp(0.0, 1.0)[:, None]
+    v = (t * 2.0 - 1.0).clamp(0.0, 1.0)[:, None]
+    return torch.where(t[:, None] < 0.5, lo + u * (mid - lo), mid + v * (hi - mid))
+
+
+def render_decomposition(scene, cam, query, channel: str, settings=DEFAULT_SETTINGS, *,
+                         device=None) -> np.ndarray:
+    """Heat map of a per-primitive scalar composited with the render's own
+    weights (raster.py:358-394): the colours become the diverging colormap of
+    the scalar, the background zero, and each pixel is divided by its
+    accumulated alpha (background where nothing was composited).
+
+    Runs the device path on records whose colour fields hold the colormap, in
+    the fp64 raster: the division by the alpha sum amplifies the fp32 raster's
+    absolute errors wherever coverage is low (measured: up to 0.9 at 1.7% of
+    the fixture pixels), so there is no fp32 variant."""
+    from .types import field_offsets
+    precision = "fp64"
+    c = scene.n_dims - 3
+    if np.asarray(query.dims).reshape(-1).shape[0] != c:
+        raise ValueError(f"query has {np.asarray(query.dims).size} dims, scene expects {c}")
+    ws = workspace(precision, device)
+    ds = _device_scene(scene, ws)
+    colors = diverging_colormap(channel_values(ds.params, scene.n_dims, channel))
+    params = ds.params.clone()
+    o = field_offsets(scene.n_dims)["color"][0]
+    params[:, o:o + 3] = colors.to(params.dtype)
+    fr = engine.render_frame(ws, engine.DeviceScene(params, scene.n_dims, (0.0, 0.0, 0.0)), cam, query, settings)
+    num, den = fr.image.double(), fr.alpha_sum.double()
+    bg = torch.as_tensor(np.asarray(scene.background, dtype=np.float64), device=num.device)
+    out = torch.where(den[..., None] > 0.0, num / den.clamp_min(1e-300)[..., None], bg)
+    return out.cpu().numpy()

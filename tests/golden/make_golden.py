@@ -3,7 +3,7 @@
 Run in the build container, which has /root/reference (it does not exist on
 the GPU box; the fixtures travel as committed .npz files):
 
-    NUMBA_CACHE_DIR=/tmp/ubs_numba python tests/golden/make_golden.py
+    NUMBA_CACHE_DIR=/tmp/ubs_numba python tests/golden/make_golden.py [--decomposition]
 
 Each case records the reference's own outputs (betasplat.raster.render_with_cache
 and betasplat.gradients.backward) on seeded fixture scenes, plus checksums of
@@ -157,5 +157,23 @@ def main():
     backward_case("grads_7_branches", br, [(cam, q, tgt)], G.LossConfig(lambda_ssim=0.5, loss_scale=2.0))
 
 
+def decomposition_cases():
+    """render_decomposition (raster.py:358-423) for every channel a scene supports."""
+    st = bs.RenderSettings()
+    for nd, chans in ((6, ("b_x", "b_d", "opacity")), (7, ("b_x", "b_d", "b_t", "opacity"))):
+        sc = f32(T.random_scene(nd, 80, seed=nd + 70))
+        cam, q = T.random_camera(48, nd + 71), T.random_query(nd, nd + 72)
+        intr, w2c = cam_arrays(cam)
+        out = {c: R.render_decomposition(sc, cam, q, c, st) for c in chans}
+        np.savez_compressed(OUT / f"decomp_{nd}.npz", in_records=records(sc), in_n_dims=nd,
+                            in_background=sc.background, in_intr=intr, in_w2c=w2c, in_query=q.dims,
+                            channels=np.array(chans), **{f"out_{c}": v for c, v in out.items()})
+        print("decomp", nd, chans)
+
+
 if __name__ == "__main__":
-    main()
+    if "--decomposition" in sys.argv:
+        decomposition_cases()
+    else:
+        main()
+        decomposition_cases()

@@ -133,3 +133,40 @@ def test_gpu_backward_matches_reference(name, precision):
     ref = {k: d[f"g_{k}"] for k in O.FIELDS}
     bad = grad_close(g.arrays(), ref, rel=1e-6 if precision == "fp64" else 1e-3)
     assert not bad, bad
+
+
+# --- render_decomposition (raster.py:358-423), fixtures from the reference ----
+DECOMP = ("decomp_6", "decomp_7")
+
+
+def _decomp_inputs(name):
+    d = np.load(GOLD / f"{name}.npz")
+    return d, _scene(d), _camera(d["in_intr"], d["in_w2c"]), Query(d["in_query"])
+
+
+@pytest.mark.parametrize("name", DECOMP)
+def test_oracle_decomposition_matches_reference(name):
+    d, sc, cam, q = _decomp_inputs(name)
+    for ch in d["channels"]:
+        got = O.render_decomposition(sc, cam, q, str(ch), RenderSettings())
+        np.testing.assert_allclose(got, d[f"out_{ch}"], rtol=0, atol=1e-12, err_msg=str(ch))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", DECOMP)
+def test_gpu_decomposition_matches_reference(name):
+    from paper_2510_03312_b200 import raster
+    d, sc, cam, q = _decomp_inputs(name)
+    for ch in d["channels"]:
+        got = raster.render_decomposition(sc, cam, q, str(ch), RenderSettings())
+        np.testing.assert_allclose(got, d[f"out_{ch}"], rtol=0, atol=1e-12, err_msg=str(ch))
+
+
+@pytest.mark.gpu
+def test_gpu_decomposition_channel_errors():
+    from paper_2510_03312_b200 import raster
+    d, sc, cam, q = _decomp_inputs("decomp_6")
+    with pytest.raises(ValueError, match="only available for 7D"):
+        raster.render_decomposition(sc, cam, q, "b_t")
+    with pytest.raises(ValueError, match="unknown channel"):
+        raster.render_decomposition(sc, cam, q, "beta")
