@@ -16,14 +16,21 @@ __version__ = "0.1.0"
 __all__ = ["DEFAULT_SETTINGS", "PARAM_FIELDS", "Camera", "DegeneratePrimitiveError", "GradientError",
            "LossConfig", "Query", "RenderSettings", "Scene", "SceneGrads", "logit", "pack_records",
            "quantize_f32", "record_width", "sigmoid", "render", "render_with_cache", "backward",
-           "FrameCache"]
+           "FrameCache", "render_decomposition", "load_scene", "save_scene", "load_scene_device",
+           "SceneFormatError", "clone_opacity", "relocate", "noise_inject"]
 
 
 def __getattr__(name):
     # the GPU entry points import torch lazily so the types stay importable anywhere
-    if name in ("render", "render_with_cache", "FrameCache"):
+    if name in ("render", "render_with_cache", "FrameCache", "render_decomposition"):
         from . import raster
         return getattr(raster, name)
+    if name in ("load_scene", "save_scene", "load_scene_device", "SceneFormatError"):
+        from . import sceneio
+        return getattr(sceneio, name)
+    if name in ("clone_opacity", "relocate", "noise_inject"):
+        from . import optim
+        return getattr(optim, name)
     if name == "backward":
         from .gradients import backward
         return backward

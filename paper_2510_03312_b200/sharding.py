@@ -153,6 +153,21 @@ class DeviceAdam:
         # DeviceScene's statics cache sees new parameters
         torch.autograd.graph.increment_version(self.params)
 
+    def reset_rows(self, idx: torch.Tensor):
+        """Zero the moments of rewritten rows (AdamState.reset_rows, optim.py:100-103)."""
+        self.m[idx] = 0.0
+        self.v[idx] = 0.0
+
+    def rebind(self, params: torch.Tensor):
+        """Follow a grown parameter buffer; new rows start with zero moments
+        (AdamState.grow, optim.py:105-112)."""
+        extra = params.shape[0] - self.m.shape[0]
+        if extra > 0:
+            z = torch.zeros((extra, self.m.shape[1]), dtype=self.m.dtype, device=self.m.device)
+            self.m = torch.cat([self.m, z])
+            self.v = torch.cat([self.v, z.clone()])
+        self.params = params
+
 
 def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=DEFAULT_SETTINGS, group=None,
                  sink: engine.HostFrameSink | None = None):
