@@ -667,6 +667,149 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
     }
 }
 
+// fp32 backward (tile_backward, _tiles.py:59-127): the forward's 8x4-pixel
+// warps walk, from the end of the list towards its front, only the splats
+// whose cover mask has their bit (a culled splat has alpha == 0 at every
+// pixel of the warp, so it contributes nothing), with the forward's exact
+// alpha expression (the same bits, so T_i = T_{i+1} / (1 - alpha_i) unwinds
+// the forward's chain) and MUFU reciprocals / lg2 in the derivatives:
+//   d alpha / d og = alpha / og,  d alpha / d beta = alpha ln(1 - x),
+//   d alpha / d m = -alpha beta / (tau (1 - x)),  x = m / tau.
+// The 10 per-splat sums are warp reduce-scattered and added with atomics.
+__global__ void __launch_bounds__(kTileThreads)
+raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                    const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
+                    const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
+                    float *__restrict__ grad2d) {
+    constexpr int kWarps = kTileThreads / 32;
+    __shared__ Rec32 srec[kTileThreads];
+    __shared__ uint32_t sid[kTileThreads];
+    __shared__ uint32_t swm[kWarps][kWarps];  // [walking warp][loading warp] ballot words
+    __shared__ int smax;
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const float pxf = (float)px, pyf = (float)py;
+    const bool inside = px < P.W && py < P.H;
+    const uint32_t start = ranges[2 * tile];
+    const int64_t pix = (int64_t)py * P.W + px;
+    int my_cnt = 0;
+    float T = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    if (threadIdx.x == 0) smax = 0;
+    __syncthreads();
+    if (inside) {
+        my_cnt = ncontrib[pix];
+        T = tstop[pix];
+        g0 = g_image[3 * pix];
+        g1 = g_image[3 * pix + 1];
+        g2 = g_image[3 * pix + 2];
+        atomicMax(&smax, my_cnt);
+    }
+    __syncthreads();
+    const int max_cnt = smax;
+    int warp_cnt = my_cnt;  // this warp's largest contributor count: splats beyond it are skipped
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) warp_cnt = max(warp_cnt, __shfl_xor_sync(0xffffffffu, warp_cnt, o));
+    const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
+    const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    const float kLn2 = 0.6931471805599453f;
+    float suffix = (g0 * (float)P.bg[0] + g1 * (float)P.bg[1] + g2 * (float)P.bg[2]) * T;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
+    // batches aligned from the list front, walked back to front
+    for (int lo = ((max_cnt - 1) / kTileThreads) * kTileThreads; lo >= 0 && max_cnt > 0; lo -= kTileThreads) {
+        __syncthreads();
+        const int q = lo + (int)threadIdx.x;
+        uint32_t cover = 0;
+        if (q < max_cnt) {
+            const uint32_t id = ids[start + q];
+            const float4 *r = reinterpret_cast<const float4 *>(recs + id);
+            float4 *d = reinterpret_cast<float4 *>(srec + threadIdx.x);
+            sid[threadIdx.x] = id;
+            const float4 r0 = __ldg(r), r1 = __ldg(r + 1);
+            d[0] = r0;
+            d[1] = r1;
+            d[2] = __ldg(r + 2);
+            d[3] = __ldg(r + 3);
+            cover = warp_cover_mask(r0, r1, tx, ty);
+        }
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
+            if (lane == 0) swm[w][warp] = word;
+        }
+        __syncthreads();
+        const int top = min(kTileThreads, warp_cnt - lo);  // splats [lo, lo + top) concern this warp
+        for (int k = (top - 1) >> 5; k >= 0; --k) {
+            uint32_t bits = swm[warp][k];
+            const int lim = top - 32 * k;  // keep bits < lim
+            if (lim < 32) bits &= (1u << lim) - 1u;
+            while (bits) {
+                const uint32_t b = msb_pos(bits);
+                bits ^= 1u << b;
+                const int jj = 32 * k + (int)b;  // index inside the batch
+                const uint32_t ra = sbase + (uint32_t)jj * (uint32_t)sizeof(Rec32);
+                float v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+                bool contrib = false;
+                if (lo + jj < my_cnt) {
+                    const float4 r0 = lds128(ra), r1 = lds128(ra + 16);
+                    const float dx = (pxf - r0.x) + r0.z;
+                    const float dy = (pyf - r0.y) + r0.w;
+                    const float y0 = fmaf(r1.x, dx, r1.y * dy);
+                    const float y1 = r1.z * dy;
+                    const float m = fmaf(y0, y0, y1 * y1);
+                    if (m < tau) {
+                        const float4 r2 = lds128(ra + 32), r3 = lds128(ra + 48);
+                        const float omx = fmaf(-m, inv_tau, 1.0f);  // 1 - x
+                        const float L = lg2_approx(omx);
+                        float a = ex2_approx(fmaf(r2.x, L, r3.w));  // the forward's alpha
+                        if (a != 0.0f) {
+                            contrib = true;
+                            const bool clamped = a > clamp;
+                            float om = 1.0f - a;
+                            if (clamped) {
+                                a = clamp;
+                                om = one_minus_clamp;
+                            }
+                            const float iom = rcp_approx(om);
+                            const float ti = T * iom;
+                            const float w = a * ti;
+                            v[7] = w * g0;
+                            v[8] = w * g1;
+                            v[9] = w * g2;
+                            const float gc = fmaf(g0, r2.y, fmaf(g1, r2.z, g2 * r2.w));
+                            const float ga = fmaf(gc, ti, -suffix * iom);
+                            suffix = fmaf(gc, w, suffix);
+                            T = ti;
+                            if (!clamped) {
+                                const float gaa = ga * a;
+                                v[5] = gaa * rcp_approx(r3.y);
+                                v[6] = gaa * (L * kLn2);
+                                const float gm = -gaa * r2.x * rcp_approx(omx) * inv_tau;
+                                const float pd0 = r1.x * y0;               // P d = U^T (U d)
+                                const float pd1 = fmaf(r1.y, y0, r1.z * y1);
+                                v[0] = -2.0f * gm * pd0;
+                                v[1] = -2.0f * gm * pd1;
+                                v[2] = gm * dx * dx;
+                                v[3] = gm * dx * dy;  // both off-diagonals of pg_p2 get this (_tiles.py:125-126)
+                                v[4] = gm * dy * dy;
+                            }
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    int idx;
+                    const float mine = warp_reduce_scatter16(v, lane, idx);
+                    if ((lane & 1) == 0 && idx < 10 && mine != 0.0f)
+                        atomicAdd(grad2d + (int64_t)sid[jj] * kGrad2dStride + idx, mine);
+                }
+            }
+        }
+    }
+}
+
 }  // namespace ubs
 
 using namespace ubs;
@@ -720,7 +863,7 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
             P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
             (const double *)gb->g_image, (double *)gb->grad2d);
     } else {
-        raster_bwd_kernel<float><<<n_tiles, kTileThreads, 0, s>>>(
+        raster_bwd32_kernel<<<n_tiles, kTileThreads, 0, s>>>(
             P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
             (const float *)gb->g_image, (float *)gb->grad2d);
     }
