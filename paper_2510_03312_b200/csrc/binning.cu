@@ -155,6 +155,99 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
     }
 }
 
+// Large frames (grid beyond one CTA's shared memory): the same three steps in
+// global memory -- row prefix (a warp per row), column prefix (a thread per
+// column), then a three-phase exclusive scan of the per-tile counts.
+__global__ void grid_row_prefix_kernel(int32_t *__restrict__ g, int gw, int rows) {
+    const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    int32_t carry = 0;
+    for (int c0 = 0; c0 < gw; c0 += 32) {
+        const int c = c0 + lane;
+        int32_t x = c < gw ? g[(int64_t)r * gw + c] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (c < gw) g[(int64_t)r * gw + c] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+__global__ void grid_col_prefix_kernel(int32_t *__restrict__ g, int gw, int rows) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= gw) return;
+    int32_t acc = 0;
+    for (int r = 0; r < rows; ++r) acc = (g[(int64_t)r * gw + c] += acc);
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan1024(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    total = warp_tot[31];
+    const uint32_t ex = (wid ? warp_tot[wid - 1] : 0u) + x - v;
+    __syncthreads();
+    return ex;
+}
+
+__device__ __forceinline__ uint32_t tile_count_at(const int32_t *g, int TX, int t) {
+    return (uint32_t)g[(int64_t)(t / TX) * (TX + 1) + (t % TX)];
+}
+
+__global__ void __launch_bounds__(1024) tile_block_sums_kernel(const int32_t *__restrict__ g, int TX, int n_tiles,
+                                                               uint32_t *__restrict__ bsum) {
+    __shared__ uint32_t warp_tot[32];
+    const int t = blockIdx.x * 1024 + threadIdx.x;
+    uint32_t total;
+    block_excl_scan1024(t < n_tiles ? tile_count_at(g, TX, t) : 0u, warp_tot, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) tile_block_scan_kernel(uint32_t *__restrict__ bsum, int nb) {
+    __shared__ uint32_t warp_tot[32];
+    uint32_t carry = 0;
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nb ? bsum[i] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_excl_scan1024(v, warp_tot, total);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(1024) tile_ranges_kernel(const int32_t *__restrict__ g, int TX, int n_tiles,
+                                                           const uint32_t *__restrict__ bsum,
+                                                           uint32_t *__restrict__ ranges) {
+    __shared__ uint32_t warp_tot[32];
+    const int t = blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t c = t < n_tiles ? tile_count_at(g, TX, t) : 0u;
+    uint32_t total;
+    const uint32_t ex = bsum[blockIdx.x] + block_excl_scan1024(c, warp_tot, total);
+    if (t < n_tiles) {
+        ranges[2 * t] = ex;
+        ranges[2 * t + 1] = ex + c;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Sort-free stable binning.
 //
@@ -511,9 +604,10 @@ static size_t depth_scan_bytes(int64_t n) {
 
 extern "C" size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles) {
     (void)pair_capacity;
-    (void)n_tiles;
     const size_t B = (size_t)1 << sort_log_buckets(n);
-    return 2 * ((B + 1) * sizeof(uint32_t) + 256) + depth_scan_bytes(n) + 256;
+    const size_t depth = 2 * ((B + 1) * sizeof(uint32_t) + 256) + depth_scan_bytes(n) + 256;
+    const size_t tiles = sizeof(uint32_t) * (size_t)((n_tiles > 0 ? n_tiles : 0) / 1024 + 1);  // large-frame tile scan
+    return depth > tiles ? depth : tiles;
 }
 
 extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
@@ -524,9 +618,20 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
     cudaStream_t s = (cudaStream_t)stream;
     const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
     const size_t gbytes = sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1);
-    if (gbytes > 200 * 1024) return UBS_E_ARGS;  // > ~50k tiles (about 3.5k x 3.5k px) is not supported
-    cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbytes);
-    tile_scan_kernel<<<1, kScanThreads, gbytes, s>>>(pb->tile_grid, TX, TY, bb->tile_ranges);
+    if (gbytes <= 200 * 1024) {  // up to ~50k tiles: one CTA in shared memory
+        cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbytes);
+        tile_scan_kernel<<<1, kScanThreads, gbytes, s>>>(pb->tile_grid, TX, TY, bb->tile_ranges);
+    } else {  // in place in global memory; block sums in the (not yet used) depth-sort scratch
+        const int n_tiles = TX * TY, nb = (n_tiles + 1023) / 1024;
+        if (bb->temp_bytes < sizeof(uint32_t) * (size_t)nb) return UBS_E_CAPACITY;
+        uint32_t *bsum = reinterpret_cast<uint32_t *>(bb->temp);
+        int32_t *g = pb->tile_grid;
+        grid_row_prefix_kernel<<<(TY + 1 + 7) / 8, 256, 0, s>>>(g, TX + 1, TY + 1);
+        grid_col_prefix_kernel<<<(TX + 1 + 255) / 256, 256, 0, s>>>(g, TX + 1, TY + 1);
+        tile_block_sums_kernel<<<nb, 1024, 0, s>>>(g, TX, n_tiles, bsum);
+        tile_block_scan_kernel<<<1, 1024, 0, s>>>(bsum, nb);
+        tile_ranges_kernel<<<nb, 1024, 0, s>>>(g, TX, n_tiles, bsum, bb->tile_ranges);
+    }
     if (n == 0) {
         UBS_CUDA_CHECK();
         return UBS_OK;

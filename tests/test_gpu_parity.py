@@ -297,3 +297,12 @@ def test_capped_tile_lists_match_full():
     engine.render_frame(ws, ds, cam, q, sync=False)
     with pytest.raises(Exception):
         engine.check_status(ws)
+
+
+def test_large_frame_uses_global_tile_scan():
+    # 4000 x 3600 px = 250 x 225 tiles: the tile-corner grid no longer fits one
+    # CTA's shared memory, so the global-memory tile scan runs; lists, order,
+    # counts and image must still match the oracle
+    sc = quantize_f32(S.synth(3, 3000, seed=41))
+    cam = S.bench_camera(4000, 3600)
+    assert_frame_parity(sc, cam, Query.static(), DEFAULT_SETTINGS, "fp32")
