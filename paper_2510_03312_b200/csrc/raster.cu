@@ -166,6 +166,13 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
     return v;
 }
 
+// 1 << p in one instruction (bmsk: width-1 mask at position p)
+__device__ __forceinline__ uint32_t bit_at(uint32_t p) {
+    uint32_t m;
+    asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(m) : "r"(p));
+    return m;
+}
+
 // position of the most significant set bit (x != 0)
 __device__ __forceinline__ uint32_t msb_pos(uint32_t x) {
     uint32_t p;
@@ -308,7 +315,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 const uint32_t stop = sbase + (uint32_t)(32 * k + 31) * (uint32_t)sizeof(Rec32);
                 while (bits) {
                     const uint32_t p = msb_pos(bits);
-                    bits ^= 1u << p;
+                    bits ^= bit_at(p);
                     const uint32_t ra = stop - (p << 6);
                     const float4 r0 = lds128(ra), r1 = lds128(ra + 16);
                     const float dx = (pxf - r0.x) + r0.z;
