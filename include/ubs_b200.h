@@ -150,6 +150,8 @@ typedef struct UbsBinBuffers {
                               materialised (0xFFFFFFFF = full lists).  Tiles saturate long before
                               their lists end; a raster CTA that runs out of a capped list with
                               unsaturated pixels sets UBS_S_LIST_TRUNC. */
+    uint64_t *rect_sorted; /* n: tile rects in depth order (written by ubs_bin_depth; all-ones when the
+                              primitive touches no tile), read coalesced by the level-1 binning */
 } UbsBinBuffers;
 
 /* Forward outputs.  Image/alpha/T are f32, or f64 in the fp64 raster. */

@@ -56,7 +56,7 @@ class UbsBinBuffers(Structure):
                 ("temp", c_void_p), ("temp_bytes", c_size_t), ("chunk_hist", c_void_p),
                 ("chunk_hist_capacity", c_int64), ("chunk_count", c_int32), ("entries", c_void_p),
                 ("seg_scratch", c_void_p), ("bucket_start", c_void_p), ("bucket_capacity", c_int64),
-                ("status", c_void_p), ("list_cap", c_uint32)]
+                ("status", c_void_p), ("list_cap", c_uint32), ("rect_sorted", c_void_p)]
 
 
 class UbsImageBuffers(Structure):

@@ -29,6 +29,8 @@ namespace ubs {
 // writes its id there.  O(n) traffic in four light passes; the rank step is
 // O(s) per element for a bucket of s elements (a few on average; thousands
 // only if that many primitives share nearly the same depth bits).
+constexpr uint64_t kNoRect = ~0ull;  // rect_sorted entry of a primitive that touches no tile
+
 __host__ __device__ inline int sort_log_buckets(int64_t n) {
     int l = 12;
     while (l < 24 && ((int64_t)4 << l) < n) ++l;
@@ -79,10 +81,13 @@ __global__ void depth_scatter_kernel(const uint64_t *__restrict__ key64, const u
     tid[pos] = (uint32_t)i;
 }
 
+// also writes each primitive's tile rect at its rank (all-ones: no tile), so
+// the level-1 binning reads rects coalesced in depth order
 __global__ void depth_rank_kernel(const unsigned long long *__restrict__ range, int logB,
                                   const uint32_t *__restrict__ start, const uint64_t *__restrict__ tkey,
                                   const uint32_t *__restrict__ tid, const uint32_t *__restrict__ n_visible,
-                                  uint32_t *__restrict__ order) {
+                                  const uint64_t *__restrict__ rect, const uint32_t *__restrict__ tile_count,
+                                  uint32_t *__restrict__ order, uint64_t *__restrict__ rect_sorted) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= (int64_t)*n_visible) return;
     const uint64_t k = tkey[p];
@@ -95,6 +100,7 @@ __global__ void depth_rank_kernel(const unsigned long long *__restrict__ range, 
         rank += (kq < k || (kq == k && tid[q] < id)) ? 1u : 0u;
     }
     order[s0 + rank] = id;
+    rect_sorted[s0 + rank] = tile_count[id] != 0 ? rect[id] : kNoRect;
 }
 
 // Per-tile [start, end) from the rect-corner difference array (one CTA):
@@ -289,6 +295,19 @@ struct FlatBatch {
     uint64_t q;      // this lane's rect
     int nb, incl;    // this lane's bucket count and inclusive prefix
     int total;       // pairs in the batch
+    bool fast;       // owner[] holds the lane of every flat index
+};
+
+// Per-warp shared staging of a 32-rank batch: each lane's rect, flat offset
+// and id, plus owner[f] = lane of flat index f when the batch has at most
+// kOwnerCap pairs (then a flat index resolves with two dependent shared loads
+// instead of a 5-step shuffle binary search).
+constexpr int kOwnerCap = 512;
+struct FlatStage {
+    uint64_t q[32];
+    int excl[32];
+    uint32_t id[32];
+    uint8_t owner[kOwnerCap];
 };
 
 __device__ __forceinline__ int rank_bucket_count(uint64_t q, bool has) {
@@ -313,7 +332,7 @@ __device__ __forceinline__ uint64_t bucket_entry(uint32_t id, uint64_t q, int ba
     return (uint64_t)id | ((uint64_t)mask << 32);
 }
 
-__device__ __forceinline__ FlatBatch flat_batch(uint64_t q, bool has, int lane) {
+__device__ __forceinline__ FlatBatch flat_batch(uint64_t q, bool has, uint32_t id, int lane, FlatStage &st) {
     FlatBatch fb;
     fb.q = q;
     fb.nb = rank_bucket_count(q, has);
@@ -325,22 +344,35 @@ __device__ __forceinline__ FlatBatch flat_batch(uint64_t q, bool has, int lane) 
     }
     fb.incl = x;
     fb.total = __shfl_sync(0xffffffffu, x, 31);
+    fb.fast = fb.total <= kOwnerCap;
+    __syncwarp();  // the previous batch's readers are done
+    const int excl = x - fb.nb;
+    st.q[lane] = q;
+    st.excl[lane] = excl;
+    st.id[lane] = id;
+    if (fb.fast)
+        for (int i = 0; i < fb.nb; ++i) st.owner[excl + i] = (uint8_t)lane;
+    __syncwarp();
     return fb;
 }
 
 // (rank lane j, bucket k = grp * NB + band) of flat index f (all lanes
-// participate in the shuffles); q = rank j's rect
-__device__ __forceinline__ int flat_locate(const FlatBatch &fb, int f, int NB, int &j, uint64_t &q, int &band,
-                                           int &grp) {
-    int lo = 0;
+// participate: the slow path shuffles); q = rank j's rect
+__device__ __forceinline__ int flat_locate(const FlatBatch &fb, const FlatStage &st, int f, int NB, int &j,
+                                           uint64_t &q, int &band, int &grp) {
+    if (fb.fast) {
+        j = st.owner[f];
+    } else {
+        int lo = 0;
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-        const int incl_mid = __shfl_sync(0xffffffffu, fb.incl, lo + step - 1);
-        if (incl_mid <= f) lo += step;
+        for (int step = 16; step > 0; step >>= 1) {
+            const int incl_mid = __shfl_sync(0xffffffffu, fb.incl, lo + step - 1);
+            if (incl_mid <= f) lo += step;
+        }
+        j = lo;  // first lane whose inclusive prefix exceeds f
     }
-    j = lo;  // first lane whose inclusive prefix exceeds f
-    q = __shfl_sync(0xffffffffu, fb.q, j);
-    const int excl = __shfl_sync(0xffffffffu, fb.incl - fb.nb, j);
+    q = st.q[j];
+    const int excl = st.excl[j];
     const int b0 = (int)(q & 0xFFFF) / kBand, g0 = (int)((q >> 16) & 0xFFFF) / kRows;
     const int nbw = (int)((q >> 32) & 0xFFFF) / kBand - b0 + 1;
     const int i = f - excl;
@@ -352,24 +384,23 @@ __device__ __forceinline__ int flat_locate(const FlatBatch &fb, int f, int NB, i
 }
 
 // count the (rank, bucket) pairs of ranks [r0, r1) into cnt (shared atomics)
-__device__ __forceinline__ void count_slice(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
-                                            const uint32_t *__restrict__ tile_count, int64_t r0, int64_t r1,
-                                            int NB, uint32_t *cnt, int lane) {
+__device__ __forceinline__ void count_slice(const uint64_t *__restrict__ rect_sorted, int64_t r0, int64_t r1,
+                                            int NB, uint32_t *cnt, int lane, FlatStage &st) {
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int64_t r = rb + lane;
         uint64_t q = 0;
         bool has = false;
         if (r < r1) {
-            const uint32_t id = order[r];
-            has = tile_count[id] != 0;
-            if (has) q = rect[id];
+            q = rect_sorted[r];
+            has = q != kNoRect;
+            if (!has) q = 0;
         }
-        const FlatBatch fb = flat_batch(q, has, lane);
+        const FlatBatch fb = flat_batch(q, has, 0u, lane, st);
         for (int f0 = 0; f0 < fb.total; f0 += 32) {
             const int f = f0 + lane;
             int j, band, grp;
             uint64_t q;
-            const int k = flat_locate(fb, min(f, fb.total - 1), NB, j, q, band, grp);
+            const int k = flat_locate(fb, st, min(f, fb.total - 1), NB, j, q, band, grp);
             if (f < fb.total) atomicAdd(&cnt[k], 1u);
         }
     }
@@ -377,17 +408,17 @@ __device__ __forceinline__ void count_slice(const uint32_t *__restrict__ order, 
 
 // (1) per-CTA-chunk bucket counts (8 warps count 128-rank slices into one array)
 __global__ void __launch_bounds__(kBinWarps * 32)
-bucket_hist_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
-                   const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G, int NB,
+bucket_hist_kernel(const uint64_t *__restrict__ rect_sorted, const uint32_t *__restrict__ n_visible, int G, int NB,
                    int nbk, uint32_t *__restrict__ hist) {
     extern __shared__ uint32_t scnt[];  // nbk
+    __shared__ FlatStage stage[kBinWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) scnt[k] = 0;
     __syncthreads();
     const int64_t nv = *n_visible;
     const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
     const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
-    count_slice(order, rect, tile_count, r0, r1, NB, scnt, lane);
+    count_slice(rect_sorted, r0, r1, NB, scnt, lane, stage[w]);
     __syncthreads();
     uint32_t *h = hist + (int64_t)blockIdx.x * nbk;
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) h[k] = scnt[k];
@@ -467,13 +498,14 @@ bucket_offsets_kernel(const uint32_t *__restrict__ hist, int G, int nbk, uint32_
 // lanes of one step that hit the same bucket are ranked with
 // __match_any_sync, so every bucket's entries come out in rank order.
 __global__ void __launch_bounds__(kBinWarps * 32)
-bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect,
-                      const uint32_t *__restrict__ tile_count, const uint32_t *__restrict__ n_visible, int G,
+bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect_sorted,
+                      const uint32_t *__restrict__ n_visible, int G,
                       int NB, int nbk, const uint32_t *__restrict__ off, const uint32_t *__restrict__ bstart,
                       uint64_t *__restrict__ entries,
                       const unsigned long long *__restrict__ n_pairs, int64_t capacity, uint32_t *status) {
     if (pairs_overflow(n_pairs, capacity, status)) return;
     extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
+    __shared__ FlatStage stage[kBinWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t nv = *n_visible;
     const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
@@ -482,7 +514,7 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     uint32_t *sfill = sfill_all + w * nbk;
     for (int k = lane; k < nbk; k += 32) sfill[k] = 0;
     __syncwarp();
-    count_slice(order, rect, tile_count, r0, r1, NB, sfill, lane);
+    count_slice(rect_sorted, r0, r1, NB, sfill, lane, stage[w]);
     __syncthreads();
     const uint32_t *o = off + (int64_t)blockIdx.x * nbk;
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) {
@@ -503,17 +535,19 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
         bool has = false;
         if (r < r1) {
             id = order[r];
-            has = tile_count[id] != 0;
-            if (has) q = rect[id];
+            q = rect_sorted[r];
+            has = q != kNoRect;
+            if (!has) q = 0;
         }
-        const FlatBatch fb = flat_batch(q, has, lane);
+        FlatStage &st = stage[w];
+        const FlatBatch fb = flat_batch(q, has, id, lane, st);
         for (int f0 = 0; f0 < fb.total; f0 += 32) {
             const int f = f0 + lane;
             const bool act = f < fb.total;
             int j, band, grp;
             uint64_t qj;
-            const int k = flat_locate(fb, act ? f : fb.total - 1, NB, j, qj, band, grp);
-            const uint32_t idj = __shfl_sync(0xffffffffu, id, j);
+            const int k = flat_locate(fb, st, act ? f : fb.total - 1, NB, j, qj, band, grp);
+            const uint32_t idj = st.id[j];
             const unsigned same = __match_any_sync(0xffffffffu, act ? k : -1);
             const uint32_t base = sfill[act ? k : 0];
             if (act) entries[base + __popc(same & lt)] = bucket_entry(idj, qj, band, grp);
@@ -653,8 +687,9 @@ extern "C" int ubs_bin_depth(const UbsView *v, const UbsPrimBuffers *pb, const U
         return UBS_E_CUDA;
     depth_scatter_kernel<<<blocks, thr, 0, s>>>(pb->depth_key, pb->depth_range, n, logB, start, hist, tkey,
                                                 bb->ids_iota);
+    if (!bb->rect_sorted) return UBS_E_ARGS;
     depth_rank_kernel<<<blocks, thr, 0, s>>>(pb->depth_range, logB, start, tkey, bb->ids_iota, pb->n_visible,
-                                             bb->order);
+                                             pb->rect, pb->tile_count, bb->order, bb->rect_sorted);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
@@ -679,15 +714,15 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     if (cnt_bytes > 200 * 1024) return UBS_E_ARGS;
     cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
     const unsigned cta = (unsigned)G;
-    bucket_hist_kernel<<<cta, kBinWarps * 32, sizeof(uint32_t) * nbk, s>>>(bb->order, pb->rect, pb->tile_count,
-                                                                           pb->n_visible, G, NB, nbk,
-                                                                           bb->chunk_hist);
+    if (!bb->rect_sorted) return UBS_E_ARGS;
+    bucket_hist_kernel<<<cta, kBinWarps * 32, sizeof(uint32_t) * nbk, s>>>(bb->rect_sorted, pb->n_visible, G, NB,
+                                                                           nbk, bb->chunk_hist);
     // seg_scratch: bucket totals (nbk) | ticket (1)
     uint32_t *total = bb->seg_scratch, *ticket = total + nbk;
     uint32_t *off = bb->chunk_hist + (size_t)G * nbk;  // second half of chunk_hist
     if (cudaMemsetAsync(ticket, 0, sizeof(uint32_t), s) != cudaSuccess) return UBS_E_CUDA;
     bucket_offsets_kernel<<<nbk, kOffThreads, 0, s>>>(bb->chunk_hist, G, nbk, off, total, bb->bucket_start, ticket);
-    bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, pb->rect, pb->tile_count,
+    bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, bb->rect_sorted,
                                                                  pb->n_visible, G, NB, nbk, off, bb->bucket_start,
                                                                  bb->entries,
                                                                  pb->n_pairs, bb->pair_capacity, bb->status);

@@ -261,6 +261,7 @@ class Workspace:
         self.rec64 = self._i(cap * REC64_BYTES // 8, torch.float64)
         self.rec32 = None if self.f64 else self._i(cap * REC32_BYTES // 4, torch.float32)
         self.keys_sorted = self._i(cap, torch.int64)
+        self.rect_sorted = self._i(cap, torch.int64)
         self.ids_iota = self._i(cap, torch.int32)
         self.order = self._i(cap, torch.int32)
         self.hit_clamp = self._i(cap, torch.uint8)
@@ -335,6 +336,7 @@ class Workspace:
     def bin_buffers(self) -> UbsBinBuffers:
         bb = UbsBinBuffers()
         bb.keys_sorted = _ptr(self.keys_sorted)
+        bb.rect_sorted = _ptr(self.rect_sorted)
         bb.ids_iota = _ptr(self.ids_iota)
         bb.order = _ptr(self.order)
         if self.pair_cap:
