@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--inflight", type=int, default=4, help="frames in flight (engine.FramePipeline depth)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step measurement")
@@ -67,7 +68,8 @@ def workload_config(a):
     return {"workload": f"config 4: {a.nd}D UBS scene, {a.n_prims} primitives, {a.width}x{a.height}, "
                         f"{SWEEP}-frame time sweep (one frame per step)",
             "n_prims": a.n_prims, "n_dims": a.nd, "width": a.width, "height": a.height,
-            "sweep_frames": SWEEP, "scene": "synth(nd, N, seed=1) (SURVEY 8d), float32 records",
+            "sweep_frames": SWEEP, "frames_in_flight": a.inflight,
+            "scene": "synth(nd, N, seed=1) (SURVEY 8d), float32 records",
             "l2": "inputs exceed L2: 4*P*N = %.0f MB of primitive records (> 126 MB L2) are re-read every "
                   "frame; no explicit flush" % (4 * (14 + 6 * (a.nd - 3)) * a.n_prims / 1e6)}
 
@@ -270,9 +272,17 @@ def run_ours(a, rank, world, local_rank):
     cam = S.bench_camera(a.width, a.height)
     dtype = torch.float64 if a.precision == "fp64" else torch.float32
     ds = engine.DeviceScene.from_scene(scene, dtype=dtype, device=dev)
+    # the sweep renders through a pipeline of `inflight` frames (own stream and
+    # workspace each); the per-stage breakdown uses one extra single-stream
+    # workspace so its event times are not inflated by the overlap
+    pipe = engine.FramePipeline(ds, max(a.inflight, 1), a.precision, dev)
     ws = engine.Workspace(dev, a.precision)
 
     def frame(k, timers=None, sync=False):
+        return pipe.render(cam, frame_query(a.nd, cam, rank + world * k), DEFAULT_SETTINGS, timers=timers,
+                           sync=sync)
+
+    def frame_single(k, timers=None, sync=False):
         return engine.render_frame(ws, ds, cam, frame_query(a.nd, cam, rank + world * k), DEFAULT_SETTINGS,
                                    timers=timers, sync=sync)
 
@@ -282,11 +292,13 @@ def run_ours(a, rank, world, local_rank):
 
     # warm-up: synchronous frames size the pair buffers for the whole sweep
     # (capacity grows by 1.3x), the timed frames are fully asynchronous
-    for k in range(max(a.warmup, 0)):
+    for k in range(max(a.warmup, pipe.depth)):
         frame(k, sync=True)
+    for k in range(max(a.warmup, 1)):
+        frame_single(k, sync=True)
     stats = {"n_vis": 0, "k": 0, "frames": 0, "entries": 0, "ids": 0}
     for k in range(0, SWEEP, 25):
-        fr = frame(k, sync=True)
+        fr = frame_single(k, sync=True)
         stats["n_vis"] += fr.n_visible
         stats["k"] += fr.n_pairs
         stats["frames"] += 1
@@ -297,6 +309,7 @@ def run_ours(a, rank, world, local_rank):
 
     # --- device-resident throughput -------------------------------------
     def timed_sweep(timers=None):
+        render = frame if timers is None else frame_single
         sampler = ClockSampler(physical_gpu_index(local_rank))
         time.sleep(0.3)
         barrier()
@@ -305,7 +318,8 @@ def run_ours(a, rank, world, local_rank):
         ds.invalidate_statics()  # the sweep pays its one scene-statics pass
         e0.record()
         for k in range(a.steps):
-            fr = frame(k, timers)
+            fr = render(k, timers)
+        pipe.join()
         e1.record()
         torch.cuda.synchronize()
         barrier()
@@ -317,20 +331,20 @@ def run_ours(a, rank, world, local_rank):
     for attempt in range(2):
         ms, _, clocks, fr = timed_sweep()
         # no async frame may have outgrown its pair buffers (decided jointly by all ranks)
-        bad = ws.status.clone().to(torch.int32)
+        bad = pipe.status().to(torch.int32)
         if world > 1:
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()) == 0:
             break
-        ws.status.zero_()
+        pipe.clear_status()
         for k in range(a.steps):  # grow the buffers with synchronous frames, then re-time
             frame(k, sync=True)
     else:
         raise RuntimeError("pair-buffer overflow persisted")
-    _, timers, _, _ = timed_sweep({})
-    engine.check_status(ws)
     fixed = fr.n_fixed
     visits = fr.processed_pixels
+    _, timers, _, _ = timed_sweep({})
+    engine.check_status(ws)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -356,8 +370,14 @@ def run_ours(a, rank, world, local_rank):
 
     # --- end to end: image streamed to pinned host memory every frame -----
     sink = engine.HostFrameSink(a.height, a.width, dtype=ws.image_buf.dtype, device=dev)
-    for k in range(2):
-        sink.submit(frame(k))
+
+    def submit(k):
+        fr = frame(k)
+        with torch.cuda.stream(pipe.stream_of(fr)):  # the snapshot follows the frame on its stream
+            sink.submit(fr)
+
+    for k in range(2 * pipe.depth):
+        submit(k)
     sink.synchronize()
     torch.cuda.synchronize()
     barrier()
@@ -365,11 +385,12 @@ def run_ours(a, rank, world, local_rank):
     ds.invalidate_statics()
     f0.record()
     for k in range(a.steps):
-        sink.submit(frame(k))
+        submit(k)
+    pipe.join()
     torch.cuda.current_stream().wait_stream(sink.copy_stream)
     f1.record()
     torch.cuda.synchronize()
-    engine.check_status(ws)
+    pipe.check_status()
     barrier()
     te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
     if world > 1:
@@ -420,7 +441,7 @@ def run_ours(a, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": sink.bytes_per_frame,
-                "path": "engine.render_frame + HostFrameSink (fp32 image -> pinned host, copy stream)"},
+                "path": "engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, copy stream)"},
         "gpu_launches": per_frame_launches * a.steps + 1,
         "clocks": clocks,
         "train": train,

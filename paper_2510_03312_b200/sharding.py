@@ -170,14 +170,24 @@ class DeviceAdam:
 
 
 def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=DEFAULT_SETTINGS, group=None,
-                 sink: engine.HostFrameSink | None = None):
+                 sink: engine.HostFrameSink | None = None, pipeline: engine.FramePipeline | None = None):
     """Forward-render this rank's share of ``views`` [(cam, query), ...]; no
-    communication.  Returns the number of frames rendered by this rank."""
+    communication.  With ``pipeline`` the frames go through its slots (several
+    frames in flight; ``ws`` is unused).  Returns the number of frames
+    rendered by this rank."""
     rank, world = dist_rank_world(group)
     k = 0
     for cam, query in shard(views, rank, world):
-        fr = engine.render_frame(ws, ds, cam, query, settings)
-        if sink is not None:
-            sink.submit(fr)
+        if pipeline is None:
+            fr = engine.render_frame(ws, ds, cam, query, settings)
+            if sink is not None:
+                sink.submit(fr)
+        else:
+            fr = pipeline.render(cam, query, settings)
+            if sink is not None:
+                with torch.cuda.stream(pipeline.stream_of(fr)):
+                    sink.submit(fr)
         k += 1
+    if pipeline is not None:
+        pipeline.join()
     return k

@@ -306,3 +306,28 @@ def test_large_frame_uses_global_tile_scan():
     sc = quantize_f32(S.synth(3, 3000, seed=41))
     cam = S.bench_camera(4000, 3600)
     assert_frame_parity(sc, cam, Query.static(), DEFAULT_SETTINGS, "fp32")
+
+
+def test_frame_pipeline_matches_single_stream():
+    # frames in flight on separate streams / workspaces give the same bits as
+    # one-at-a-time rendering, and the pipeline's status covers every slot
+    import torch
+    from paper_2510_03312_b200 import engine
+    sc = quantize_f32(S.random_scene(7, 4000, seed=61))
+    cam = S.random_camera(160, 62)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    qs = [S.random_query(7, 70 + k) for k in range(7)]
+    ref = [engine.render_frame(ws, ds, cam, q).image.clone() for q in qs]
+    pipe = engine.FramePipeline(ds, depth=3)
+    for q in qs * 3:  # 21 synchronous frames: every slot sized by every query
+        pipe.render(cam, q, sync=True)
+    got = []
+    for q in qs:
+        fr = pipe.render(cam, q)
+        with torch.cuda.stream(pipe.stream_of(fr)):
+            got.append(fr.image.clone())
+    pipe.join()
+    assert pipe.check_status() == 0
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
