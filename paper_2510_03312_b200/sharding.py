@@ -47,37 +47,93 @@ def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
 
 
 class GpuViewBackend:
-    """Per-view loss + gradient on this rank's GPU through the C-ABI engine."""
+    """Per-view loss + gradient on this rank's GPU through the C-ABI engine.
+
+    ``depth`` > 1 keeps that many views in flight: view k of a batch runs on
+    slot k % depth (own stream, workspace and gradient buffer), so one view's
+    latency-bound preprocess / loss / chain kernels overlap another view's
+    raster backward.  Slot gradients are summed into the caller's buffer at
+    :meth:`end` (summation order differs from one-at-a-time accumulation only
+    at the rounding level)."""
 
     def __init__(self, ds: engine.DeviceScene, precision: str = "fp32", settings=DEFAULT_SETTINGS,
-                 grad_dtype=torch.float32):
+                 grad_dtype=torch.float32, depth: int = 1):
         self.ds = ds
-        self.ws = engine.Workspace(ds.device, precision)
         self.settings = settings
         self.grad_dtype = grad_dtype
+        self.depth = max(1, int(depth))
+        self.workspaces = [engine.Workspace(ds.device, precision) for _ in range(self.depth)]
+        self.ws = self.workspaces[0]
+        self.streams = [torch.cuda.Stream(ds.device) for _ in range(self.depth)] if self.depth > 1 else None
+        self.slot_grads = [None] * self.depth
+        self._k = 0
+        self._grad = None
+        self._rec = None
 
     def new_grad(self) -> torch.Tensor:
         return torch.zeros(self.ds.params.shape, dtype=self.grad_dtype, device=self.ds.device)
+
+    def _view(self, ws, cam, query, target, cfg: LossConfig, scale: float, grad, sync: bool):
+        fr = engine.render_frame(ws, self.ds, cam, query, self.settings, sync=sync or ws.pair_cap == 0)
+        ws.loss_parts.zero_()
+        g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
+        engine.backward_frame(fr, self.ds, g_img, grad)
+        size = fr.width * fr.height * 3
+        return (1.0 - cfg.lambda_ssim) * parts[0] / size + cfg.lambda_ssim * (1.0 - parts[1] / size)
 
     def view_loss_grad(self, cam, query, target: torch.Tensor, cfg: LossConfig, scale: float,
                        grad: torch.Tensor, sync: bool = False) -> torch.Tensor:
         """Adds this view's d(loss)/d(params) into ``grad``; returns the view's
         reconstruction term (1-l) L1 + l (1 - SSIM) as a 0-d device tensor.
         Frames are asynchronous unless ``sync`` (see :meth:`status`)."""
-        fr = engine.render_frame(self.ws, self.ds, cam, query, self.settings,
-                                 sync=sync or self.ws.pair_cap == 0)
-        self.ws.loss_parts.zero_()
-        g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
-        engine.backward_frame(fr, self.ds, g_img, grad)
-        size = fr.width * fr.height * 3
-        return (1.0 - cfg.lambda_ssim) * parts[0] / size + cfg.lambda_ssim * (1.0 - parts[1] / size)
+        return self._view(self.ws, cam, query, target, cfg, scale, grad, sync)
+
+    # --- batched interface (ViewShardedStep) -------------------------------
+    def begin(self, grad: torch.Tensor):
+        self._k = 0
+        self._grad = grad
+        self._rec = torch.zeros(self.depth, dtype=torch.float64, device=grad.device)
+        for i in range(1, self.depth):
+            if self.slot_grads[i] is None or self.slot_grads[i].shape != grad.shape:
+                self.slot_grads[i] = torch.zeros_like(grad)
+            else:
+                self.slot_grads[i].zero_()
+
+    def view(self, cam, query, target, cfg: LossConfig, scale: float, sync: bool = False):
+        i = self._k % self.depth
+        self._k += 1
+        if self.depth == 1:
+            self._rec[0] += self._view(self.ws, cam, query, target, cfg, scale, self._grad, sync)
+            return
+        self.ds.statics_ptr(self.settings)  # on the caller's stream, before any slot reads them
+        s = self.streams[i]
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g = self._grad if i == 0 else self.slot_grads[i]
+            term = self._view(self.workspaces[i], cam, query, target, cfg, scale, g, sync)
+            self._rec[i:i + 1] += term
+
+    def end(self) -> torch.Tensor:
+        """Join the slots, fold their gradients into the batch buffer; returns
+        the summed reconstruction terms (0-d device tensor)."""
+        if self.depth > 1:
+            cur = torch.cuda.current_stream()
+            for s in self.streams:
+                cur.wait_stream(s)
+            for i in range(1, min(self.depth, self._k)):
+                self._grad += self.slot_grads[i]
+        return self._rec.sum()
 
     def status(self) -> torch.Tensor:
         """Device flag, nonzero when an asynchronous view outgrew the pair buffers."""
-        return self.ws.status
+        out = self.workspaces[0].status.clone()
+        for ws in self.workspaces[1:]:
+            out |= ws.status
+        return out
 
     def clear_status(self):
-        self.ws.status.zero_()
+        for ws in self.workspaces:
+            ws.status.zero_()
 
     def add_regularisers(self, grad: torch.Tensor, cfg: LossConfig):
         lib = _lib.load()
@@ -113,8 +169,14 @@ class ViewShardedStep:
             sync = attempt > 0  # retry with synchronous frames if a view outgrew the pair buffers
             grad = b.new_grad() if grad is None else grad.zero_()
             rec = torch.zeros(2, dtype=torch.float64, device=grad.device)
-            for cam, query, target in shard(views, rank, world):
-                rec[0] += b.view_loss_grad(cam, query, target, cfg, scale, grad, sync=sync)
+            if hasattr(b, "begin"):  # batched backend: views may be in flight concurrently
+                b.begin(grad)
+                for cam, query, target in shard(views, rank, world):
+                    b.view(cam, query, target, cfg, scale, sync=sync)
+                rec[0] += b.end()
+            else:
+                for cam, query, target in shard(views, rank, world):
+                    rec[0] += b.view_loss_grad(cam, query, target, cfg, scale, grad, sync=sync)
             if hasattr(b, "status"):
                 rec[1] = b.status().to(torch.float64)[0]
             allreduce_sum_(rec, self.group)  # loss term and overflow flag in one collective
