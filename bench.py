@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
-    ap.add_argument("--inflight", type=int, default=4, help="frames in flight (engine.FramePipeline depth)")
+    ap.add_argument("--inflight", type=int, default=8, help="frames in flight (engine.FramePipeline depth)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step measurement")
