@@ -136,6 +136,23 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_issue(stage: str):
+    """Issue-rate roofline of the stage's longest kernel from the committed ncu
+    capture (profiles/issue.json): warp instructions / duration against
+    148 SMs x 4 schedulers x 1 warp-instruction per clock."""
+    p = ROOT / "profiles" / "issue.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    ks = [(k, v) for k, v in d.items() if isinstance(v, dict) and v.get("stage") == stage]
+    if not ks:
+        return None
+    k, v = max(ks, key=lambda kv: kv[1]["duration_us"])
+    return {"kernel": k, "bound": "issue", "achieved": v["achieved_warp_inst_per_s"],
+            "peak": v["peak_warp_inst_per_s"], "unit": "warp-instructions/s", "frac": v["frac"],
+            "warp_instructions": v["warp_instructions"], "source": "profiles/issue.json (ncu capture)"}
+
+
 def ncu_traffic(stage: str):
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
@@ -434,6 +451,7 @@ def run_ours(a, rank, world, local_rank):
         "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": b_dom, "launch_ms": stage_ms[dominant]},
+        "issue_roofline": ncu_issue(dominant),
         "frame_roofline": {"bytes_per_frame": b_frame, "achieved_gbs": b_frame / (ms_max / a.steps / 1e3) / 1e9,
                            "frac": b_frame / (ms_max / a.steps / 1e3) / 1e9 / peak,
                            "ceiling_fps": peak * 1e9 / b_frame},
