@@ -76,8 +76,11 @@ def workload_config(a):
 
 
 def frame_query(nd, cam, k):
+    """Query of step k: sweep frame (37 k) mod 300 -- 37 is coprime with the
+    sweep length, so 300 steps visit every frame once and any shorter run
+    samples the whole time range instead of its cheap start."""
     from paper_2510_03312_b200 import synthetic as S
-    return S.bench_query(nd, cam, (k % SWEEP) / (SWEEP - 1))
+    return S.bench_query(nd, cam, ((37 * k) % SWEEP) / (SWEEP - 1))
 
 
 # ---------------------------------------------------------------------------
@@ -173,7 +176,7 @@ def cpu_frames(scene, cam, nd, settings, budget_s, max_frames, warm=True):
     t0 = time.perf_counter()
     done = 0
     while done < max_frames:
-        O.render_frame(scene, cam, frame_query(nd, cam, done * 37), settings)
+        O.render_frame(scene, cam, frame_query(nd, cam, done), settings)
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
