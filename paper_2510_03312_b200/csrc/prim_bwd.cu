@@ -100,14 +100,20 @@ prim_bwd_kernel(const UbsView v, const GT *__restrict__ grad2d, OT *__restrict__
     double mu_x[3];
     prim_geom<C, PT>(rec, v, g, mu_x);
 
+    // grad2d holds raw per-pixel moments (raster_bwd kernels); the per-splat
+    // factors of tile_backward (_tiles.py:114-127) are applied here once:
+    //   g_mean2 = -2 c P sum(h d), g_P = c sum(h d d^T) (both off-diagonals get
+    //   the dx dy moment), c = -beta / tau; g_og = sum(g_a a) / og
     const GT *q = grad2d + i * kGrad2dStride;
-    const double gm2x = q[0], gm2y = q[1];
-    const double gPa = q[2], gPc = q[3], gPb = q[4];
-    const double g_og = q[5], g_bx = q[6];
+    const double p00 = g.p2[0], p01 = g.p2[1], p11 = g.p2[2];
+    const double cm = -g.beta_x / v.set.tau_sq;
+    const double sx = q[0], sy = q[1];
+    const double gm2x = -2.0 * cm * (p00 * sx + p01 * sy), gm2y = -2.0 * cm * (p01 * sx + p11 * sy);
+    const double gPa = cm * (double)q[2], gPc = cm * (double)q[3], gPb = cm * (double)q[4];
+    const double g_og = g.og != 0.0 ? (double)q[5] / g.og : 0.0, g_bx = q[6];
     const double gcol[3] = {(double)q[7], (double)q[8], (double)q[9]};
 
     // conic -> covariance: g_cov2 = -P g_P P (gradients.py:161)
-    const double p00 = g.p2[0], p01 = g.p2[1], p11 = g.p2[2];
     double gc2[2][2];
     {
         // t = g_P P

@@ -651,16 +651,18 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
                     suffix += gc * w;
                     T = ti;
                     if (e.a < clamp) {
+                        // raw moments (see raster_bwd32_kernel); prim_bwd applies -2 P,
+                        // -beta / tau and 1 / og per primitive
                         const Real x = e.m / tau;
                         const Real gaa = ga * e.a;
-                        v[5] = ga * e.a * rcp_(e.og);
+                        v[5] = gaa;
                         v[6] = gaa * log1p_(-x);
-                        const Real gm = gaa * (-e.bx / ((Real)1 - x)) / tau;
-                        v[0] = (Real)-2 * gm * e.pd0;
-                        v[1] = (Real)-2 * gm * e.pd1;
-                        v[2] = gm * e.dx * e.dx;
-                        v[3] = gm * e.dx * e.dy;  // both off-diagonals of pg_p2 get this (_tiles.py:125-126)
-                        v[4] = gm * e.dy * e.dy;
+                        const Real h = gaa / ((Real)1 - x);
+                        v[0] = h * e.dx;
+                        v[1] = h * e.dy;
+                        v[2] = h * e.dx * e.dx;
+                        v[3] = h * e.dx * e.dy;
+                        v[4] = h * e.dy * e.dy;
                     }
                 }
             }
@@ -682,7 +684,11 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
 // the forward's chain) and MUFU reciprocals / lg2 in the derivatives:
 //   d alpha / d og = alpha / og,  d alpha / d beta = alpha ln(1 - x),
 //   d alpha / d m = -alpha beta / (tau (1 - x)),  x = m / tau.
-// The 10 per-splat sums are warp reduce-scattered and added with atomics.
+// The 10 per-splat sums (raw moments: sum h d, sum h d d^T with
+// h = g_alpha alpha / (1 - x), sum g_alpha alpha, sum g_alpha alpha ln(1 - x),
+// sum w g_rgb) are warp reduce-scattered and added with atomics; prim_bwd turns
+// them into d/d mean2 = -2 (-beta/tau) P sum h d, d/d P = (-beta/tau) sum h d d^T,
+// d/d og = sum / og, d/d beta = sum g_alpha alpha ln(1 - x) (_tiles.py:97-127).
 __global__ void __launch_bounds__(kTileThreads)
 raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
@@ -791,17 +797,18 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                             suffix = fmaf(gc, w, suffix);
                             T = ti;
                             if (!clamped) {
+                                // raw moments; prim_bwd applies the per-splat factors
+                                // (-2 P, -beta / tau, 1 / og) once per primitive
                                 const float gaa = ga * a;
-                                v[5] = gaa * rcp_approx(r3.y);
-                                v[6] = gaa * (L * kLn2);
-                                const float gm = -gaa * r2.x * rcp_approx(omx) * inv_tau;
-                                const float pd0 = r1.x * y0;               // P d = U^T (U d)
-                                const float pd1 = fmaf(r1.y, y0, r1.z * y1);
-                                v[0] = -2.0f * gm * pd0;
-                                v[1] = -2.0f * gm * pd1;
-                                v[2] = gm * dx * dx;
-                                v[3] = gm * dx * dy;  // both off-diagonals of pg_p2 get this (_tiles.py:125-126)
-                                v[4] = gm * dy * dy;
+                                v[5] = gaa;
+                                v[6] = gaa * (L * kLn2);  // gaa ln(1 - x)
+                                const float h = gaa * rcp_approx(omx);
+                                const float hx = h * dx, hy = h * dy;
+                                v[0] = hx;
+                                v[1] = hy;
+                                v[2] = hx * dx;
+                                v[3] = hx * dy;
+                                v[4] = hy * dy;
                             }
                         }
                     }
