@@ -584,6 +584,45 @@ __device__ __forceinline__ T warp_reduce_scatter16(T (&v)[16], int lane, int &id
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// Warp sums of 10 per-lane values v[0..9] in ~44 instructions: components
+// 0..7 by a reduce-scatter over lane bits 4..2 plus two xor levels (lane l
+// ends with component ((l >> 2) & 7) bit-reversed as idx below), components
+// 8 and 9 by one exchange over bit 4 plus four xor levels (every lower lane
+// holds sum v8, every upper lane sum v9).  Lanes l % 4 == 0 report component
+// idx, lane 1 component 8, lane 17 component 9: one atomic instruction.
+template <typename T>
+__device__ __forceinline__ bool warp_reduce10(T (&v)[16], int lane, int &idx, T &out) {
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+        const int half = 4 >> lvl, off = 16 >> lvl;
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const T send = upper ? v[i] : v[i + half];
+            const T keep = upper ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    T r = v[0];
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    const bool up = (lane & 16) != 0;
+    T c = (up ? v[9] : v[8]) + __shfl_xor_sync(0xffffffffu, up ? v[8] : v[9], 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((lane & 3) == 0) {
+        idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        out = r;
+        return true;
+    }
+    if (lane == 1 || lane == 17) {
+        idx = lane == 1 ? 8 : 9;
+        out = c;
+        return true;
+    }
+    return false;
+}
+
 template <typename Real>
 __global__ void __launch_bounds__(kTileThreads)
 raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
@@ -667,9 +706,9 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
                 }
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                int idx;
-                const Real mine = warp_reduce_scatter16(v, lane, idx);
-                if ((lane & 1) == 0 && idx < 10 && mine != (Real)0)
+                int idx = 0;
+                Real mine = 0;
+                if (warp_reduce10(v, lane, idx, mine) && mine != (Real)0)
                     atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + idx, mine);
             }
         }
@@ -814,9 +853,9 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     }
                 }
                 if (__any_sync(0xffffffffu, contrib)) {
-                    int idx;
-                    const float mine = warp_reduce_scatter16(v, lane, idx);
-                    if ((lane & 1) == 0 && idx < 10 && mine != 0.0f)
+                    int idx = 0;
+                    float mine = 0.0f;
+                    if (warp_reduce10(v, lane, idx, mine) && mine != 0.0f)
                         atomicAdd(grad2d + (int64_t)sid[jj] * kGrad2dStride + idx, mine);
                 }
             }
