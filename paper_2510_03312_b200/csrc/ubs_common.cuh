@@ -18,7 +18,7 @@ namespace ubs {
 constexpr int kTile = 16;
 constexpr int kTileThreads = kTile * kTile;
 constexpr uint64_t kInvisibleKey = 0xFFFFFFFFFFFFFFFFull;
-constexpr int kGrad2dStride = 12;  // g_mean2[2] g_P[00,01,11] g_og g_bx g_color[3] pad[2]
+constexpr int kGrad2dStride = 12;  // 10 raw moment sums (see ubs_b200.h UbsGradBuffers.grad2d) + pad[2]
 
 // fp64 raster record: exactly the operands tile_forward reads (_tiles.py:36-50).
 struct __align__(16) Rec64 {
