@@ -395,8 +395,9 @@ def run_ours(a, rank, world, local_rank):
 
     def submit(k):
         fr = frame(k)
-        with torch.cuda.stream(pipe.stream_of(fr)):  # the snapshot follows the frame on its stream
-            sink.submit(fr)
+        # zero-copy: the D2H reads the slot's own image; the slot's next frame waits for it
+        sink.submit(fr, source_stream=pipe.stream_of(fr))
+        pipe.hold(fr, sink.last_copy)
 
     for k in range(2 * pipe.depth):
         submit(k)

@@ -503,6 +503,7 @@ class FramePipeline:
         self.ds = ds
         self.workspaces = [Workspace(dev, precision) for _ in range(depth)]
         self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
+        self.pending = [None] * depth  # event a slot's next frame must wait for (a consumer of its buffers)
         self.k = 0
 
     @property
@@ -516,12 +517,20 @@ class FramePipeline:
         self.ds.statics_ptr(settings)  # (re)computed on the caller's stream if stale
         s = self.streams[i]
         s.wait_stream(torch.cuda.current_stream())
+        if self.pending[i] is not None:
+            s.wait_event(self.pending[i])
+            self.pending[i] = None
         with torch.cuda.stream(s):
             return render_frame(self.workspaces[i], self.ds, cam, query, settings, timers=timers, sync=sync,
                                 full_lists=full_lists)
 
     def stream_of(self, fr: Frame) -> torch.cuda.Stream:
         return self.streams[self.workspaces.index(fr.ws)]
+
+    def hold(self, fr: Frame, event: torch.cuda.Event):
+        """Keep ``fr``'s buffers until ``event`` (e.g. a host copy reading them)
+        completes: the slot's next frame waits for it."""
+        self.pending[self.workspaces.index(fr.ws)] = event
 
     def join(self):
         """Make the caller's stream wait for every frame issued so far."""
@@ -649,23 +658,35 @@ class HostFrameSink:
         self.dev_bufs = [torch.empty((height, width, 3), dtype=dtype, device=self.dev) for _ in range(slots)]
         self.host_bufs = [torch.empty((height, width, 3), dtype=dtype, pin_memory=True) for _ in range(slots)]
         self.done = [None] * slots
+        self.last_copy = None
         self.k = 0
         self.bytes_per_frame = height * width * 3 * torch.finfo(dtype).bits // 8
 
-    def submit(self, fr: Frame) -> torch.Tensor:
-        i = self.k % len(self.dev_bufs)
+    def submit(self, fr: Frame, source_stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Queue frame ``fr``'s image for the host.  With ``source_stream``
+        (the stream the frame was rendered on) the copy reads the frame's own
+        buffer with no device snapshot -- the caller must keep that buffer
+        alive until :attr:`last_copy` completes (FramePipeline.hold)."""
+        i = self.k % len(self.host_bufs)
         self.k += 1
-        if self.done[i] is not None:
-            torch.cuda.current_stream().wait_event(self.done[i])
-        self.dev_bufs[i].copy_(fr.image)
-        ready = torch.cuda.Event()
-        ready.record()
+        if source_stream is not None:
+            ready = torch.cuda.Event()
+            ready.record(source_stream)
+            src = fr.image
+        else:
+            if self.done[i] is not None:
+                torch.cuda.current_stream().wait_event(self.done[i])
+            self.dev_bufs[i].copy_(fr.image)
+            ready = torch.cuda.Event()
+            ready.record()
+            src = self.dev_bufs[i]
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_event(ready)
-            self.host_bufs[i].copy_(self.dev_bufs[i], non_blocking=True)
+            self.host_bufs[i].copy_(src, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
         self.done[i] = ev
+        self.last_copy = ev
         return self.host_bufs[i]
 
     def synchronize(self):

@@ -247,8 +247,8 @@ def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=D
         else:
             fr = pipeline.render(cam, query, settings)
             if sink is not None:
-                with torch.cuda.stream(pipeline.stream_of(fr)):
-                    sink.submit(fr)
+                sink.submit(fr, source_stream=pipeline.stream_of(fr))
+                pipeline.hold(fr, sink.last_copy)
         k += 1
     if pipeline is not None:
         pipeline.join()

@@ -331,3 +331,29 @@ def test_frame_pipeline_matches_single_stream():
     assert pipe.check_status() == 0
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+def test_pipeline_zero_copy_host_sink():
+    # the sink reads each slot's image directly; the slot's next frame waits
+    # for that copy, so every host image equals the single-stream render
+    import torch
+    from paper_2510_03312_b200 import engine
+    sc = quantize_f32(S.random_scene(6, 3000, seed=71))
+    cam = S.random_camera(96, 72)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    qs = [S.random_query(6, 80 + k) for k in range(9)]
+    ref = [engine.render_frame(ws, ds, cam, q).image.cpu() for q in qs]
+    pipe = engine.FramePipeline(ds, depth=2)
+    for q in qs * 2:
+        pipe.render(cam, q, sync=True)
+    sink = engine.HostFrameSink(96, 96, slots=len(qs))
+    outs = []
+    for q in qs:
+        fr = pipe.render(cam, q)
+        outs.append(sink.submit(fr, source_stream=pipe.stream_of(fr)))
+        pipe.hold(fr, sink.last_copy)
+    pipe.join()
+    sink.synchronize()
+    for a, b in zip(ref, outs):
+        assert torch.equal(a, b)
