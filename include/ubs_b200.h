@@ -137,7 +137,8 @@ typedef struct UbsBinBuffers {
     int64_t pair_capacity;
     void *temp;            /* ubs_bin_temp_bytes: depth-bucket histogram, starts, CUB scan scratch */
     size_t temp_bytes;
-    uint32_t *chunk_hist;  /* 2 x chunk_count x n_buckets: per-chunk bucket counts, then offsets */
+    uint32_t *chunk_hist;  /* 10 x chunk_count x n_buckets: per-chunk bucket counts, chunk offsets, then the
+                              per-warp counts of each chunk (8 warps) */
     int64_t chunk_hist_capacity; /* elements */
     int32_t chunk_count;   /* G rank chunks */
     uint64_t *entries;     /* pair_capacity: bucket entries (id | covered-tile mask of the 8 x 4

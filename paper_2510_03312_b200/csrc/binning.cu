@@ -409,19 +409,27 @@ __device__ __forceinline__ void count_slice(const uint64_t *__restrict__ rect_so
 // (1) per-CTA-chunk bucket counts (8 warps count 128-rank slices into one array)
 __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_hist_kernel(const uint64_t *__restrict__ rect_sorted, const uint32_t *__restrict__ n_visible, int G, int NB,
-                   int nbk, uint32_t *__restrict__ hist) {
-    extern __shared__ uint32_t scnt[];  // nbk
+                   int nbk, uint32_t *__restrict__ hist, uint32_t *__restrict__ whist) {
+    extern __shared__ uint32_t scnt_all[];  // kBinWarps x nbk: per-warp counts
     __shared__ FlatStage stage[kBinWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) scnt[k] = 0;
+    for (int k = threadIdx.x; k < kBinWarps * nbk; k += kBinWarps * 32) scnt_all[k] = 0;
     __syncthreads();
     const int64_t nv = *n_visible;
     const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
     const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
-    count_slice(rect_sorted, r0, r1, NB, scnt, lane, stage[w]);
+    count_slice(rect_sorted, r0, r1, NB, scnt_all + w * nbk, lane, stage[w]);
     __syncthreads();
+    // per-warp counts (the scatter's intra-chunk offsets) and the chunk totals
+    uint32_t *hw = whist + (int64_t)blockIdx.x * kBinWarps * nbk;
+    for (int k = threadIdx.x; k < kBinWarps * nbk; k += kBinWarps * 32) hw[k] = scnt_all[k];
     uint32_t *h = hist + (int64_t)blockIdx.x * nbk;
-    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) h[k] = scnt[k];
+    for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int ww = 0; ww < kBinWarps; ++ww) t += scnt_all[ww * nbk + k];
+        h[k] = t;
+    }
 }
 
 // (2) one kernel, one CTA per bucket k: off[c][k] = sum_{c' < c} hist[c'][k]
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(kBinWarps * 32)
 bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rect_sorted,
                       const uint32_t *__restrict__ n_visible, int G,
                       int NB, int nbk, const uint32_t *__restrict__ off, const uint32_t *__restrict__ bstart,
-                      uint64_t *__restrict__ entries,
+                      const uint32_t *__restrict__ whist, uint64_t *__restrict__ entries,
                       const unsigned long long *__restrict__ n_pairs, int64_t capacity, uint32_t *status) {
     if (pairs_overflow(n_pairs, capacity, status)) return;
     extern __shared__ uint32_t sfill_all[];  // kBinWarps x nbk
@@ -512,18 +520,15 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
     if (c0 >= nv) return;
     const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
     uint32_t *sfill = sfill_all + w * nbk;
-    for (int k = lane; k < nbk; k += 32) sfill[k] = 0;
-    __syncwarp();
-    count_slice(rect_sorted, r0, r1, NB, sfill, lane, stage[w]);
-    __syncthreads();
+    // per-warp start offsets: bucket start + chunk offset + earlier warps' counts
     const uint32_t *o = off + (int64_t)blockIdx.x * nbk;
+    const uint32_t *hw = whist + (int64_t)blockIdx.x * kBinWarps * nbk;
     for (int k = threadIdx.x; k < nbk; k += kBinWarps * 32) {
         uint32_t run = bstart[k] + o[k];
 #pragma unroll
         for (int ww = 0; ww < kBinWarps; ++ww) {
-            const uint32_t c = sfill_all[ww * nbk + k];
             sfill_all[ww * nbk + k] = run;
-            run += c;
+            run += hw[ww * nbk + k];
         }
     }
     __syncthreads();
@@ -707,7 +712,7 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     const int G = bb->chunk_count;
     if (G < 1 || !bb->chunk_hist || !bb->entries || !bb->seg_scratch || !bb->bucket_start || !bb->tile_ids)
         return UBS_E_ARGS;
-    if (2 * (int64_t)G * nbk > bb->chunk_hist_capacity || (int64_t)nbk + 1 > bb->bucket_capacity)
+    if ((2 + kBinWarps) * (int64_t)G * nbk > bb->chunk_hist_capacity || (int64_t)nbk + 1 > bb->bucket_capacity)
         return UBS_E_CAPACITY;
     if ((int64_t)G * kCtaRanks < v->n) return UBS_E_ARGS;  // chunk_count must cover n / kCtaRanks
     const size_t cnt_bytes = sizeof(uint32_t) * (size_t)kBinWarps * nbk;
@@ -715,8 +720,11 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
     const unsigned cta = (unsigned)G;
     if (!bb->rect_sorted) return UBS_E_ARGS;
-    bucket_hist_kernel<<<cta, kBinWarps * 32, sizeof(uint32_t) * nbk, s>>>(bb->rect_sorted, pb->n_visible, G, NB,
-                                                                           nbk, bb->chunk_hist);
+    // chunk_hist: chunk totals (G x nbk) | chunk offsets (G x nbk) | per-warp counts (G x kBinWarps x nbk)
+    uint32_t *whist = bb->chunk_hist + 2 * (size_t)G * nbk;
+    cudaFuncSetAttribute(bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cnt_bytes);
+    bucket_hist_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->rect_sorted, pb->n_visible, G, NB, nbk,
+                                                              bb->chunk_hist, whist);
     // seg_scratch: bucket totals (nbk) | ticket (1)
     uint32_t *total = bb->seg_scratch, *ticket = total + nbk;
     uint32_t *off = bb->chunk_hist + (size_t)G * nbk;  // second half of chunk_hist
@@ -724,7 +732,7 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     bucket_offsets_kernel<<<nbk, kOffThreads, 0, s>>>(bb->chunk_hist, G, nbk, off, total, bb->bucket_start, ticket);
     bucket_scatter_kernel<<<cta, kBinWarps * 32, cnt_bytes, s>>>(bb->order, bb->rect_sorted,
                                                                  pb->n_visible, G, NB, nbk, off, bb->bucket_start,
-                                                                 bb->entries,
+                                                                 whist, bb->entries,
                                                                  pb->n_pairs, bb->pair_capacity, bb->status);
     tile_lists_kernel<<<nbk * kRows, kListThreads, 0, s>>>(bb->entries, bb->bucket_start, bb->tile_ranges, TX, TY, NB,
                                                    bb->list_cap ? bb->list_cap : 0xFFFFFFFFu, bb->tile_ids,

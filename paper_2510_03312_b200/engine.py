@@ -299,8 +299,9 @@ class Workspace:
         nbk = math.ceil(ty / self.ROWS) * math.ceil(tx / self.BAND)
         g = max(1, -(-n // self.CHUNK_RANKS))
         self.chunk_count = g
-        if self.chunk_hist is None or self.chunk_hist.numel() < 2 * g * nbk:
-            self.chunk_hist = self._i(2 * g * nbk, torch.int32)
+        need = (2 + 8) * g * nbk  # chunk totals | chunk offsets | per-warp counts (8 warps per chunk)
+        if self.chunk_hist is None or self.chunk_hist.numel() < need:
+            self.chunk_hist = self._i(need, torch.int32)
         if self.seg_scratch is None or self.seg_scratch.numel() < nbk + 1:
             self.seg_scratch = self._i(nbk + 1, torch.int32)  # bucket totals | ticket
             self.bucket_start = self._i(nbk + 1, torch.int32)
