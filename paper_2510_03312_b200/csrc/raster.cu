@@ -502,87 +502,24 @@ raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 // ---------------------------------------------------------------------------
 // backward: reverse replay of the blend (tile_backward), warp-reduced atomics
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ T warp_sum(T x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
-
-template <typename Real>
-struct BwdTraits;
-template <>
-struct BwdTraits<double> {
-    using Rec = Rec64;
-};
-template <>
-struct BwdTraits<float> {
-    using Rec = Rec32;
-};
-
 // alpha (clamped), 1 - alpha, and the operands of its derivative at a pixel
-template <typename Real>
 struct SplatEval {
-    Real dx, dy, m, a, om, og, bx, c0, c1, c2, pd0, pd1;
+    double dx, dy, m, a, om, og, bx, c0, c1, c2;
 };
 
 __device__ __forceinline__ void eval_splat(const Rec64 &r, int px, int py, double tau, double clamp,
-                                           double one_minus_clamp, SplatEval<double> &e) {
+                                           double one_minus_clamp, SplatEval &e) {
     e.dx = sub((double)px + 0.5, r.mx);
     e.dy = sub((double)py + 0.5, r.my);
     e.m = add(add(mul(mul(r.p00, e.dx), e.dx), mul(mul(mul(2.0, r.p01), e.dx), e.dy)), mul(mul(r.p11, e.dy), e.dy));
     e.og = r.og; e.bx = r.bx; e.c0 = r.cr; e.c1 = r.cg; e.c2 = r.cb;
-    e.pd0 = r.p00 * e.dx + r.p01 * e.dy;
-    e.pd1 = r.p01 * e.dx + r.p11 * e.dy;
     e.a = (e.m < tau) ? mul(e.og, exp(mul(e.bx, log1p(-e.m / tau)))) : 0.0;
     if (e.a > clamp) e.a = clamp;
     e.om = sub(1.0, e.a);
 }
 
-__device__ __forceinline__ void eval_splat(const Rec32 &r, int px, int py, float tau, float clamp,
-                                           float one_minus_clamp, SplatEval<float> &e) {
-    e.dx = ((float)px - r.r0.x) + r.r0.z;
-    e.dy = ((float)py - r.r0.y) + r.r0.w;
-    const float y0 = fmaf(r.r1.x, e.dx, r.r1.y * e.dy), y1 = r.r1.z * e.dy;
-    e.m = fmaf(y0, y0, y1 * y1);
-    e.og = r.r3.y; e.bx = r.r2.x; e.c0 = r.r2.y; e.c1 = r.r2.z; e.c2 = r.r2.w;
-    e.pd0 = r.r1.x * y0;  // P d = U^T (U d)
-    e.pd1 = fmaf(r.r1.y, y0, r.r1.z * y1);
-    e.a = (e.m < tau) ? ex2_approx(fmaf(e.bx, lg2_approx(1.0f - e.m / tau), r.r3.w)) : 0.f;
-    if (e.a > clamp) {
-        e.a = clamp;
-        e.om = one_minus_clamp;  // same factor the forward multiplied T by
-    } else {
-        e.om = 1.0f - e.a;
-    }
-}
-
 __device__ __forceinline__ double log1p_(double x) { return log1p(x); }
-__device__ __forceinline__ float log1p_(float x) { return 0.69314718f * lg2_approx(1.0f + x); }
 __device__ __forceinline__ double rcp_(double x) { return 1.0 / x; }
-__device__ __forceinline__ float rcp_(float x) { return __frcp_rn(x); }
-
-// Reduce-scatter of 16 per-lane values over the warp in 16 shuffles (instead
-// of 16 x 5 for 16 all-reduces): at each level a lane keeps the half of its
-// vector selected by its lane bit and adds the partner's copy of that half.
-// Returns the full warp sum of component idx(lane), idx = bits 4..1 of lane;
-// lanes 2i and 2i+1 hold component i.
-template <typename T>
-__device__ __forceinline__ T warp_reduce_scatter16(T (&v)[16], int lane, int &idx) {
-#pragma unroll
-    for (int lvl = 0; lvl < 4; ++lvl) {
-        const int half = 8 >> lvl, off = 16 >> lvl;
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < half; ++i) {
-            const T send = upper ? v[i] : v[i + half];
-            const T keep = upper ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-    }
-    idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
 
 // Warp sums of 10 per-lane values v[0..9] in ~44 instructions: components
 // 0..7 by a reduce-scatter over lane bits 4..2 plus two xor levels (lane l
@@ -623,13 +560,12 @@ __device__ __forceinline__ bool warp_reduce10(T (&v)[16], int lane, int &idx, T 
     return false;
 }
 
-template <typename Real>
+// fp64 backward (tile_backward, _tiles.py:59-127) in the reference's operation order
 __global__ void __launch_bounds__(kTileThreads)
-raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
-                  const typename BwdTraits<Real>::Rec *__restrict__ recs, const Real *__restrict__ tstop,
-                  const int32_t *__restrict__ ncontrib, const Real *__restrict__ g_image, Real *__restrict__ grad2d) {
-    using Rec = typename BwdTraits<Real>::Rec;
-    __shared__ Rec srec[kTileThreads];
+raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                  const Rec64 *__restrict__ recs, const double *__restrict__ tstop,
+                  const int32_t *__restrict__ ncontrib, const double *__restrict__ g_image, double *__restrict__ grad2d) {
+    __shared__ Rec64 srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
     __shared__ int smax;
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
@@ -641,7 +577,7 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
     const uint32_t start = ranges[2 * tile];
     const int64_t pix = (int64_t)py * P.W + px;
     int my_cnt = 0;
-    Real T = 0, g0 = 0, g1 = 0, g2 = 0;
+    double T = 0, g0 = 0, g1 = 0, g2 = 0;
     if (threadIdx.x == 0) smax = 0;
     __syncthreads();
     if (inside) {
@@ -657,8 +593,8 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
     int warp_cnt = my_cnt;  // this warp's largest contributor count: splats beyond it are skipped
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) warp_cnt = max(warp_cnt, __shfl_xor_sync(0xffffffffu, warp_cnt, o));
-    const Real tau = (Real)P.tau, clamp = (Real)P.clamp, one_minus_clamp = (Real)(1.0 - P.clamp);
-    Real suffix = (g0 * (Real)P.bg[0] + g1 * (Real)P.bg[1] + g2 * (Real)P.bg[2]) * T;
+    const double tau = (double)P.tau, clamp = (double)P.clamp, one_minus_clamp = (double)(1.0 - P.clamp);
+    double suffix = (g0 * (double)P.bg[0] + g1 * (double)P.bg[1] + g2 * (double)P.bg[2]) * T;
     const int lane = threadIdx.x & 31;
     for (int hi = max_cnt; hi > 0; hi -= kTileThreads) {
         const int lo = hi > kTileThreads ? hi - kTileThreads : 0;
@@ -671,32 +607,32 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
         }
         __syncthreads();
         for (int j = min(hi, warp_cnt) - 1; j >= lo; --j) {
-            Real v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+            double v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             bool contrib = false;
             if (j < my_cnt) {
-                SplatEval<Real> e;
+                SplatEval e;
                 eval_splat(srec[j - lo], px, py, tau, clamp, one_minus_clamp, e);
-                if (e.a != (Real)0) {
+                if (e.a != (double)0) {
                     // _tiles.py:97-127, T_i rebuilt by division from T_final
                     contrib = true;
-                    const Real iom = rcp_(e.om);
-                    const Real ti = T * iom;
-                    const Real w = e.a * ti;
+                    const double iom = rcp_(e.om);
+                    const double ti = T * iom;
+                    const double w = e.a * ti;
                     v[7] = w * g0;
                     v[8] = w * g1;
                     v[9] = w * g2;
-                    const Real gc = g0 * e.c0 + g1 * e.c1 + g2 * e.c2;
-                    const Real ga = gc * ti - suffix * iom;
+                    const double gc = g0 * e.c0 + g1 * e.c1 + g2 * e.c2;
+                    const double ga = gc * ti - suffix * iom;
                     suffix += gc * w;
                     T = ti;
                     if (e.a < clamp) {
                         // raw moments (see raster_bwd32_kernel); prim_bwd applies -2 P,
                         // -beta / tau and 1 / og per primitive
-                        const Real x = e.m / tau;
-                        const Real gaa = ga * e.a;
+                        const double x = e.m / tau;
+                        const double gaa = ga * e.a;
                         v[5] = gaa;
                         v[6] = gaa * log1p_(-x);
-                        const Real h = gaa / ((Real)1 - x);
+                        const double h = gaa / ((double)1 - x);
                         v[0] = h * e.dx;
                         v[1] = h * e.dy;
                         v[2] = h * e.dx * e.dx;
@@ -707,8 +643,8 @@ raster_bwd_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, con
             }
             if (__any_sync(0xffffffffu, contrib)) {
                 int idx = 0;
-                Real mine = 0;
-                if (warp_reduce10(v, lane, idx, mine) && mine != (Real)0)
+                double mine = 0;
+                if (warp_reduce10(v, lane, idx, mine) && mine != (double)0)
                     atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + idx, mine);
             }
         }
@@ -912,7 +848,7 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
     const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
     cudaStream_t s = (cudaStream_t)stream;
     if (ib->raster_f64) {
-        raster_bwd_kernel<double><<<n_tiles, kTileThreads, 0, s>>>(
+        raster_bwd64_kernel<<<n_tiles, kTileThreads, 0, s>>>(
             P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
             (const double *)gb->g_image, (double *)gb->grad2d);
     } else {
