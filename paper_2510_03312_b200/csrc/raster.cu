@@ -354,13 +354,16 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     if (T < tmin_hi) {
                         const float band = err + 1.0e-6f;
                         if (T < tmin) {
-                            // the reference stops before the next splat
+                            // the reference stops before the next splat; ending the walk
+                            // through the loop condition (bits = 0, !done) avoids a
+                            // divergent break
                             flag |= (T > tmin * (1.0f - band));
                             done = true;
                             cnt = b - start + (uint32_t)(32 * k + 31) - p + 1u;
-                            break;
+                            bits = 0u;
+                        } else {
+                            flag |= (T < tmin * (1.0f + band));
                         }
-                        flag |= (T < tmin * (1.0f + band));
                     }
                 }
             }
