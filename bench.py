@@ -282,6 +282,46 @@ def run_train(a, rank, world, local_rank):
             "steps": a.train_steps, "warmup": 2, "dtype": "f32 (fp64 geometry/chain)", "data": "synthetic"}
 
 
+def run_other_configs(a, dev, frames=64):
+    """BASELINE.json configs 1 and 2 on this GPU (informational, single rank):
+    3D static 1M primitives and 6D view-dependent 2M primitives, each a
+    64-view 1080p orbit through a FramePipeline of a.inflight frames."""
+    import torch
+    from paper_2510_03312_b200 import engine, synthetic as S
+    from paper_2510_03312_b200.types import DEFAULT_SETTINGS
+    out = {}
+    for name, nd, n in (("3D static, 1M primitives, 1080p 64-view orbit", 3, 1_000_000),
+                        ("6D view-dependent, 2M primitives, 1080p 64-view orbit", 6, 2_000_000)):
+        ds = engine.DeviceScene.from_scene(S.synth(nd, n, seed=1), device=dev)
+        cams = [S.bench_camera(a.width, a.height, k, frames) for k in range(frames)]
+        qs = [S.bench_query(nd, c) for c in cams]
+        pipe = engine.FramePipeline(ds, max(a.inflight, 1), "fp32", dev)
+        for k in range(2 * pipe.depth):
+            pipe.render(cams[k % frames], qs[k % frames], DEFAULT_SETTINGS, sync=True)
+        ms = None
+        for _ in range(2):  # a second pass if an asynchronous frame outgrew its slot
+            pipe.clear_status()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ds.invalidate_statics()
+            e0.record()
+            for k in range(frames):
+                pipe.render(cams[k], qs[k], DEFAULT_SETTINGS)
+            pipe.join()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if int(pipe.status().item()) == 0:
+                break
+            for k in range(frames):
+                pipe.render(cams[k], qs[k], DEFAULT_SETTINGS, sync=True)
+        out[name] = {"value": frames / (ms / 1e3), "unit": "frames/s", "frames": frames,
+                     "frames_in_flight": pipe.depth}
+        del pipe, ds
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -432,9 +472,12 @@ def run_ours(a, rank, world, local_rank):
                          f"C OpenMP binning + compositing) with {os.cpu_count()} host threads"}
 
     train = None
+    other = None
     if not a.no_train:
-        del ws
+        del ws, pipe
         torch.cuda.empty_cache()
+        if world == 1:
+            other = run_other_configs(a, dev)
         train = run_train(a, rank, world, local_rank)
 
     if rank != 0:
@@ -469,6 +512,7 @@ def run_ours(a, rank, world, local_rank):
         "gpu_launches": per_frame_launches * a.steps + 1,
         "clocks": clocks,
         "train": train,
+        "other_configs": other,
     }
     return out
 
