@@ -159,10 +159,15 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 constexpr float kImgErrTol = 1.0e-3f;
 
 // 16 B shared-memory load at a 32-bit shared address (keeps the splat walk
-// in 32-bit shared offsets instead of generic 64-bit pointers)
+// in 32-bit shared offsets instead of generic 64-bit pointers); the record
+// offset is an immediate, so every field of a record shares one address
+// register
+template <int OFF = 0>
 __device__ __forceinline__ float4 lds128(uint32_t a) {
     float4 v;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(a), "n"(OFF));
     return v;
 }
 
@@ -317,7 +322,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const uint32_t p = msb_pos(bits);
                     bits ^= bit_at(p);
                     const uint32_t ra = stop - (p << 6);
-                    const float4 r0 = lds128(ra), r1 = lds128(ra + 16);
+                    const float4 r0 = lds128<0>(ra), r1 = lds128<16>(ra);
                     const float dx = (pxf - r0.x) + r0.z;
                     const float dy = (pyf - r0.y) + r0.w;
                     const float y0 = fmaf(r1.x, dx, r1.y * dy);
@@ -327,7 +332,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                         edge = fminf(edge, m - r1.w);  // support edge within the m-error band
                         continue;
                     }
-                    const float4 r2 = lds128(ra + 32), r3 = lds128(ra + 48);
+                    const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
                     const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                     float a = ex2_approx(arg);
                     // q = num / d; the T-error term a q / (1 - a) takes one reciprocal
@@ -745,14 +750,14 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 float v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
                 bool contrib = false;
                 if (lo + jj < my_cnt) {
-                    const float4 r0 = lds128(ra), r1 = lds128(ra + 16);
+                    const float4 r0 = lds128<0>(ra), r1 = lds128<16>(ra);
                     const float dx = (pxf - r0.x) + r0.z;
                     const float dy = (pyf - r0.y) + r0.w;
                     const float y0 = fmaf(r1.x, dx, r1.y * dy);
                     const float y1 = r1.z * dy;
                     const float m = fmaf(y0, y0, y1 * y1);
                     if (m < tau) {
-                        const float4 r2 = lds128(ra + 32), r3 = lds128(ra + 48);
+                        const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
                         const float omx = fmaf(-m, inv_tau, 1.0f);  // 1 - x
                         const float L = lg2_approx(omx);
                         float a = ex2_approx(fmaf(r2.x, L, r3.w));  // the forward's alpha
