@@ -414,9 +414,15 @@ __device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const 
     g.raw2[2] = r11;
     {
         double w[2], E[2][2];
-        eigh2(g.raw2[0], g.raw2[1], g.raw2[2], w, E);
-        g.floored2 = w[0] < v.set.screen_cov_floor;
+        // the floor test needs only the smaller eigenvalue (eigh2's own
+        // arithmetic, so the same bits); eigenvectors only for floored splats
+        {
+            const double h = 0.5 * (g.raw2[0] + g.raw2[2]), gg = 0.5 * (g.raw2[0] - g.raw2[2]);
+            const double r = sqrt(gg * gg + g.raw2[1] * g.raw2[1]);
+            g.floored2 = h - r < v.set.screen_cov_floor;
+        }
         if (g.floored2) {
+            eigh2(g.raw2[0], g.raw2[1], g.raw2[2], w, E);
             double f0 = fmax(w[0], v.set.screen_cov_floor), f1 = fmax(w[1], v.set.screen_cov_floor);
             g.cov2[0] = E[0][0] * f0 * E[0][0] + E[0][1] * f1 * E[0][1];
             g.cov2[1] = E[0][0] * f0 * E[1][0] + E[0][1] * f1 * E[1][1];
