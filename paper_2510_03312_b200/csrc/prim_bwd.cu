@@ -82,13 +82,24 @@ prim_active_kernel(const GT *__restrict__ grad2d, const uint16_t *__restrict__ f
         }
         need = nz || add_reg || (flags[i] & UBS_F_GATE_SAT);
     }
+    // one atomic per CTA (a per-warp atomic on the single counter serialises
+    // ~n/32 atomics per view)
+    __shared__ uint32_t wcnt[8], cta_base;
     const unsigned m = __ballot_sync(0xffffffffu, need);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(count, (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (need) active[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wcnt[wid] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const uint32_t c = wcnt[w];
+            wcnt[w] = t;
+            t += c;
+        }
+        cta_base = t ? atomicAdd(count, t) : 0u;
+    }
+    __syncthreads();
+    if (need) active[cta_base + wcnt[wid] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
 template <int C, typename PT, typename GT, typename OT>
