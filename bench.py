@@ -482,11 +482,11 @@ def run_ours(a, rank, world, local_rank):
 
     if rank != 0:
         return None
-    # kernels of libubs_b200.so per frame (ncu launch list, profiles/): preprocess, tile_scan,
-    # depth hist, CUB scan (init + scan), depth scatter, depth rank, bucket hist / segsum /
-    # segscan / start / offsets / scatter, tile_lists, raster, fixup; plus one scene-statics
-    # pass per sweep
-    per_frame_launches = 16
+    # kernels of libubs_b200.so per frame (ncu launch list, profiles/r01_launches_v4.csv):
+    # preprocess, tile_scan, depth hist, CUB scan (init + scan), depth scatter, depth rank,
+    # bucket hist, bucket offsets, bucket scatter, tile_lists, raster, fixup; plus one
+    # scene-statics pass per sweep
+    per_frame_launches = 13
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",

@@ -230,7 +230,8 @@ using namespace ubs;
 extern "C" int ubs_abi_version(void) { return UBS_ABI_VERSION; }
 
 extern "C" const char *ubs_build_info(void) {
-    return "ubs_b200 sm_100a; fp64 preprocess; CUB radix binning; tile-per-CTA raster fp32/fp64";
+    return "ubs_b200 sm_100a; fp64 preprocess (scene statics); depth bucket sort; two-level 8x4-tile binning; "
+           "tile-per-CTA raster fp32 (certified, fp64 fix-up) / fp64";
 }
 
 extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32,
