@@ -672,7 +672,7 @@ raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 // sum w g_rgb) are warp reduce-scattered and added with atomics; prim_bwd turns
 // them into d/d mean2 = -2 (-beta/tau) P sum h d, d/d P = (-beta/tau) sum h d d^T,
 // d/d og = sum / og, d/d beta = sum g_alpha alpha ln(1 - x) (_tiles.py:97-127).
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, 5)
 raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                     const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
