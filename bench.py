@@ -435,9 +435,13 @@ def run_ours(a, rank, world, local_rank):
 
     def submit(k):
         fr = frame(k)
-        # zero-copy: the D2H reads the slot's own image; the slot's next frame waits for it
-        sink.submit(fr, source_stream=pipe.stream_of(fr))
-        pipe.hold(fr, sink.last_copy)
+        if pipe.depth > 1:
+            # zero-copy: the D2H reads the slot's own image; the slot's next frame waits for it
+            sink.submit(fr, source_stream=pipe.stream_of(fr))
+            pipe.hold(fr, sink.last_copy)
+        else:  # one slot: snapshot on the device so the next frame need not wait for the copy
+            with torch.cuda.stream(pipe.stream_of(fr)):
+                sink.submit(fr)
 
     for k in range(2 * pipe.depth):
         submit(k)

@@ -246,9 +246,12 @@ def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=D
                 sink.submit(fr)
         else:
             fr = pipeline.render(cam, query, settings)
-            if sink is not None:
+            if sink is not None and pipeline.depth > 1:
                 sink.submit(fr, source_stream=pipeline.stream_of(fr))
                 pipeline.hold(fr, sink.last_copy)
+            elif sink is not None:
+                with torch.cuda.stream(pipeline.stream_of(fr)):
+                    sink.submit(fr)
         k += 1
     if pipeline is not None:
         pipeline.join()
