@@ -588,41 +588,37 @@ tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restri
         t0 = ranges[2 * tile];
         want = min(cap, ranges[2 * tile + 1] - t0);
     }
-    const int bit = 32 + ly * kBand + lx;  // this tile's bit in the entry mask
+    const uint32_t tmask = 1u << (ly * kBand + lx);  // this tile's bit in the entry mask (high word)
+    uint32_t *dst = out + t0;
     const uint32_t e0 = bstart[k], e1 = bstart[k + 1];
     const unsigned lt = (1u << lane) - 1u;
     uint32_t written = 0;
     for (uint32_t base = e0; base < e1; base += kListRound) {
         if (__syncthreads_count(written < want) == 0) break;
 #pragma unroll
-        for (int r = 0; r < kListRound / kListThreads; ++r) {
+        for (int r = 0; r < kListRound / kListThreads; ++r) {  // zero entries pad the round: mask 0 never matches
             const uint32_t i = base + r * kListThreads + threadIdx.x;
-            if (i < e1) sbuf[r * kListThreads + threadIdx.x] = entries[i];
+            sbuf[r * kListThreads + threadIdx.x] = i < e1 ? entries[i] : 0ull;
         }
         __syncthreads();
         const int m = (int)min((uint32_t)kListRound, e1 - base);
         // 4 x 32 entries per step: independent loads / tests / ballots, then
-        // the ordered appends
+        // the ordered appends (no bounds test: the round is zero-padded)
         for (int j0 = 0; j0 < m && written < want; j0 += 128) {
+            uint32_t idv[4];
             bool p[4];
-            uint32_t id[4];
             unsigned bal[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int j = j0 + 32 * u + lane;
-                p[u] = false;
-                id[u] = 0;
-                if (j < m) {
-                    const uint64_t e = sbuf[j];
-                    p[u] = (e >> bit) & 1ull;
-                    id[u] = (uint32_t)e;
-                }
+                const uint64_t e = sbuf[j0 + 32 * u + lane];
+                idv[u] = (uint32_t)e;
+                p[u] = ((uint32_t)(e >> 32) & tmask) != 0u;
                 bal[u] = __ballot_sync(0xffffffffu, p[u]);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t pos = written + __popc(bal[u] & lt);
-                if (p[u] && pos < want) out[t0 + pos] = id[u];
+                if (p[u] && pos < want) dst[pos] = idv[u];
                 written += __popc(bal[u]);
             }
         }
