@@ -22,7 +22,7 @@ namespace ubs {
 
 // Depth order = lexsort((ids, depth)) (raster.py:274-275) as a bucket sort.
 // key32 = (f64 depth bits - min) >> shift (< 2^31, monotone in depth); its top
-// log2(B) bits pick one of B ~ n/4 buckets.  (1) histogram, (2) exclusive
+// log2(B) bits pick one of B ~ n buckets.  (1) histogram, (2) exclusive
 // scan (CUB), (3) scatter of (f64 bits, id) into bucket slots in arrival
 // order, (4) inside each bucket every element counts the elements that
 // precede it by (f64 bits, id) -- the exact lexsort order, ties by id -- and
@@ -33,7 +33,7 @@ constexpr uint64_t kNoRect = ~0ull;  // rect_sorted entry of a primitive that to
 
 __host__ __device__ inline int sort_log_buckets(int64_t n) {
     int l = 12;
-    while (l < 24 && ((int64_t)4 << l) < n) ++l;
+    while (l < 24 && ((int64_t)1 << l) < n) ++l;
     return l;
 }
 
