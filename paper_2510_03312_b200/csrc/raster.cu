@@ -246,8 +246,9 @@ __device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float
 // the MUFU lg2/ex2 approximations; their error (qc, and 2.1e-7 per unit of
 // the exponent) is part of the per-visit relative alpha bound
 //     q = eb / (tau - m) + qc + 2.1e-7 |arg|,
-// and err accumulates q a / (1 - a) + 2u, the first-order relative error of T.
-// T and err change only on in-support visits, so the reference's cut test
+// and D, the bound on |T32 - T64|, accumulates D (1 - a) + T a q + 2u T: the
+// first-order error of T (D / T = sum a q / (1 - a) + 2u per visit).
+// T and D change only on in-support visits, so the reference's cut test
 // (T < t_min before each splat) and its certification band are evaluated
 // right after each update: the next splat is iterated iff T >= t_min, exactly
 // as in tile_forward.  Each warp walks only the splats whose cover mask has
@@ -278,13 +279,13 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
     const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
     // alpha below clamp_lo cannot be clamp-ambiguous unless its error bound is
-    // so large that err > kImgErrTol flags the pixel anyway: a(1+q) > clamp
+    // so large that D > kImgErrTol T flags the pixel anyway: a(1+q) > clamp
     // with a < clamp_lo implies a q / (1 - a) > clamp - clamp_lo >> kImgErrTol
     const float clamp_lo = clamp - 0.05f;
     const float tmin = (float)P.tmin;
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
     float T = 1.0f, a0 = 0.f, a1 = 0.f, a2 = 0.f;
-    float err = 0.f;  // bound on |T32 - T64| / T
+    float D = 0.f;  // bound on |T32 - T64|
     uint32_t cnt = inside ? end - start : 0u;
     int flag = 0;
     float edge = 1.0f;  // min over out-of-support visits of m - (tau + E): < 0 flags the pixel
@@ -335,12 +336,10 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
                     const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                     float a = ex2_approx(arg);
-                    // q = num / d; the T-error term a q / (1 - a) takes one reciprocal
-                    const float d = tau - m;
-                    const float num = fmaf(fmaf(fabsf(arg), 2.1e-7f, r3.z), d, r3.x);
+                    // relative alpha bound q = eb / (tau - m) + qc + 2.1e-7 |arg|
+                    const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
                     float om = 1.0f - a;
                     if (a > clamp_lo) {
-                        const float qrel = num * rcp_approx(d);
                         if (a > clamp) {
                             if (a * (1.0f - qrel) > clamp) hit[sid[32 * k + 31 - (int)p]] = 1;
                             else flag = 1;
@@ -350,24 +349,26 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                             flag |= (a * (1.0f + qrel) > clamp);
                         }
                     }
-                    err = fmaf(a * num, rcp_approx(d * om), err + 1.2e-7f);  // + rounding of 1 - a and of T * om
                     const float w = a * T;
                     a0 = fmaf(w, r2.y, a0);
                     a1 = fmaf(w, r2.z, a1);
                     a2 = fmaf(w, r2.w, a2);
+                    // D' = D (1 - a) + T a q + rounding of 1 - a and of T (1 - a)
+                    D = fmaf(D, om, w * qrel);
                     T *= om;
+                    D = fmaf(1.2e-7f, T, D);
                     if (T < tmin_hi) {
-                        const float band = err + 1.0e-6f;
+                        const float slack = fmaf(1.0e-6f, tmin, D);
                         if (T < tmin) {
                             // the reference stops before the next splat; ending the walk
                             // through the loop condition (bits = 0, !done) avoids a
                             // divergent break
-                            flag |= (T > tmin * (1.0f - band));
+                            flag |= (T > tmin - slack);
                             done = true;
                             cnt = b - start + (uint32_t)(32 * k + 31) - p + 1u;
                             bits = 0u;
                         } else {
-                            flag |= (T < tmin * (1.0f + band));
+                            flag |= (T < tmin + slack);
                         }
                     }
                 }
@@ -375,7 +376,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         }
     }
     if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
-    if (err > kImgErrTol || edge < 0.0f) flag = 1;
+    if (D > kImgErrTol * T || edge < 0.0f) flag = 1;
     if (inside) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
