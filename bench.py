@@ -502,7 +502,7 @@ def run_ours(a, rank, world, local_rank):
         "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": b_dom, "launch_ms": stage_ms[dominant]},
-        "issue_roofline": ncu_issue(dominant),
+        "issue_roofline": ncu_issue(dominant) if a.precision == "fp32" else None,
         "frame_roofline": {"bytes_per_frame": b_frame, "achieved_gbs": b_frame / (ms_max / a.steps / 1e3) / 1e9,
                            "frac": b_frame / (ms_max / a.steps / 1e3) / 1e9 / peak,
                            "ceiling_fps": peak * 1e9 / b_frame},

@@ -74,80 +74,6 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long x
 }
 
 // ---------------------------------------------------------------------------
-// forward, fp64 (bit-faithful to tile_forward)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads)
-raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
-                    const Rec64 *__restrict__ recs, double *__restrict__ image, double *__restrict__ asum,
-                    double *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
-                    unsigned long long *__restrict__ visits) {
-    __shared__ Rec64 srec[kTileThreads];
-    __shared__ uint32_t sid[kTileThreads];
-    __shared__ unsigned long long red[kTileThreads / 32];
-    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
-    const int tile = blockIdx.x;
-    const int ty = tile / P.TX, tx = tile - ty * P.TX;
-    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty * kTile + (threadIdx.x >> 4);
-    const bool inside = px < P.W && py < P.H;
-    uint32_t start, end;
-    bool capped;
-    tile_span(P, ranges, tile, start, end, capped);
-    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
-    const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
-    double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
-    int cnt = 0;
-    bool done = !inside;
-    for (uint32_t b = start; b < end; b += kTileThreads) {
-        if (__syncthreads_count(done) == kTileThreads) break;
-        const uint32_t q = b + threadIdx.x;
-        if (q < end) {
-            const uint32_t id = ids[q];
-            sid[threadIdx.x] = id;
-            srec[threadIdx.x] = recs[id];
-        }
-        __syncthreads();
-        const int nb = (int)min((uint32_t)kTileThreads, end - b);
-        if (!done) {
-            for (int j = 0; j < nb; ++j) {
-                if (T < tmin) { done = true; break; }
-                ++cnt;
-                const Rec64 &r = srec[j];
-                const double dx = sub(pxc, r.mx), dy = sub(pyc, r.my);
-                const double m = add(add(mul(mul(r.p00, dx), dx), mul(mul(mul(2.0, r.p01), dx), dy)),
-                                     mul(mul(r.p11, dy), dy));
-                if (m >= tau) continue;
-                double a = mul(r.og, exp(mul(r.bx, log1p(-m / tau))));
-                if (a > clamp) {
-                    a = clamp;
-                    hit[sid[j]] = 1;
-                }
-                const double w = mul(a, T);
-                a0 = add(a0, mul(w, r.cr));
-                a1 = add(a1, mul(w, r.cg));
-                a2 = add(a2, mul(w, r.cb));
-                ws = add(ws, w);
-                T = mul(T, sub(1.0, a));
-            }
-            done = done || (T < tmin);
-        }
-    }
-    if (capped && inside && !(T < tmin)) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
-    if (inside) {
-        const int64_t pix = (int64_t)py * P.W + px;
-        image[3 * pix] = add(a0, mul(T, P.bg[0]));
-        image[3 * pix + 1] = add(a1, mul(T, P.bg[1]));
-        image[3 * pix + 2] = add(a2, mul(T, P.bg[2]));
-        asum[pix] = ws;
-        tstop[pix] = T;
-        ncontrib[pix] = cnt;
-    }
-    __syncthreads();
-    const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
-    if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
-}
-
-// ---------------------------------------------------------------------------
 // forward, fp32 with certified fall-back to fp64
 // ---------------------------------------------------------------------------
 // Linear worst-case bound on the relative transmittance error above which a
@@ -393,6 +319,116 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (fl) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
+    }
+    __syncthreads();
+    const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
+    if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
+}
+
+// ---------------------------------------------------------------------------
+// forward, fp64 (bit-faithful to tile_forward)
+// ---------------------------------------------------------------------------
+// The reference's per-pixel loop in its operation order (no FMA contraction),
+// on the fp32 kernel's 8x4-pixel warps: each warp walks only the splats whose
+// cover mask has its bit.  The masks come from each record's fp64 conic
+// rounded to the fp32 factor form with a 1e-3 relative margin on tau (far
+// above that rounding), so a culled splat is one every pixel of the warp
+// evaluates to m >= tau in fp64 anyway; the contributor count is the list
+// position where T first fell below t_min (tile_forward counts every iterated
+// splat), exactly as in the fp32 kernel.
+__device__ __forceinline__ uint32_t warp_cover_mask64(const Rec64 &r, float tau, int tx, int ty) {
+    if (!(fabs(r.mx) < 4.0e6 && fabs(r.my) < 4.0e6) || !(r.p00 > 0.0)) return 0xffu;
+    const double fx = floor(r.mx), fy = floor(r.my);
+    const double u00 = sqrt(r.p00), u01 = r.p01 / u00;
+    const double u11 = sqrt(fmax(r.p11 - u01 * u01, 0.0));
+    const float4 r0 = make_float4((float)fx, (float)fy, (float)(0.5 - (r.mx - fx)), (float)(0.5 - (r.my - fy)));
+    const float4 r1 = make_float4((float)u00, (float)u01, (float)u11, tau * 1.001f);
+    return warp_cover_mask(r0, r1, tx, ty);
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                    const Rec64 *__restrict__ recs, double *__restrict__ image, double *__restrict__ asum,
+                    double *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
+                    unsigned long long *__restrict__ visits) {
+    constexpr int kWarps = kTileThreads / 32;
+    __shared__ Rec64 srec[kTileThreads];
+    __shared__ uint32_t sid[kTileThreads];
+    __shared__ uint32_t swm[kWarps][kWarps];
+    __shared__ unsigned long long red[kWarps];
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = px < P.W && py < P.H;
+    uint32_t start, end;
+    bool capped;
+    tile_span(P, ranges, tile, start, end, capped);
+    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+    const double tau = P.tau, clamp = P.clamp, tmin = P.tmin;
+    double T = 1.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
+    uint32_t cnt = inside ? end - start : 0u;
+    bool done = !inside;
+    for (uint32_t b = start; b < end; b += kTileThreads) {
+        if (__syncthreads_count(done) == kTileThreads) break;
+        const uint32_t q = b + threadIdx.x;
+        uint32_t cover = 0;
+        if (q < end) {
+            const uint32_t id = ids[q];
+            sid[threadIdx.x] = id;
+            const Rec64 r = recs[id];
+            srec[threadIdx.x] = r;
+            cover = warp_cover_mask64(r, (float)tau, tx, ty);
+        }
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
+            if (lane == 0) swm[w][warp] = word;
+        }
+        __syncthreads();
+        if (!done) {
+            const int nw = (int)((min((uint32_t)kTileThreads, end - b) + 31u) >> 5);
+            for (int k = 0; k < nw && !done; ++k) {
+                uint32_t bits = swm[warp][k];
+                while (bits) {
+                    const int j = (k << 5) + __ffs(bits) - 1;  // ascending list order
+                    bits &= bits - 1u;
+                    const Rec64 &r = srec[j];
+                    const double dx = sub(pxc, r.mx), dy = sub(pyc, r.my);
+                    const double m = add(add(mul(mul(r.p00, dx), dx), mul(mul(mul(2.0, r.p01), dx), dy)),
+                                         mul(mul(r.p11, dy), dy));
+                    if (m >= tau) continue;
+                    double a = mul(r.og, exp(mul(r.bx, log1p(-m / tau))));
+                    if (a > clamp) {
+                        a = clamp;
+                        hit[sid[j]] = 1;
+                    }
+                    const double w = mul(a, T);
+                    a0 = add(a0, mul(w, r.cr));
+                    a1 = add(a1, mul(w, r.cg));
+                    a2 = add(a2, mul(w, r.cb));
+                    ws = add(ws, w);
+                    T = mul(T, sub(1.0, a));
+                    if (T < tmin) {  // the reference stops before the next splat
+                        done = true;
+                        cnt = b - start + (uint32_t)j + 1u;
+                        bits = 0u;
+                    }
+                }
+            }
+        }
+    }
+    if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
+    if (inside) {
+        const int64_t pix = (int64_t)py * P.W + px;
+        image[3 * pix] = add(a0, mul(T, P.bg[0]));
+        image[3 * pix + 1] = add(a1, mul(T, P.bg[1]));
+        image[3 * pix + 2] = add(a2, mul(T, P.bg[2]));
+        asum[pix] = ws;
+        tstop[pix] = T;
+        ncontrib[pix] = (int32_t)cnt;
     }
     __syncthreads();
     const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
