@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--train-views-per-gpu", type=int, default=8)
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-inflight", type=int, default=3, help="views in flight per GPU in the training step")
+    ap.add_argument("--train-only", action="store_true",
+                    help="only the config-5 training step (its own JSON line; for profiling)")
     return ap.parse_args()
 
 
@@ -537,7 +539,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_ours(a, rank, world, local_rank)
+    res = run_train(a, rank, world, local_rank) if a.train_only else run_ours(a, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -774,14 +774,14 @@ __device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float4 r0, const fl
 }
 
 template <int NP>
-__global__ void __launch_bounds__(kTileThreads / NP)
+__global__ void __launch_bounds__(kTileThreads / NP, 8)  // 64 registers: 8 CTAs per SM
 raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                     const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
                     float *__restrict__ grad2d) {
     constexpr int kThreads = kTileThreads / NP;
     constexpr int kWarps = kThreads / 32;
-    constexpr int kBatch = 128;
+    constexpr int kBatch = 256;  // 2 records per thread: half the barriers of a 128 batch
     constexpr int kWords = kBatch / 32;
     constexpr int kBlocks = kTileThreads / 32;  // the forward's 8x4 blocks per tile
     __shared__ Rec32 srec[kBatch];
