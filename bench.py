@@ -465,6 +465,19 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * a.steps / (float(te.item()) / 1e3)
+    # the link's own ceiling: back-to-back device -> pinned host copies of one frame's image
+    src = torch.empty(sink.bytes_per_frame, dtype=torch.uint8, device=dev)
+    dst = torch.empty(sink.bytes_per_frame, dtype=torch.uint8, pin_memory=True)
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0.record()
+    for _ in range(20):
+        dst.copy_(src, non_blocking=True)
+    l1.record()
+    torch.cuda.synchronize()
+    d2h_gbs = 20 * sink.bytes_per_frame / (l0.elapsed_time(l1) / 1e3) / 1e9
+    del src, dst
     import ctypes
     from paper_2510_03312_b200._lib import UbsView
     h2d = ctypes.sizeof(UbsView)  # camera + query + settings travel as kernel parameters
@@ -514,7 +527,8 @@ def run_ours(a, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": sink.bytes_per_frame,
-                "path": "engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, copy stream)"},
+                "path": "engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, copy stream)",
+                "d2h_link_gbs": d2h_gbs, "link_ceiling_fps": d2h_gbs * 1e9 / sink.bytes_per_frame},
         "gpu_launches": per_frame_launches * a.steps + 1,
         "clocks": clocks,
         "train": train,

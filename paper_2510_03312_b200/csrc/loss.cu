@@ -206,31 +206,47 @@ __global__ void ssim_hadj_combine_kernel(const T *__restrict__ a, const T *__res
 // ---------------------------------------------------------------------------
 // Tiled path (both sides >= 12): two kernels over kSsimTW x kSsimTH pixel
 // tiles, all three channels, the blurs in shared memory.
-//   fwd: horizontal blur of (a, b, a^2, b^2, ab) over the tile's halo rows
-//        (reflected loads: exactly the padded blur), vertical blur from shared
-//        memory, SSIM map and its pointwise adjoint -> g3 (3 maps) + sums;
+//   fwd: a, b over the tile's halo (reflected loads: exactly the padded
+//        image); horizontal blur of (a, b, a^2, b^2, ab), each thread a run
+//        of kSsimHPx outputs from one register window of source pixels;
+//        vertical blur, each thread kSsimVRows outputs of one column from a
+//        streamed window of rows; SSIM map and its pointwise adjoint -> g3
+//        (3 maps) + the L1 / SSIM sums;
 //   adj: g3 over the tile's halo (zero outside the image), vertical then
-//        horizontal transpose blur in shared memory, combine with a, b.
-// For n >= 12 every source of output j's adjoint lies in [j-5, j+5] (the
-// reflections p = -j and p = 2n-2-j only reach j < 6 / j > n-8): interior
-// outputs take the plain taps k[j - r + 5], the 12 border ones fold the
-// reflected taps, sum_t k[t] [reflect(r - 5 + t) == j].
+//        horizontal transpose blur (the same register windows), combine with
+//        a, b.
+// Every output sums its taps in ascending tap order, as the per-output loops
+// of the small-image path do.  For n >= 12 every source of output j's adjoint
+// lies in [j-5, j+5] (the reflections p = -j and p = 2n-2-j only reach j < 6 /
+// j > n-8): interior outputs take the plain taps k[j - r + 5], the 12 border
+// ones fold the reflected taps, sum_t k[t] [reflect(r - 5 + t) == j].
 constexpr int kSsimTW = 32, kSsimTH = 16, kSsimR = 5;
 constexpr int kSsimCols = kSsimTW * 3;                  // floats per tile row
 constexpr int kSsimHaloCols = kSsimCols + 6 * kSsimR;   // + 5 px each side
 constexpr int kSsimHaloRows = kSsimTH + 2 * kSsimR;
+constexpr int kSsimThreads = 256;
+constexpr int kSsimHPx = 4;    // horizontal-blur outputs per thread (forward)
+constexpr int kSsimVRows = 8;  // vertical-blur outputs per thread; also the adjoint's horizontal run
+static_assert(kSsimTH % kSsimVRows == 0 && kSsimTW % kSsimHPx == 0 && kSsimTW % kSsimVRows == 0, "tile");
 
+// reflect() for the halo of an n >= 12 axis: i in [-5, n + 4]
+__device__ __forceinline__ int reflect_near(int i, int n) { return i < 0 ? -i : (i >= n ? 2 * n - 2 - i : i); }
+
+// sum_t k[t] [reflect(r - 5 + t) == j] for n >= 12 and |j - r| <= 5: the
+// padded position p = r - 5 + t lies in [j - 10, j + 10], where reflect() is
+// one mirror at most, so p is j itself, -j (j >= 1) or 2n - 2 - j (j <= n - 2)
 template <typename T>
-__device__ __forceinline__ T fold_weight(const BlurTaps &w, int j, int r, int n) {
+__device__ __forceinline__ T fold_weight(const T *__restrict__ sk, int j, int r, int n) {
     T s = 0;
-#pragma unroll
-    for (int t = 0; t < 11; ++t)
-        if (reflect_idx(r - kSsimR + t, n) == j) s += (T)w.k[t];
+    const int td = j - r + kSsimR, tl = -j - r + kSsimR, th = 2 * n - 2 - j - r + kSsimR;
+    if (td >= 0 && td <= 10) s += sk[td];
+    if (j >= 1 && tl >= 0 && tl <= 10) s += sk[tl];
+    if (j <= n - 2 && th >= 0 && th <= 10) s += sk[th];
     return s;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSsimThreads)
 ssim_fwd_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, int H, int W, BlurTaps w,
                      T *__restrict__ g3, double *__restrict__ sums) {
     extern __shared__ __align__(16) unsigned char ssim_smem[];
@@ -239,13 +255,19 @@ ssim_fwd_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, int H, in
         ssim_smem + sizeof(T) * 5 * kSsimHaloRows * kSsimCols);
     const int x0 = blockIdx.x * kSsimTW, y0 = blockIdx.y * kSsimTH;
     const int64_t rs = (int64_t)W * 3;
+    T k[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) k[t] = (T)w.k[t];
     // a, b over the halo with reflected rows and columns: the padded image
-    for (int e = threadIdx.x; e < kSsimHaloRows * kSsimHaloCols; e += blockDim.x) {
+    // (rows / columns past n + 4 feed no output inside the image: zero)
+#pragma unroll 4  // several halo loads in flight per thread
+    for (int e = threadIdx.x; e < kSsimHaloRows * kSsimHaloCols; e += kSsimThreads) {
         const int yy = e / kSsimHaloCols, hc = e - yy * kSsimHaloCols;
-        const int px = x0 - kSsimR + hc / 3, c = hc % 3;
+        const int hp = hc / 3, c = hc - 3 * hp;
+        const int px = x0 - kSsimR + hp, py = y0 - kSsimR + yy;
         T av = 0, bv = 0;
-        if (px < W + kSsimR) {
-            const int64_t q = (int64_t)reflect_idx(y0 - kSsimR + yy, H) * rs + (int64_t)reflect_idx(px, W) * 3 + c;
+        if (px < W + kSsimR && py < H + kSsimR) {
+            const int64_t q = (int64_t)reflect_near(py, H) * rs + (int64_t)reflect_near(px, W) * 3 + c;
             av = a[q];
             bv = b[q];
         }
@@ -253,80 +275,110 @@ ssim_fwd_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, int H, in
         sab[1][yy][hc] = bv;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < kSsimHaloRows * kSsimCols; e += blockDim.x) {
-        const int yy = e / kSsimCols, cc = e - yy * kSsimCols;
-        const int x = x0 + cc / 3;
-        T s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
-        if (x < W) {
+    // horizontal blur: item = (halo row, run of kSsimHPx pixels, channel)
+    constexpr int kRuns = kSsimTW / kSsimHPx;
+    for (int it = threadIdx.x; it < kSsimHaloRows * kRuns * 3; it += kSsimThreads) {
+        const int yy = it / (kRuns * 3), rem = it - yy * (kRuns * 3);
+        const int g = rem / 3, c = rem - 3 * g;
+        const int p0 = g * kSsimHPx;  // first output pixel of the run (tile-relative)
+        if (x0 + p0 >= W) continue;
+        T acc[kSsimHPx][5];
 #pragma unroll
-            for (int t = 0; t < 11; ++t) {  // padded column x - 5 + t at halo column cc + 3 t
-                const T av = sab[0][yy][cc + 3 * t], bv = sab[1][yy][cc + 3 * t], k = (T)w.k[t];
-                s0 += k * av;
-                s1 += k * bv;
-                s2 += k * (av * av);
-                s3 += k * (bv * bv);
-                s4 += k * (av * bv);
+        for (int o = 0; o < kSsimHPx; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[o][q] = 0;
+#pragma unroll
+        for (int i = 0; i < kSsimHPx + 10; ++i) {  // halo pixel p0 + i = padded column x - 5 + t, t = i - o
+            const T av = sab[0][yy][(p0 + i) * 3 + c], bv = sab[1][yy][(p0 + i) * 3 + c];
+            const T aa = av * av, bb = bv * bv, ab = av * bv;
+#pragma unroll
+            for (int o = 0; o < kSsimHPx; ++o) {
+                const int t = i - o;
+                if (t >= 0 && t <= 10) {
+                    acc[o][0] += k[t] * av;
+                    acc[o][1] += k[t] * bv;
+                    acc[o][2] += k[t] * aa;
+                    acc[o][3] += k[t] * bb;
+                    acc[o][4] += k[t] * ab;
+                }
             }
         }
-        h5[0][yy][cc] = s0;
-        h5[1][yy][cc] = s1;
-        h5[2][yy][cc] = s2;
-        h5[3][yy][cc] = s3;
-        h5[4][yy][cc] = s4;
+#pragma unroll
+        for (int o = 0; o < kSsimHPx; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) h5[q][yy][(p0 + o) * 3 + c] = acc[o][q];
     }
     __syncthreads();
+    // vertical blur + SSIM: item = (column, run of kSsimVRows rows)
     const int64_t N = (int64_t)H * W * 3;
+    const T g = (T)(1.0 / (double)N);
+    const T C1 = (T)(0.01 * 0.01), C2 = (T)(0.03 * 0.03);
     double l1 = 0.0, sm = 0.0;
-    for (int e = threadIdx.x; e < kSsimTH * kSsimCols; e += blockDim.x) {
-        const int ty = e / kSsimCols, cc = e - ty * kSsimCols;
-        const int y = y0 + ty, x = x0 + cc / 3;
-        if (y >= H || x >= W) continue;
-        T m[5];
+    for (int it = threadIdx.x; it < kSsimCols * (kSsimTH / kSsimVRows); it += kSsimThreads) {
+        const int rg = it / kSsimCols, cc = it - rg * kSsimCols;
+        const int x = x0 + cc / 3, ty0 = rg * kSsimVRows;
+        if (x >= W || y0 + ty0 >= H) continue;
+        T acc[kSsimVRows][5];
 #pragma unroll
-        for (int qd = 0; qd < 5; ++qd) {
-            T s = 0;
+        for (int o = 0; o < kSsimVRows; ++o)
 #pragma unroll
-            for (int t = 0; t < 11; ++t) s += (T)w.k[t] * h5[qd][ty + t][cc];
-            m[qd] = s;
+            for (int q = 0; q < 5; ++q) acc[o][q] = 0;
+#pragma unroll
+        for (int i = 0; i < kSsimVRows + 10; ++i) {  // halo row ty0 + i, tap t = i - o
+            T hv[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) hv[q] = h5[q][ty0 + i][cc];
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                const int t = i - o;
+                if (t >= 0 && t <= 10)
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) acc[o][q] += k[t] * hv[q];
+            }
         }
-        const T C1 = (T)(0.01 * 0.01), C2 = (T)(0.03 * 0.03);
-        const T mu_a = m[0], mu_b = m[1];
-        const T va = m[2] - mu_a * mu_a, vb = m[3] - mu_b * mu_b, cab = m[4] - mu_a * mu_b;
-        const T n1 = (T)2 * mu_a * mu_b + C1, n2 = (T)2 * cab + C2;
-        const T d1 = mu_a * mu_a + mu_b * mu_b + C1, d2 = va + vb + C2;
-        const T den = d1 * d2;
-        const T sv = n1 * n2 / den;
-        const T g = (T)(1.0 / (double)N);
-        const T g_n1 = g * n2 / den, g_n2 = g * n1 / den;
-        const T g_den = -g * sv / den;
-        const T g_d1 = g_den * d2, g_d2 = g_den * d1;
-        const T g_cab = (T)2 * g_n2;
-        const T g_mu_a = (T)2 * mu_b * g_n1 + (T)2 * mu_a * g_d1 - (T)2 * mu_a * g_d2 - mu_b * g_cab;
-        const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
-        g3[idx] = g_mu_a;
-        g3[N + idx] = g_d2;       // g_E[a^2]
-        g3[2 * N + idx] = g_cab;  // g_E[ab]
-        sm += (double)sv;
-        l1 += fabs((double)a[idx] - (double)b[idx]);
+#pragma unroll
+        for (int o = 0; o < kSsimVRows; ++o) {
+            const int y = y0 + ty0 + o;
+            if (y >= H) break;
+            const T mu_a = acc[o][0], mu_b = acc[o][1];
+            const T va = acc[o][2] - mu_a * mu_a, vb = acc[o][3] - mu_b * mu_b, cab = acc[o][4] - mu_a * mu_b;
+            const T n1 = (T)2 * mu_a * mu_b + C1, n2 = (T)2 * cab + C2;
+            const T d1 = mu_a * mu_a + mu_b * mu_b + C1, d2 = va + vb + C2;
+            const T den = d1 * d2;
+            const T inv = (T)1 / den;
+            const T sv = n1 * n2 * inv;
+            const T g_n1 = g * n2 * inv, g_n2 = g * n1 * inv;
+            const T g_den = -g * sv * inv;
+            const T g_d1 = g_den * d2, g_d2 = g_den * d1;
+            const T g_cab = (T)2 * g_n2;
+            const T g_mu_a = (T)2 * mu_b * g_n1 + (T)2 * mu_a * g_d1 - (T)2 * mu_a * g_d2 - mu_b * g_cab;
+            const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
+            g3[idx] = g_mu_a;
+            g3[N + idx] = g_d2;       // g_E[a^2]
+            g3[2 * N + idx] = g_cab;  // g_E[ab]
+            sm += (double)sv;
+            const T av = sab[0][ty0 + o + kSsimR][cc + 3 * kSsimR], bv = sab[1][ty0 + o + kSsimR][cc + 3 * kSsimR];
+            l1 += fabs((double)av - (double)bv);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         sm += __shfl_xor_sync(0xffffffffu, sm, o);
     }
-    __shared__ double red[2][8];
+    __shared__ double red[2][kSsimThreads / 32];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) { red[0][wid] = l1; red[1][wid] = sm; }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t0 = 0.0, t1 = 0.0;
-        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t0 += red[0][k]; t1 += red[1][k]; }
+        for (int q = 0; q < kSsimThreads / 32; ++q) { t0 += red[0][q]; t1 += red[1][q]; }
         atomicAdd(sums, t0);
         atomicAdd(sums + 1, t1);
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSsimThreads)
 ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *__restrict__ g3, int H, int W,
                      BlurTaps w, double lambda_ssim, double scale, T *__restrict__ g_image) {
     extern __shared__ __align__(16) unsigned char ssim_smem[];
@@ -335,8 +387,16 @@ ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *
         ssim_smem + sizeof(T) * 3 * kSsimHaloRows * kSsimHaloCols);
     const int x0 = blockIdx.x * kSsimTW, y0 = blockIdx.y * kSsimTH;
     const int64_t rs = (int64_t)W * 3, N = (int64_t)H * W * 3;
+    __shared__ T sk[11];  // the taps, for the border folds' dynamic indexing
+    T k[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) k[t] = (T)w.k[t];
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int t = 0; t < 11; ++t) sk[t] = k[t];
     // g3 over rows y0-5 .. y0+TH+5 and columns (x0-5)*3 .. (x0+TW+5)*3, zero outside
-    for (int e = threadIdx.x; e < kSsimHaloRows * kSsimHaloCols; e += blockDim.x) {
+#pragma unroll 4  // several halo loads in flight per thread
+    for (int e = threadIdx.x; e < kSsimHaloRows * kSsimHaloCols; e += kSsimThreads) {
         const int yy = e / kSsimHaloCols, hc = e - yy * kSsimHaloCols;
         const int y = y0 - kSsimR + yy, xf = x0 * 3 - 3 * kSsimR + hc;  // float column
         T v0 = 0, v1 = 0, v2 = 0;
@@ -351,69 +411,129 @@ ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *
         gs[2][yy][hc] = v2;
     }
     __syncthreads();
-    // vertical transpose blur for the tile's rows, all halo columns
-    for (int e = threadIdx.x; e < kSsimTH * kSsimHaloCols; e += blockDim.x) {
-        const int ty = e / kSsimHaloCols, hc = e - ty * kSsimHaloCols;
-        const int y = y0 + ty;
-        T s0 = 0, s1 = 0, s2 = 0;
-        if (y < H) {
-            if (y >= 6 && y + 7 < H) {
+    // vertical transpose blur: item = (halo column, run of kSsimVRows rows)
+    for (int it = threadIdx.x; it < kSsimHaloCols * (kSsimTH / kSsimVRows); it += kSsimThreads) {
+        const int rg = it / kSsimHaloCols, hc = it - rg * kSsimHaloCols;
+        const int ty0 = rg * kSsimVRows, yb = y0 + ty0;
+        if (yb >= 6 && yb + kSsimVRows - 1 + 7 < H) {
+            T acc[kSsimVRows][3];
 #pragma unroll
-                for (int t = 0; t < 11; ++t) {  // source row r = y + 5 - t, at yy = ty + 10 - t
-                    const T k = (T)w.k[t];
-                    s0 += k * gs[0][ty + 10 - t][hc];
-                    s1 += k * gs[1][ty + 10 - t][hc];
-                    s2 += k * gs[2][ty + 10 - t][hc];
-                }
-            } else {
-                for (int d = -kSsimR; d <= kSsimR; ++d) {
-                    const int r = y + d;
-                    if (r < 0 || r >= H) continue;
-                    const T k = fold_weight<T>(w, y, r, H);
-                    s0 += k * gs[0][ty + kSsimR + d][hc];
-                    s1 += k * gs[1][ty + kSsimR + d][hc];
-                    s2 += k * gs[2][ty + kSsimR + d][hc];
+            for (int o = 0; o < kSsimVRows; ++o) acc[o][0] = acc[o][1] = acc[o][2] = 0;
+            // output row ty0 + o takes source halo row ty0 + i with tap t = 10 - (i - o);
+            // descending i walks every output's taps in ascending order
+#pragma unroll
+            for (int i = kSsimVRows + 9; i >= 0; --i) {
+                const T s0 = gs[0][ty0 + i][hc], s1 = gs[1][ty0 + i][hc], s2 = gs[2][ty0 + i][hc];
+#pragma unroll
+                for (int o = 0; o < kSsimVRows; ++o) {
+                    const int t = 10 - (i - o);
+                    if (t >= 0 && t <= 10) {
+                        acc[o][0] += k[t] * s0;
+                        acc[o][1] += k[t] * s1;
+                        acc[o][2] += k[t] * s2;
+                    }
                 }
             }
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                vs[0][ty0 + o][hc] = acc[o][0];
+                vs[1][ty0 + o][hc] = acc[o][1];
+                vs[2][ty0 + o][hc] = acc[o][2];
+            }
+        } else {
+            for (int o = 0; o < kSsimVRows; ++o) {  // border rows: folded reflected taps
+                const int y = yb + o;
+                T s0 = 0, s1 = 0, s2 = 0;
+                if (y < H) {
+                    for (int d = -kSsimR; d <= kSsimR; ++d) {
+                        const int r = y + d;
+                        if (r < 0 || r >= H) continue;
+                        const T kw = fold_weight<T>(sk, y, r, H);
+                        const int yy = ty0 + o + kSsimR + d;
+                        s0 += kw * gs[0][yy][hc];
+                        s1 += kw * gs[1][yy][hc];
+                        s2 += kw * gs[2][yy][hc];
+                    }
+                }
+                vs[0][ty0 + o][hc] = s0;
+                vs[1][ty0 + o][hc] = s1;
+                vs[2][ty0 + o][hc] = s2;
+            }
         }
-        vs[0][ty][hc] = s0;
-        vs[1][ty][hc] = s1;
-        vs[2][ty][hc] = s2;
     }
     __syncthreads();
-    // horizontal transpose blur + combine (gradients.py:110-116)
-    for (int e = threadIdx.x; e < kSsimTH * kSsimCols; e += blockDim.x) {
+    // horizontal transpose blur: item = (row, run of kSsimVRows pixels, channel);
+    // the three sums go to shared memory (over the g3 halo, dead since the
+    // vertical pass's barrier) so the combine
+    // below reads a, b and writes the gradient coalesced
+    T(*adj)[kSsimTH][kSsimCols] = reinterpret_cast<T(*)[kSsimTH][kSsimCols]>(ssim_smem);
+    constexpr int kRuns = kSsimTW / kSsimVRows;
+    for (int it = threadIdx.x; it < kSsimTH * kRuns * 3; it += kSsimThreads) {
+        const int ty = it / (kRuns * 3), rem = it - ty * (kRuns * 3);
+        const int g = rem / 3, c = rem - 3 * g;
+        const int p0 = g * kSsimVRows, xb = x0 + p0, y = y0 + ty;
+        if (y >= H || xb >= W) continue;
+        T hacc[kSsimVRows][3];
+        if (xb >= 6 && xb + kSsimVRows - 1 + 7 < W) {
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) hacc[o][0] = hacc[o][1] = hacc[o][2] = 0;
+            // output pixel p0 + o takes halo pixel p0 + i with tap t = 10 - (i - o)
+#pragma unroll
+            for (int i = kSsimVRows + 9; i >= 0; --i) {
+                const int hc = (p0 + i) * 3 + c;
+                const T s0 = vs[0][ty][hc], s1 = vs[1][ty][hc], s2 = vs[2][ty][hc];
+#pragma unroll
+                for (int o = 0; o < kSsimVRows; ++o) {
+                    const int t = 10 - (i - o);
+                    if (t >= 0 && t <= 10) {
+                        hacc[o][0] += k[t] * s0;
+                        hacc[o][1] += k[t] * s1;
+                        hacc[o][2] += k[t] * s2;
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {  // border columns: folded reflected taps
+                const int x = xb + o;
+                T s0 = 0, s1 = 0, s2 = 0;
+                if (x < W) {
+                    for (int d = -kSsimR; d <= kSsimR; ++d) {
+                        const int r = x + d;
+                        if (r < 0 || r >= W) continue;
+                        const T kw = fold_weight<T>(sk, x, r, W);
+                        const int hc = (p0 + o + kSsimR + d) * 3 + c;
+                        s0 += kw * vs[0][ty][hc];
+                        s1 += kw * vs[1][ty][hc];
+                        s2 += kw * vs[2][ty][hc];
+                    }
+                }
+                hacc[o][0] = s0;
+                hacc[o][1] = s1;
+                hacc[o][2] = s2;
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < kSsimVRows; ++o) {
+            adj[0][ty][p0 * 3 + c + 3 * o] = hacc[o][0];
+            adj[1][ty][p0 * 3 + c + 3 * o] = hacc[o][1];
+            adj[2][ty][p0 * 3 + c + 3 * o] = hacc[o][2];
+        }
+    }
+    static_assert(3 * kSsimTH * kSsimCols <= 3 * kSsimHaloRows * kSsimHaloCols, "adj fits over gs");
+    __syncthreads();
+    // combine (gradients.py:110-116), coalesced over the tile's rows
+    const T w_l1 = (T)(1.0 - lambda_ssim) / (T)N, w_ssim = (T)lambda_ssim, sc = (T)scale;
+    for (int e = threadIdx.x; e < kSsimTH * kSsimCols; e += kSsimThreads) {
         const int ty = e / kSsimCols, cc = e - ty * kSsimCols;
         const int y = y0 + ty, x = x0 + cc / 3;
         if (y >= H || x >= W) continue;
-        const int hc0 = cc + 3 * kSsimR;  // this element in halo columns
-        T adj0 = 0, adj1 = 0, adj2 = 0;
-        if (x >= 6 && x + 7 < W) {
-#pragma unroll
-            for (int t = 0; t < 11; ++t) {  // source column x + 5 - t
-                const int hc = hc0 + 3 * (kSsimR - t);
-                const T k = (T)w.k[t];
-                adj0 += k * vs[0][ty][hc];
-                adj1 += k * vs[1][ty][hc];
-                adj2 += k * vs[2][ty][hc];
-            }
-        } else {
-            for (int d = -kSsimR; d <= kSsimR; ++d) {
-                const int r = x + d;
-                if (r < 0 || r >= W) continue;
-                const T k = fold_weight<T>(w, x, r, W);
-                const int hc = hc0 + 3 * d;
-                adj0 += k * vs[0][ty][hc];
-                adj1 += k * vs[1][ty][hc];
-                adj2 += k * vs[2][ty][hc];
-            }
-        }
         const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
         const T av = a[idx], bv = b[idx];
-        const T gsum = adj0 + adj1 * (T)2 * av + adj2 * bv;
+        const T gsum = adj[0][ty][cc] + adj[1][ty][cc] * (T)2 * av + adj[2][ty][cc] * bv;
         const T diff = av - bv;
         const T sgn = diff > (T)0 ? (T)1 : (diff < (T)0 ? (T)-1 : (T)0);
-        g_image[idx] = (T)scale * ((T)(1.0 - lambda_ssim) * sgn / (T)N - (T)lambda_ssim * gsum);
+        g_image[idx] = sc * (w_l1 * sgn - w_ssim * gsum);
     }
 }
 
@@ -443,8 +563,8 @@ static void run_loss(const T *a, const T *b, int H, int W, double lam, double sc
         const size_t adj_smem = sizeof(T) * 3 * (kSsimHaloRows + kSsimTH) * kSsimHaloCols;
         cudaFuncSetAttribute(ssim_fwd_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
         cudaFuncSetAttribute(ssim_adj_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem);
-        ssim_fwd_tile_kernel<T><<<grid, 256, fwd_smem, s>>>(a, b, H, W, w, g3, sums);
-        ssim_adj_tile_kernel<T><<<grid, 256, adj_smem, s>>>(a, b, g3, H, W, w, lam, scale, g);
+        ssim_fwd_tile_kernel<T><<<grid, kSsimThreads, fwd_smem, s>>>(a, b, H, W, w, g3, sums);
+        ssim_adj_tile_kernel<T><<<grid, kSsimThreads, adj_smem, s>>>(a, b, g3, H, W, w, lam, scale, g);
         return;
     }
     ssim_hblur_kernel<T><<<blocks, thr, 0, s>>>(a, b, H, W, w, h5);
