@@ -5,7 +5,9 @@ Workload (one step = one frame): the 7D dynamic UBS scene, 1M primitives
 (``synth(7, 1_000_000, seed=1)``), rendered at 1920x1080 along
 the 300-frame time sweep t = k/299 with the benchmark camera.  The scene is
 resident in HBM; each frame runs preprocess -> depth sort -> tile binning ->
-fp32 raster -> fp64 fix-up, all in libubs_b200.so.
+fp32 raster -> fp64 fix-up, all in libubs_b200.so.  Frames run 16 in flight
+(engine.FramePipeline) in groups of 4 that share one preprocess launch
+(ubs_preprocess_views: one read of the scene statics per group).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -54,7 +56,9 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
-    ap.add_argument("--inflight", type=int, default=8, help="frames in flight (engine.FramePipeline depth)")
+    ap.add_argument("--inflight", type=int, default=16, help="frames in flight (engine.FramePipeline depth)")
+    ap.add_argument("--group", type=int, default=4,
+                    help="frames per shared preprocess (FramePipeline.render_group; 0: frame by frame)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step measurement")
@@ -71,7 +75,7 @@ def workload_config(a):
     return {"workload": f"config 4: {a.nd}D UBS scene, {a.n_prims} primitives, {a.width}x{a.height}, "
                         f"{SWEEP}-frame time sweep (one frame per step)",
             "n_prims": a.n_prims, "n_dims": a.nd, "width": a.width, "height": a.height,
-            "sweep_frames": SWEEP, "frames_in_flight": a.inflight,
+            "sweep_frames": SWEEP, "frames_in_flight": a.inflight, "frames_per_preprocess": max(a.group, 1),
             "scene": "synth(nd, N, seed=1) (SURVEY 8d), float32 records",
             "l2": "inputs exceed L2: 4*P*N = %.0f MB of primitive records (> 126 MB L2) are re-read every "
                   "frame; no explicit flush" % (4 * (14 + 6 * (a.nd - 3)) * a.n_prims / 1e6)}
@@ -346,6 +350,18 @@ def run_ours(a, rank, world, local_rank):
         return pipe.render(cam, frame_query(a.nd, cam, rank + world * k), DEFAULT_SETTINGS, timers=timers,
                            sync=sync)
 
+    def frames(k0, count):
+        """frames k0 .. k0+count-1 of this rank: grouped (one preprocess per group) or one by one"""
+        out = []
+        for g0 in range(k0, k0 + count, max(a.group, 1)):
+            ks = range(g0, min(g0 + max(a.group, 1), k0 + count))
+            if a.group > 1:
+                out += pipe.render_group([(cam, frame_query(a.nd, cam, rank + world * k)) for k in ks],
+                                         DEFAULT_SETTINGS)
+            else:
+                out += [frame(k) for k in ks]
+        return out
+
     def frame_single(k, timers=None, sync=False):
         return engine.render_frame(ws, ds, cam, frame_query(a.nd, cam, rank + world * k), DEFAULT_SETTINGS,
                                    timers=timers, sync=sync)
@@ -381,8 +397,11 @@ def run_ours(a, rank, world, local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ds.invalidate_statics()  # the sweep pays its one scene-statics pass
         e0.record()
-        for k in range(a.steps):
-            fr = render(k, timers)
+        if timers is None:
+            fr = frames(0, a.steps)[-1]
+        else:
+            for k in range(a.steps):
+                fr = render(k, timers)
         pipe.join()
         e1.record()
         torch.cuda.synchronize()
@@ -435,26 +454,29 @@ def run_ours(a, rank, world, local_rank):
     # --- end to end: image streamed to pinned host memory every frame -----
     sink = engine.HostFrameSink(a.height, a.width, dtype=ws.image_buf.dtype, device=dev)
 
-    def submit(k):
-        fr = frame(k)
-        if pipe.depth > 1:
-            # zero-copy: the D2H reads the slot's own image; the slot's next frame waits for it
-            sink.submit(fr, source_stream=pipe.stream_of(fr))
-            pipe.hold(fr, sink.last_copy)
-        else:  # one slot: snapshot on the device so the next frame need not wait for the copy
-            with torch.cuda.stream(pipe.stream_of(fr)):
-                sink.submit(fr)
+    def submit(k0, count=1):
+        g = max(a.group, 1)
+        for g0 in range(k0, k0 + count, g):  # each group's copies are queued before the next group renders
+            submit_frames(frames(g0, min(g, k0 + count - g0)))
 
-    for k in range(2 * pipe.depth):
-        submit(k)
+    def submit_frames(frs):
+        for fr in frs:
+            if pipe.depth > 1:
+                # zero-copy: the D2H reads the slot's own image; the slot's next frame waits for it
+                sink.submit(fr, source_stream=pipe.stream_of(fr))
+                pipe.hold(fr, sink.last_copy)
+            else:  # one slot: snapshot on the device so the next frame need not wait for the copy
+                with torch.cuda.stream(pipe.stream_of(fr)):
+                    sink.submit(fr)
+
+    submit(0, 2 * pipe.depth)
     sink.synchronize()
     torch.cuda.synchronize()
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ds.invalidate_statics()
     f0.record()
-    for k in range(a.steps):
-        submit(k)
+    submit(0, a.steps)
     pipe.join()
     torch.cuda.current_stream().wait_stream(sink.copy_stream)
     f1.record()
@@ -529,7 +551,8 @@ def run_ours(a, rank, world, local_rank):
                 "d2h_bytes_per_step": sink.bytes_per_frame,
                 "path": "engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, copy stream)",
                 "d2h_link_gbs": d2h_gbs, "link_ceiling_fps": d2h_gbs * 1e9 / sink.bytes_per_frame},
-        "gpu_launches": per_frame_launches * a.steps + 1,
+        # one preprocess launch per group of frames (--group), the rest per frame
+        "gpu_launches": (per_frame_launches - 1) * a.steps + -(-a.steps // max(a.group, 1)) + 1,
         "clocks": clocks,
         "train": train,
         "other_configs": other,

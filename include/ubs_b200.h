@@ -51,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 2
+#define UBS_ABI_VERSION 3
 #define UBS_TILE 16
 
 enum {
@@ -201,6 +201,17 @@ int ubs_scene_statics(const UbsView *v, void *statics, ubs_stream_t s);
 
 /* slice + project + tile rects (fp64 arithmetic, one thread per primitive) */
 int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32, ubs_stream_t s);
+
+/* ubs_preprocess for n_views views of ONE scene (same params, statics, n,
+ * n_dims, settings; cameras and queries differ), each into its own
+ * UbsPrimBuffers: the scene statics (required) are read once per
+ * UBS_MAX_VIEWS views instead of once per view.  Outputs are bit-identical
+ * to n_views ubs_preprocess calls.  The same reference functions as
+ * ubs_preprocess (slicing.py:185-235, raster.py:95-134, raster.py:252-266),
+ * applied to a batch of frames (a sweep or a training batch). */
+#define UBS_MAX_VIEWS 8
+int ubs_preprocess_views(const UbsView *views, const UbsPrimBuffers *pbs, int32_t n_views, int32_t want_rec32,
+                         ubs_stream_t s);
 
 /* scratch bytes (UbsBinBuffers.temp) needed for n primitives */
 size_t ubs_bin_temp_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);

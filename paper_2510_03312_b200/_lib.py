@@ -71,7 +71,8 @@ class UbsGradBuffers(Structure):
                 ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p)]
 
 
-ABI_VERSION = 2  # UBS_ABI_VERSION in include/ubs_b200.h
+ABI_VERSION = 3  # UBS_ABI_VERSION in include/ubs_b200.h
+MAX_VIEWS = 8  # UBS_MAX_VIEWS
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares
 SIGNATURES = [
@@ -80,6 +81,7 @@ SIGNATURES = [
     ("ubs_statics_bytes", c_size_t, [c_int64, c_int32, c_int32]),
     ("ubs_scene_statics", c_int32, [POINTER(UbsView), c_void_p, c_void_p]),
     ("ubs_preprocess", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), c_int32, c_void_p]),
+    ("ubs_preprocess_views", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), c_int32, c_int32, c_void_p]),
     ("ubs_bin_temp_bytes", c_size_t, [c_int64, c_int64, c_int32]),
     ("ubs_bin_depth", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers), c_void_p]),
     ("ubs_bin_tiles", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers), c_int64,

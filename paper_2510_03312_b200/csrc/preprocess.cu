@@ -40,6 +40,160 @@ statics_kernel(const UbsView v, void *out) {
     store_statics<C, PT>(out, base + t, g, mu_x, mu_q);
 }
 
+// Block-wide visible count, pair total and depth range of one view, added to
+// the view's counters with one atomic each per CTA.
+struct PreAgg {
+    uint32_t vis;
+    unsigned long long pairs, dmin, dmax;
+};
+
+__device__ __forceinline__ void preprocess_aggregate(PreAgg &agg, const UbsPrimBuffers &pb, bool vis,
+                                                     uint32_t my_count, unsigned long long my_key) {
+    unsigned ballot = __ballot_sync(0xffffffffu, vis);
+    unsigned long long wsum = my_count;
+    unsigned long long kmin = vis ? my_key : ~0ull, kmax = vis ? my_key : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        kmin = min(kmin, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (ballot) {
+            atomicAdd(&agg.vis, (uint32_t)__popc(ballot));
+            atomicMin(&agg.dmin, kmin);
+            atomicMax(&agg.dmax, kmax);
+        }
+        if (wsum) atomicAdd(&agg.pairs, wsum);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (agg.vis) {
+            atomicAdd(pb.n_visible, agg.vis);
+            atomicMin(pb.depth_range, agg.dmin);
+            atomicMax(pb.depth_range + 1, agg.dmax);
+        }
+        if (agg.pairs) atomicAdd(pb.n_pairs, agg.pairs);
+        agg.vis = 0;
+        agg.pairs = 0;
+        agg.dmin = ~0ull;
+        agg.dmax = 0;
+    }
+}
+
+// The per-view outputs of primitive i once g holds its view-dependent
+// geometry (prim_view / prim_geom): depth key, tile rect and count (plus the
+// rect's corners in the 2D difference array), flags, raster records.
+template <int C>
+__device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimBuffers &pb, int want_rec32,
+                                                int64_t i, const PrimGeom<C> &g, bool &vis, uint32_t &my_count,
+                                                unsigned long long &my_key) {
+    const int W = v.cam.width, H = v.cam.height;
+    const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
+    uint32_t count = 0;
+    uint64_t rect = 0;
+    vis = g.visible;
+    if (vis) {
+        // inclusive tile test of raster.py:261-264 as a closed form:
+        // tile tx is hit iff hi >= 16 tx and lo <= min(16 (tx+1), W)
+        const double lox = g.mean2[0] - g.radii[0], hix = g.mean2[0] + g.radii[0];
+        const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
+        if (hix >= 0.0 && lox <= (double)W && hiy >= 0.0 && loy <= (double)H) {
+            double tx0 = fmax(0.0, ceil(lox / kTile) - 1.0), tx1 = fmin((double)(TX - 1), floor(hix / kTile));
+            double ty0 = fmax(0.0, ceil(loy / kTile) - 1.0), ty1 = fmin((double)(TY - 1), floor(hiy / kTile));
+            if (tx1 >= tx0 && ty1 >= ty0) {
+                uint64_t a = (uint64_t)tx0, b = (uint64_t)ty0, c = (uint64_t)tx1, d = (uint64_t)ty1;
+                rect = a | (b << 16) | (c << 32) | (d << 48);
+                count = (uint32_t)((c - a + 1) * (d - b + 1));
+                // 2D difference array: a prefix sum over it gives every tile's pair count
+                const int gw = TX + 1;
+                atomicAdd(pb.tile_grid + (int)b * gw + (int)a, 1);
+                atomicAdd(pb.tile_grid + (int)b * gw + (int)c + 1, -1);
+                atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)a, -1);
+                atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)c + 1, 1);
+            }
+        }
+    }
+    pb.depth_key[i] = vis ? (uint64_t)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
+    my_key = pb.depth_key[i];
+    pb.rect[i] = rect;
+    pb.tile_count[i] = count;
+    my_count = count;
+    uint16_t fl = (vis ? UBS_F_VISIBLE : 0) | (g.valid ? 0 : UBS_F_DEGENERATE) |
+                  (g.floored3 ? UBS_F_FLOOR3 : 0) | (g.floored2 ? UBS_F_FLOOR2 : 0);
+    if constexpr (C > 0) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            fl |= (g.s_tanh[k] > 0.0 ? 1 : 0) << (8 + k);
+            if (g.d_gate[k] == 1.0) fl |= UBS_F_GATE_SAT;
+        }
+    }
+
+    // raster records (only read for visible primitives)
+    if (pb.rec64) {
+        Rec64 r;
+        r.mx = g.mean2[0]; r.my = g.mean2[1];
+        r.p00 = g.p2[0]; r.p01 = g.p2[1]; r.p11 = g.p2[2];
+        r.og = g.og; r.bx = g.beta_x;
+        r.cr = g.color[0]; r.cg = g.color[1]; r.cb = g.color[2];
+        reinterpret_cast<Rec64 *>(pb.rec64)[i] = r;
+    }
+    if (want_rec32 && pb.rec32) {
+        // P = U^T U with U upper triangular (Cholesky of P, transposed)
+        const double u00 = sqrt(g.p2[0]);
+        const double u01 = g.p2[1] / u00;
+        const double u11 = sqrt(fmax(g.p2[2] - u01 * u01, 0.0));
+        const double fxm = floor(g.mean2[0]), fym = floor(g.mean2[1]);
+        const bool in_range = fabs(g.mean2[0]) < 4.0e6 && fabs(g.mean2[1]) < 4.0e6 && isfinite(u11);
+        // E bounds |m32 - m64| over the support (m < tau => |dx| < rx, |dy| < ry,
+        // |y0|, |y1| < sqrt(tau)), with u = 2^-24 the fp32 unit roundoff:
+        //   dx = (px - fx) + ox        |d dx| <= u (|dx| + 0.5)   (ox rounded, one add)
+        //   y0 = fma(u01, dy, u00 dx)  |d y0| <= u (|u00|(3|dx| + .5) + |u01|(3|dy| + .5) + |y0|)
+        //                              (either product may be the separately rounded one)
+        //   y1 = u11 dy                |d y1| <= u (|u11|(2|dy| + .5) + |y1|)
+        //   m  = fma(y0, y0, y1 y1)    |d m|  <= 2|y0||d y0| + 2|y1||d y1| + 2 u tau
+        // (u.. rounded to fp32 included), times a 1.25 safety factor.
+        const double u = 5.9604644775390625e-08;
+        const double st = sqrt(v.set.tau_sq);
+        const double rx = g.radii[0], ry = g.radii[1];
+        double E = 1.25 * u * (2.0 * st * (fabs(u00) * (3.0 * rx + 0.5) + fabs(u01) * (3.0 * ry + 0.5) + st) +
+                               2.0 * st * (fabs(u11) * (2.0 * ry + 0.5) + st) + 2.0 * v.set.tau_sq);
+        double eb = in_range ? g.beta_x * E : INFINITY;
+        if (!isfinite(eb)) fl |= UBS_F_THIN;
+        Rec32 r;
+        r.r0 = make_float4(in_range ? (float)fxm : 0.f, in_range ? (float)fym : 0.f,
+                           (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
+        r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)(v.set.tau_sq + E));
+        r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
+        // qc: lg2.approx absolute error 2^-22.6 (near 1) times ln2 beta, ex2.approx
+        // relative error 2^-22, og / log2(og) representation; the |arg|-relative
+        // parts are added per visit in the raster (2.1e-7 |arg|)
+        const double qc = 0.6931471805599453 * g.beta_x * 1.6e-7 + 4.0e-7;
+        r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2(g.og));
+        reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
+    }
+    pb.flags[i] = fl;
+
+    if (pb.debug) {
+        double *d = pb.debug + i * UBS_DEBUG_STRIDE;
+        d[0] = g.tcam[2];
+        d[1] = g.mean2[0]; d[2] = g.mean2[1];
+        d[3] = g.p2[0]; d[4] = g.p2[1]; d[5] = g.p2[2];
+        d[6] = g.radii[0]; d[7] = g.radii[1];
+        d[8] = g.og; d[9] = g.beta_x;
+        d[10] = g.cov2[0]; d[11] = g.cov2[1]; d[12] = g.cov2[2];
+        d[13] = g.cov3[0][0]; d[14] = g.cov3[0][1]; d[15] = g.cov3[0][2];
+        d[16] = g.cov3[1][1]; d[17] = g.cov3[1][2]; d[18] = g.cov3[2][2];
+        d[19] = g.tcam[0]; d[20] = g.tcam[1]; d[21] = g.tcam[2];
+        d[22] = g.mean3[0]; d[23] = g.mean3[1]; d[24] = g.mean3[2];
+        d[25] = g.gate; d[26] = g.opacity;
+        for (int k = 0; k < 4; ++k) d[27 + k] = 0.0;
+        if constexpr (C > 0) {
+            for (int k = 0; k < C; ++k) d[27 + k] = g.s_tanh[k];
+        }
+        d[31] = g.floor_eps;
+    }
+}
+
 // kStatic: the query-invariant half comes from v.statics (ubs_scene_statics)
 // and only prim_view runs here; otherwise the whole of prim_geom.
 template <int C, typename PT, bool kStatic>
@@ -47,12 +201,11 @@ __global__ void __launch_bounds__(kPreThreads, kStatic ? 5 : 4)
 preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
     constexpr int P = 14 + 6 * C;
     __shared__ PT stage[kStatic ? 1 : kPreThreads * P];
-    __shared__ uint32_t block_vis;
-    __shared__ unsigned long long block_pairs, block_dmin, block_dmax;
+    __shared__ PreAgg agg;
     const int64_t base = (int64_t)blockIdx.x * kPreThreads;
     const int64_t n = v.n;
     const int nloc = (int)min((int64_t)kPreThreads, n - base);
-    if (threadIdx.x == 0) { block_vis = 0; block_pairs = 0; block_dmin = ~0ull; block_dmax = 0; }
+    if (threadIdx.x == 0) { agg.vis = 0; agg.pairs = 0; agg.dmin = ~0ull; agg.dmax = 0; }
     if constexpr (!kStatic) {
         const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
         for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
@@ -73,139 +226,90 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
         } else {
             prim_geom<C, PT>(stage + t * P, v, g, mu_x);
         }
-
-        const int W = v.cam.width, H = v.cam.height;
-        const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
-        uint32_t count = 0;
-        uint64_t rect = 0;
-        vis = g.visible;
-        if (vis) {
-            // inclusive tile test of raster.py:261-264 as a closed form:
-            // tile tx is hit iff hi >= 16 tx and lo <= min(16 (tx+1), W)
-            const double lox = g.mean2[0] - g.radii[0], hix = g.mean2[0] + g.radii[0];
-            const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
-            if (hix >= 0.0 && lox <= (double)W && hiy >= 0.0 && loy <= (double)H) {
-                double tx0 = fmax(0.0, ceil(lox / kTile) - 1.0), tx1 = fmin((double)(TX - 1), floor(hix / kTile));
-                double ty0 = fmax(0.0, ceil(loy / kTile) - 1.0), ty1 = fmin((double)(TY - 1), floor(hiy / kTile));
-                if (tx1 >= tx0 && ty1 >= ty0) {
-                    uint64_t a = (uint64_t)tx0, b = (uint64_t)ty0, c = (uint64_t)tx1, d = (uint64_t)ty1;
-                    rect = a | (b << 16) | (c << 32) | (d << 48);
-                    count = (uint32_t)((c - a + 1) * (d - b + 1));
-                    // 2D difference array: a prefix sum over it gives every tile's pair count
-                    const int gw = TX + 1;
-                    atomicAdd(pb.tile_grid + (int)b * gw + (int)a, 1);
-                    atomicAdd(pb.tile_grid + (int)b * gw + (int)c + 1, -1);
-                    atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)a, -1);
-                    atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)c + 1, 1);
-                }
-            }
-        }
-        pb.depth_key[i] = vis ? (uint64_t)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
-        my_key = pb.depth_key[i];
-        pb.rect[i] = rect;
-        pb.tile_count[i] = count;
-        my_count = count;
-        uint16_t fl = (vis ? UBS_F_VISIBLE : 0) | (g.valid ? 0 : UBS_F_DEGENERATE) |
-                      (g.floored3 ? UBS_F_FLOOR3 : 0) | (g.floored2 ? UBS_F_FLOOR2 : 0);
-        if constexpr (C > 0) {
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                fl |= (g.s_tanh[k] > 0.0 ? 1 : 0) << (8 + k);
-                if (g.d_gate[k] == 1.0) fl |= UBS_F_GATE_SAT;
-            }
-        }
-
-        // raster records (only read for visible primitives)
-        if (pb.rec64) {
-            Rec64 r;
-            r.mx = g.mean2[0]; r.my = g.mean2[1];
-            r.p00 = g.p2[0]; r.p01 = g.p2[1]; r.p11 = g.p2[2];
-            r.og = g.og; r.bx = g.beta_x;
-            r.cr = g.color[0]; r.cg = g.color[1]; r.cb = g.color[2];
-            reinterpret_cast<Rec64 *>(pb.rec64)[i] = r;
-        }
-        if (want_rec32 && pb.rec32) {
-            // P = U^T U with U upper triangular (Cholesky of P, transposed)
-            const double u00 = sqrt(g.p2[0]);
-            const double u01 = g.p2[1] / u00;
-            const double u11 = sqrt(fmax(g.p2[2] - u01 * u01, 0.0));
-            const double fxm = floor(g.mean2[0]), fym = floor(g.mean2[1]);
-            const bool in_range = fabs(g.mean2[0]) < 4.0e6 && fabs(g.mean2[1]) < 4.0e6 && isfinite(u11);
-            // E bounds |m32 - m64| over the support (m < tau => |dx| < rx, |dy| < ry,
-            // |y0|, |y1| < sqrt(tau)), with u = 2^-24 the fp32 unit roundoff:
-            //   dx = (px - fx) + ox        |d dx| <= u (|dx| + 0.5)   (ox rounded, one add)
-            //   y0 = fma(u01, dy, u00 dx)  |d y0| <= u (|u00|(3|dx| + .5) + |u01|(3|dy| + .5) + |y0|)
-            //                              (either product may be the separately rounded one)
-            //   y1 = u11 dy                |d y1| <= u (|u11|(2|dy| + .5) + |y1|)
-            //   m  = fma(y0, y0, y1 y1)    |d m|  <= 2|y0||d y0| + 2|y1||d y1| + 2 u tau
-            // (u.. rounded to fp32 included), times a 1.25 safety factor.
-            const double u = 5.9604644775390625e-08;
-            const double st = sqrt(v.set.tau_sq);
-            const double rx = g.radii[0], ry = g.radii[1];
-            double E = 1.25 * u * (2.0 * st * (fabs(u00) * (3.0 * rx + 0.5) + fabs(u01) * (3.0 * ry + 0.5) + st) +
-                                   2.0 * st * (fabs(u11) * (2.0 * ry + 0.5) + st) + 2.0 * v.set.tau_sq);
-            double eb = in_range ? g.beta_x * E : INFINITY;
-            if (!isfinite(eb)) fl |= UBS_F_THIN;
-            Rec32 r;
-            r.r0 = make_float4(in_range ? (float)fxm : 0.f, in_range ? (float)fym : 0.f,
-                               (float)(0.5 - (g.mean2[0] - fxm)), (float)(0.5 - (g.mean2[1] - fym)));
-            r.r1 = make_float4((float)u00, (float)u01, (float)u11, (float)(v.set.tau_sq + E));
-            r.r2 = make_float4((float)g.beta_x, (float)g.color[0], (float)g.color[1], (float)g.color[2]);
-            // qc: lg2.approx absolute error 2^-22.6 (near 1) times ln2 beta, ex2.approx
-            // relative error 2^-22, og / log2(og) representation; the |arg|-relative
-            // parts are added per visit in the raster (2.1e-7 |arg|)
-            const double qc = 0.6931471805599453 * g.beta_x * 1.6e-7 + 4.0e-7;
-            r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2(g.og));
-            reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
-        }
-        pb.flags[i] = fl;
-
-        if (pb.debug) {
-            double *d = pb.debug + i * UBS_DEBUG_STRIDE;
-            d[0] = g.tcam[2];
-            d[1] = g.mean2[0]; d[2] = g.mean2[1];
-            d[3] = g.p2[0]; d[4] = g.p2[1]; d[5] = g.p2[2];
-            d[6] = g.radii[0]; d[7] = g.radii[1];
-            d[8] = g.og; d[9] = g.beta_x;
-            d[10] = g.cov2[0]; d[11] = g.cov2[1]; d[12] = g.cov2[2];
-            d[13] = g.cov3[0][0]; d[14] = g.cov3[0][1]; d[15] = g.cov3[0][2];
-            d[16] = g.cov3[1][1]; d[17] = g.cov3[1][2]; d[18] = g.cov3[2][2];
-            d[19] = g.tcam[0]; d[20] = g.tcam[1]; d[21] = g.tcam[2];
-            d[22] = g.mean3[0]; d[23] = g.mean3[1]; d[24] = g.mean3[2];
-            d[25] = g.gate; d[26] = g.opacity;
-            for (int k = 0; k < 4; ++k) d[27 + k] = 0.0;
-            if constexpr (C > 0) {
-                for (int k = 0; k < C; ++k) d[27 + k] = g.s_tanh[k];
-            }
-            d[31] = g.floor_eps;
-        }
+        preprocess_emit<C>(v, pb, want_rec32, i, g, vis, my_count, my_key);
     }
-    // block-aggregated visible count and pair total
-    unsigned ballot = __ballot_sync(0xffffffffu, vis);
-    unsigned long long wsum = my_count;
-    unsigned long long kmin = vis ? my_key : ~0ull, kmax = vis ? my_key : 0ull;
-    for (int o = 16; o > 0; o >>= 1) {
-        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-        kmin = min(kmin, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (ballot) {
-            atomicAdd(&block_vis, (uint32_t)__popc(ballot));
-            atomicMin(&block_dmin, kmin);
-            atomicMax(&block_dmax, kmax);
-        }
-        if (wsum) atomicAdd(&block_pairs, wsum);
-    }
-    __syncthreads();
+    preprocess_aggregate(agg, pb, vis, my_count, my_key);
+}
+
+// Several views of one scene from one read of its statics: the CTA's
+// 128-primitive statics block (StaticLayout, 16..62 KB contiguous) is pulled
+// into shared memory with one TMA bulk copy, then every view runs prim_view
+// from it.  Per view this saves the statics read (352 B per primitive at 7D
+// of the ~520 B a view moves), which is most of preprocess's HBM traffic;
+// the arithmetic and outputs are those of preprocess_kernel<C, PT, true>.
+constexpr int kMaxViews = UBS_MAX_VIEWS;
+
+struct PreViews {
+    UbsView v[kMaxViews];
+    UbsPrimBuffers pb[kMaxViews];
+    int nv;
+    int want_rec32;
+};
+
+template <int C, typename PT>
+__global__ void __launch_bounds__(kPreThreads, 4)
+preprocess_views_kernel(const __grid_constant__ PreViews m) {
+    using L = StaticLayout<C>;
+    constexpr uint32_t kBlockBytes = (uint32_t)kStaticBlock * (8 * L::D + sizeof(PT) * L::R);
+    static_assert(kStaticBlock == kPreThreads && kBlockBytes % 16 == 0, "statics block = CTA, 16 B multiple");
+    extern __shared__ __align__(128) unsigned char st_block[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ PreAgg agg;
+    const int64_t base = (int64_t)blockIdx.x * kPreThreads;
+    const int nloc = (int)min((int64_t)kPreThreads, m.v[0].n - base);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar);
     if (threadIdx.x == 0) {
-        if (block_vis) {
-            atomicAdd(pb.n_visible, block_vis);
-            atomicMin(pb.depth_range, block_dmin);
-            atomicMax(pb.depth_range + 1, block_dmax);
-        }
-        if (block_pairs) atomicAdd(pb.n_pairs, block_pairs);
+        agg.vis = 0; agg.pairs = 0; agg.dmin = ~0ull; agg.dmax = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const char *src = reinterpret_cast<const char *>(m.v[0].statics) + (size_t)blockIdx.x * kBlockBytes;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBlockBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(st_block)),
+            "l"(src), "r"(kBlockBytes), "r"(bar)
+            : "memory");
     }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(bar)
+        : "memory");
+    const int t = threadIdx.x;
+    for (int k = 0; k < m.nv; ++k) {
+        const UbsView &v = m.v[k];
+        const UbsPrimBuffers &pb = m.pb[k];
+        bool vis = false;
+        uint32_t my_count = 0;
+        unsigned long long my_key = ~0ull;
+        if (t < nloc) {
+            PrimGeom<C> g;
+            double mu_x[3], mu_q[PrimGeom<C>::CC];
+            load_statics<C, PT, false>(st_block, t, g, mu_x, mu_q);  // slot t of the staged block
+            prim_view<C>(g, mu_x, mu_q, v, pb.debug != nullptr);
+            preprocess_emit<C>(v, pb, m.want_rec32, base + t, g, vis, my_count, my_key);
+        }
+        preprocess_aggregate(agg, pb, vis, my_count, my_key);
+        __syncthreads();  // agg reset by thread 0 before the next view adds to it
+    }
+}
+
+template <int C, typename PT>
+static int launch_views(const PreViews &m, cudaStream_t s) {
+    using L = StaticLayout<C>;
+    constexpr size_t kBlockBytes = (size_t)kStaticBlock * (8 * L::D + sizeof(PT) * L::R);
+    static bool attr = false;  // per process; the attribute is per function
+    if (!attr) {
+        if (cudaFuncSetAttribute(preprocess_views_kernel<C, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBlockBytes) != cudaSuccess)
+            return UBS_E_CUDA;
+        attr = true;
+    }
+    const int64_t blocks = (m.v[0].n + kPreThreads - 1) / kPreThreads;
+    preprocess_views_kernel<C, PT><<<(unsigned)blocks, kPreThreads, kBlockBytes, s>>>(m);
+    return UBS_OK;
 }
 
 template <int C, typename PT>
@@ -234,23 +338,32 @@ extern "C" const char *ubs_build_info(void) {
            "tile-per-CTA raster fp32 (certified, fp64 fix-up) / fp64";
 }
 
-extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32,
-                              ubs_stream_t stream) {
+static int preprocess_check(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32) {
     if (!v || !pb || !pb->n_visible || !pb->n_pairs) return UBS_E_ARGS;
     if (v->set.tile_size != kTile) return UBS_E_ARGS;
     if (v->n < 0 || (v->n > 0 && !v->params)) return UBS_E_ARGS;
     if (!pb->depth_key || !pb->rect || !pb->tile_count || !pb->flags) return UBS_E_ARGS;
     if (!pb->rec64 && !(want_rec32 && pb->rec32)) return UBS_E_ARGS;
     if (!pb->tile_grid || !pb->depth_range) return UBS_E_ARGS;
-    cudaStream_t s = (cudaStream_t)stream;
+    return UBS_OK;
+}
+
+static int preprocess_reset(const UbsView *v, const UbsPrimBuffers *pb, cudaStream_t s) {
     if (cudaMemsetAsync(pb->depth_range, 0xFF, 8, s) != cudaSuccess ||
         cudaMemsetAsync(pb->depth_range + 1, 0, 8, s) != cudaSuccess)
         return UBS_E_CUDA;
-    {
-        const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
-        if (cudaMemsetAsync(pb->tile_grid, 0, sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1), s) != cudaSuccess)
-            return UBS_E_CUDA;
-    }
+    const int TX = (v->cam.width + kTile - 1) / kTile, TY = (v->cam.height + kTile - 1) / kTile;
+    if (cudaMemsetAsync(pb->tile_grid, 0, sizeof(int32_t) * (size_t)(TX + 1) * (TY + 1), s) != cudaSuccess)
+        return UBS_E_CUDA;
+    return UBS_OK;
+}
+
+extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_t want_rec32,
+                              ubs_stream_t stream) {
+    const int rc = preprocess_check(v, pb, want_rec32);
+    if (rc != UBS_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (preprocess_reset(v, pb, s) != UBS_OK) return UBS_E_CUDA;
     if (v->n == 0) return UBS_OK;
     const bool f64 = v->param_f64 != 0;
     switch (v->n_dims) {
@@ -261,6 +374,47 @@ extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_
         case 7: f64 ? launch_pre<4, double>(*v, *pb, want_rec32, s)
                     : launch_pre<4, float>(*v, *pb, want_rec32, s); break;
         default: return UBS_E_ARGS;
+    }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" int ubs_preprocess_views(const UbsView *views, const UbsPrimBuffers *pbs, int32_t n_views,
+                                    int32_t want_rec32, ubs_stream_t stream) {
+    if (!views || !pbs || n_views < 1) return UBS_E_ARGS;
+    const UbsView &v0 = views[0];
+    for (int k = 0; k < n_views; ++k) {
+        const int rc = preprocess_check(views + k, pbs + k, want_rec32);
+        if (rc != UBS_OK) return rc;
+        const UbsView &v = views[k];
+        // one scene: the views differ in camera and query only
+        if (!v.statics || v.statics != v0.statics || v.params != v0.params || v.n != v0.n ||
+            v.n_dims != v0.n_dims || v.param_f64 != v0.param_f64 || v.set.tau_sq != v0.set.tau_sq)
+            return UBS_E_ARGS;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int k = 0; k < n_views; ++k) {
+        const int rc = preprocess_reset(views + k, pbs + k, s);
+        if (rc != UBS_OK) return rc;
+    }
+    if (v0.n == 0) return UBS_OK;
+    for (int k0 = 0; k0 < n_views; k0 += kMaxViews) {
+        PreViews m;
+        m.nv = min(kMaxViews, n_views - k0);
+        m.want_rec32 = want_rec32;
+        for (int k = 0; k < m.nv; ++k) {
+            m.v[k] = views[k0 + k];
+            m.pb[k] = pbs[k0 + k];
+        }
+        const bool f64 = v0.param_f64 != 0;
+        int rc;
+        switch (v0.n_dims) {
+            case 3: rc = f64 ? launch_views<0, double>(m, s) : launch_views<0, float>(m, s); break;
+            case 6: rc = f64 ? launch_views<3, double>(m, s) : launch_views<3, float>(m, s); break;
+            case 7: rc = f64 ? launch_views<4, double>(m, s) : launch_views<4, float>(m, s); break;
+            default: return UBS_E_ARGS;
+        }
+        if (rc != UBS_OK) return rc;
     }
     UBS_CUDA_CHECK();
     return UBS_OK;

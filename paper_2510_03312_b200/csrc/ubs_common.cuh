@@ -529,7 +529,15 @@ __device__ inline void store_statics(void *buf, int64_t i, const PrimGeom<C> &g,
 // k order for (i, j) and (j, i)), so its upper triangle restores it exactly;
 // the floored cov3 (V w V^T with left-to-right products) is not, so all nine
 // entries are kept.
-template <int C, typename PT>
+// kGlobal: buf is device memory (read-only path); else a shared-memory copy
+// of the primitive's statics block (preprocess_views_kernel)
+template <typename T, bool kGlobal>
+__device__ __forceinline__ T ld_statics(const T *p) {
+    if constexpr (kGlobal) return __ldg(p);
+    else return *p;
+}
+
+template <int C, typename PT, bool kGlobal = true>
 __device__ inline void load_statics(const void *buf, int64_t i, PrimGeom<C> &g, double (&mu_x)[3],
                                     double (&mu_q)[PrimGeom<C>::CC]) {
     using L = StaticLayout<C>;
@@ -537,23 +545,23 @@ __device__ inline void load_statics(const void *buf, int64_t i, PrimGeom<C> &g, 
     double *d;
     PT *r;
     static_slot<C, PT>(const_cast<void *>(buf), i, d, r);
-    for (int k = 0; k < C; ++k) g.beta_q[k] = __ldg(d + (L::kBetaQ + k) * S);
+    for (int k = 0; k < C; ++k) g.beta_q[k] = ld_statics<double, kGlobal>(d + (L::kBetaQ + k) * S);
     int o = L::kM;
     for (int a = 0; a < C; ++a)
-        for (int b = a; b < C; ++b) g.M[a][b] = g.M[b][a] = __ldg(d + (o++) * S);
+        for (int b = a; b < C; ++b) g.M[a][b] = g.M[b][a] = ld_statics<double, kGlobal>(d + (o++) * S);
     for (int a = 0; a < 3; ++a)
-        for (int k = 0; k < C; ++k) g.Sxq[a][k] = __ldg(d + (L::kSxq + a * C + k) * S);
+        for (int k = 0; k < C; ++k) g.Sxq[a][k] = ld_statics<double, kGlobal>(d + (L::kSxq + a * C + k) * S);
     for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) g.cov3[a][b] = __ldg(d + (L::kCov3 + 3 * a + b) * S);
-    g.opacity = __ldg(d + L::kOpacity * S);
-    g.beta_x = __ldg(d + L::kBetaX * S);
-    g.floor_eps = __ldg(d + L::kFloorEps * S);
-    const int fl = (int)__ldg(d + L::kFlags * S);
+        for (int b = 0; b < 3; ++b) g.cov3[a][b] = ld_statics<double, kGlobal>(d + (L::kCov3 + 3 * a + b) * S);
+    g.opacity = ld_statics<double, kGlobal>(d + L::kOpacity * S);
+    g.beta_x = ld_statics<double, kGlobal>(d + L::kBetaX * S);
+    g.floor_eps = ld_statics<double, kGlobal>(d + L::kFloorEps * S);
+    const int fl = (int)ld_statics<double, kGlobal>(d + L::kFlags * S);
     g.valid = (fl & 1) != 0;
     g.floored3 = (fl & 2) != 0;
-    for (int k = 0; k < 3; ++k) mu_x[k] = (double)__ldg(r + k * S);
-    for (int k = 0; k < C; ++k) mu_q[k] = (double)__ldg(r + (3 + k) * S);
-    for (int k = 0; k < 3; ++k) g.color[k] = (double)__ldg(r + (3 + C + k) * S);
+    for (int k = 0; k < 3; ++k) mu_x[k] = (double)ld_statics<PT, kGlobal>(r + k * S);
+    for (int k = 0; k < C; ++k) mu_q[k] = (double)ld_statics<PT, kGlobal>(r + (3 + k) * S);
+    for (int k = 0; k < 3; ++k) g.color[k] = (double)ld_statics<PT, kGlobal>(r + (3 + C + k) * S);
 }
 
 // Device-side capacity guard for the pair buffers: true (and the overflow

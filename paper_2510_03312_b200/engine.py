@@ -413,7 +413,14 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
     e.g. for FrameCache.tiles).  A frame that needed more sets
     UBS_S_LIST_TRUNC: synchronous frames then double the cap and re-render,
     asynchronous ones leave it to :func:`check_status`."""
-    lib = ws.lib
+    v, pb = _frame_begin(ws, ds, cam, query, settings, want_debug)
+    with _Timed(timers, "preprocess"):
+        check(ws.lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, _stream_ptr()), "ubs_preprocess")
+    return _frame_end(ws, ds, v, pb, cam, query, settings, want_debug, timers, sync, full_lists)
+
+
+def _frame_begin(ws: Workspace, ds: DeviceScene, cam, query, settings, want_debug: bool):
+    """Size the workspace for the frame and reset its counters (current stream)."""
     if ds.device != ws.device:
         raise ValueError("scene and workspace live on different devices")
     v = make_view(ds, cam, query, settings)
@@ -426,11 +433,16 @@ def render_frame(ws: Workspace, ds: DeviceScene, cam, query, settings=DEFAULT_SE
             ws.debug = torch.zeros(max(n, 1) * _lib.DEBUG_STRIDE, dtype=torch.float64, device=ws.device)
     if ws.temp_bytes == 0:
         ws.ensure_pairs(0)
-    s = _stream_ptr()
     ws.counters.zero_()
-    pb = ws.prim_buffers(want_debug)
-    with _Timed(timers, "preprocess"):
-        check(lib.ubs_preprocess(v, pb, 0 if ws.f64 else 1, s), "ubs_preprocess")
+    return v, ws.prim_buffers(want_debug)
+
+
+def _frame_end(ws: Workspace, ds: DeviceScene, v, pb, cam, query, settings, want_debug, timers, sync,
+               full_lists) -> Frame:
+    """Binning, raster and fix-up of a preprocessed frame (current stream)."""
+    lib = ws.lib
+    W, H, n = int(cam.width), int(cam.height), ds.n
+    s = _stream_ptr()
     with _Timed(timers, "bin_depth"):
         check(lib.ubs_bin_depth(v, pb, ws.bin_buffers(), s), "ubs_bin_depth")
     if sync or ws.pair_cap == 0:
@@ -506,6 +518,7 @@ class FramePipeline:
         self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
         self.pending = [None] * depth  # event a slot's next frame must wait for (a consumer of its buffers)
         self.k = 0
+        self.lead = torch.cuda.Stream(dev)  # render_group's shared preprocess
 
     @property
     def depth(self) -> int:
@@ -524,6 +537,53 @@ class FramePipeline:
         with torch.cuda.stream(s):
             return render_frame(self.workspaces[i], self.ds, cam, query, settings, timers=timers, sync=sync,
                                 full_lists=full_lists)
+
+    def render_group(self, views, settings=DEFAULT_SETTINGS) -> list:
+        """Render up to ``depth`` (camera, query) pairs as consecutive frames of
+        the pipeline, with ONE preprocess for all of them
+        (``ubs_preprocess_views``: the scene statics are read once per
+        group instead of once per frame).  The group's slots must be free, so
+        the preprocess waits for the frames that last used them; with
+        ``depth`` = 2 x group size the next group's preprocess overlaps this
+        group's rasters.  Frames are asynchronous (``check_status``)."""
+        views = list(views)
+        if not views:
+            return []
+        if len(views) > self.depth:
+            raise ValueError("a group cannot exceed the pipeline depth")
+        ds = self.ds
+        if not ds.statics_ptr(settings):  # no statics (empty scene, use_statics=False): frame by frame
+            return [self.render(cam, q, settings) for cam, q in views]
+        slots = [(self.k + j) % self.depth for j in range(len(views))]
+        self.k += len(views)
+        lead = self.lead
+        lead.wait_stream(torch.cuda.current_stream())
+        for i in slots:
+            lead.wait_stream(self.streams[i])
+            if self.pending[i] is not None:
+                lead.wait_event(self.pending[i])
+                self.pending[i] = None
+        vs, pbs = [], []
+        with torch.cuda.stream(lead):
+            for (cam, q), i in zip(views, slots):
+                v, pb = _frame_begin(self.workspaces[i], ds, cam, q, settings, False)
+                vs.append(v)
+                pbs.append(pb)
+            ws0 = self.workspaces[slots[0]]
+            va = (_lib.UbsView * len(vs))(*vs)
+            pa = (_lib.UbsPrimBuffers * len(pbs))(*pbs)
+            check(ws0.lib.ubs_preprocess_views(va, pa, len(vs), 0 if ws0.f64 else 1, lead.cuda_stream),
+                  "ubs_preprocess_views")
+            ev = torch.cuda.Event()
+            ev.record(lead)
+        frames = []
+        for (cam, q), i, v, pb in zip(views, slots, vs, pbs):
+            s = self.streams[i]
+            s.wait_event(ev)
+            with torch.cuda.stream(s):
+                frames.append(_frame_end(self.workspaces[i], ds, v, pb, cam, q, settings, False, None, False,
+                                         False))
+        return frames
 
     def stream_of(self, fr: Frame) -> torch.cuda.Stream:
         return self.streams[self.workspaces.index(fr.ws)]

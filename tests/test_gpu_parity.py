@@ -357,3 +357,31 @@ def test_pipeline_zero_copy_host_sink():
     sink.synchronize()
     for a, b in zip(ref, outs):
         assert torch.equal(a, b)
+
+
+def test_grouped_pipeline_zero_copy_host_sink():
+    # groups of frames share one preprocess (render_group); the sink reads each
+    # slot's image and the slot's next group waits for that copy, so every
+    # host image equals the single-stream render
+    import torch
+    from paper_2510_03312_b200 import engine
+    sc = quantize_f32(S.random_scene(7, 3000, seed=73))
+    cam = S.random_camera(96, 74)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    qs = [S.random_query(7, 90 + k) for k in range(11)]
+    ref = [engine.render_frame(ws, ds, cam, q).image.cpu() for q in qs]
+    pipe = engine.FramePipeline(ds, depth=6)
+    for q in qs * 2:
+        pipe.render(cam, q, sync=True)
+    sink = engine.HostFrameSink(96, 96, slots=len(qs))
+    outs = []
+    for g0 in range(0, len(qs), 3):  # groups of 3, the last one short
+        for fr in pipe.render_group([(cam, q) for q in qs[g0:g0 + 3]]):
+            outs.append(sink.submit(fr, source_stream=pipe.stream_of(fr)))
+            pipe.hold(fr, sink.last_copy)
+    pipe.join()
+    sink.synchronize()
+    assert pipe.check_status() == 0
+    for a, b in zip(ref, outs):
+        assert torch.equal(a, b)

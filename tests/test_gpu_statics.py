@@ -84,3 +84,36 @@ def test_statics_follow_parameter_updates():
     assert torch.equal(got.view(torch.int64), ws2.debug[:ds.n * 32].view(torch.int64))
     ds.params.mul_(1.0)  # torch in-place op: version bump
     assert ds.statics_ptr(DEFAULT_SETTINGS) and ds._statics_key[1] == ds.params._version
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
+def test_preprocess_views_matches_per_view(case, precision):
+    """ubs_preprocess_views (one statics read for a group of frames) gives
+    every frame exactly the bits of its own ubs_preprocess: per-primitive
+    outputs, counters and the rendered frame.  10 views: two launches."""
+    _, sc, cam, q = case
+    ds = engine.DeviceScene.from_scene(sc, dtype=torch.float32, device="cuda")
+    nd = sc.n_dims
+    views = [(cam, q)]  # the case's own view, then an orbit with a time sweep
+    for k in range(1, 10):
+        c = S.bench_camera(cam.width, cam.height, k, 10)
+        views.append((c, S.bench_query(nd, c, k / 9.0)))
+    pipe = engine.FramePipeline(ds, depth=10, precision=precision)
+    frames = pipe.render_group(views)
+    pipe.join()
+    torch.cuda.synchronize()
+    pipe.check_status()
+    ref_ws = engine.Workspace("cuda", precision)
+    n = ds.n
+    for (c, qq), fr in zip(views, frames):
+        want = engine.render_frame(ref_ws, ds, c, qq, sync=True)
+        ws = fr.ws
+        for name in ("depth_key", "rect", "flags", "tile_count"):
+            assert torch.equal(getattr(ws, name)[:n], getattr(ref_ws, name)[:n]), name
+        assert torch.equal(ws.rec64[:n * 10].view(torch.int64), ref_ws.rec64[:n * 10].view(torch.int64))
+        if ws.rec32 is not None:
+            assert torch.equal(ws.rec32[:n * 16].view(torch.int32), ref_ws.rec32[:n * 16].view(torch.int32))
+        assert torch.equal(ws.counters[:3], ref_ws.counters[:3])
+        assert torch.equal(fr.n_contrib, want.n_contrib)
+        assert torch.equal(fr.image, want.image)
