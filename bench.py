@@ -65,7 +65,8 @@ def parse():
     ap.add_argument("--train-prims", type=int, default=3_000_000)
     ap.add_argument("--train-views-per-gpu", type=int, default=8)
     ap.add_argument("--train-steps", type=int, default=5)
-    ap.add_argument("--train-inflight", type=int, default=3, help="views in flight per GPU in the training step")
+    ap.add_argument("--train-inflight", type=int, default=8, help="views in flight per GPU in the training step")
+    ap.add_argument("--train-group", type=int, default=4, help="training views per shared preprocess")
     ap.add_argument("--train-only", action="store_true",
                     help="only the config-5 training step (its own JSON line; for profiling)")
     return ap.parse_args()
@@ -257,7 +258,8 @@ def run_train(a, rank, world, local_rank):
         targets.append(engine.render_frame(tws, tds, c, q).image.clone().clamp_(0.0, 1.0))
     del tws, tds
     views = list(zip(cams, views_q, targets))
-    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=a.train_inflight))
+    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=a.train_inflight,
+                                                            group=a.train_group))
     adam = sharding.DeviceAdam(ds.params, 7)
     cfg = LossConfig()
     grad = step.backend.new_grad()
@@ -282,7 +284,8 @@ def run_train(a, rank, world, local_rank):
             "views_per_s": batch * 1e3 / ms, "loss": float(loss),
             "config": {"workload": f"config 5: 7D UBS training step, {a.train_prims} primitives, batch {batch} "
                                    f"1920x1080 orbit views ({a.train_views_per_gpu} per GPU, {a.train_inflight} in "
-                                   f"flight), fwd + L1/SSIM + bwd + all-reduce + Adam",
+                                   f"flight, groups of {a.train_group} sharing one preprocess), "
+                                   f"fwd + L1/SSIM + bwd + all-reduce + Adam",
                        "parallelism": f"dp{world} (view sharding, NCCL "
                                    f"all-reduce of the {4 * 38 * a.train_prims / 1e6:.0f} MB gradient)"},
             "steps": a.train_steps, "warmup": 2, "dtype": "f32 (fp64 geometry/chain)", "data": "synthetic"}

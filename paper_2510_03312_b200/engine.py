@@ -660,10 +660,20 @@ def loss_image_grad(fr: Frame, target: torch.Tensor, lambda_ssim: float, scale: 
 def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
                    add_regularisers: bool = False, reg_opacity: float = 0.0, reg_scale: float = 0.0):
     """Accumulate d(loss)/d(params) of one frame into ``grad_params`` (n x P)."""
+    gb = backward_raster(fr, ds, g_image, grad_params, reg_opacity, reg_scale)
+    if gb is not None:
+        backward_chain(fr, gb, add_regularisers)
+
+
+def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
+                    reg_opacity: float = 0.0, reg_scale: float = 0.0):
+    """First half of :func:`backward_frame` on the current stream: the
+    raster backward into the frame's screen-space sums (ws.grad2d).  Returns
+    the UbsGradBuffers for :func:`backward_chain` (None for an empty scene)."""
     ws = fr.ws
     n = fr.n
     if n == 0:
-        return
+        return None
     gdt = torch.float64 if fr.raster_f64 else torch.float32
     if ws.grad2d is None or ws.grad2d.numel() < n * GRAD2D_STRIDE or ws.grad2d.dtype != gdt:
         ws.grad2d = torch.empty(ws.n_cap * GRAD2D_STRIDE, dtype=gdt, device=ws.device)
@@ -685,10 +695,18 @@ def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_param
     gb.flags = _ptr(ws.flags)
     gb.active = _ptr(ws.active)
     gb.active_count = _ptr(ws.active_count)
-    s = _stream_ptr()
-    check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb, s),
-          "ubs_raster_backward")
-    check(ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, s), "ubs_prim_backward")
+    check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb,
+                                     _stream_ptr()), "ubs_raster_backward")
+    return gb
+
+
+def backward_chain(fr: Frame, gb, add_regularisers: bool = False):
+    """Second half of :func:`backward_frame` on the current stream: the
+    per-primitive chain rule from the screen-space sums into
+    gb.grad_params.  It reads the frame's workspace (grad2d, flags, active),
+    so the workspace must not be reused before it completes."""
+    check(fr.ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, _stream_ptr()),
+          "ubs_prim_backward")
 
 
 def field_slices(n_dims: int) -> dict:

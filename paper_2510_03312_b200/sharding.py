@@ -50,25 +50,33 @@ class GpuViewBackend:
     """Per-view loss + gradient on this rank's GPU through the C-ABI engine.
 
     ``depth`` > 1 keeps that many views in flight: view k of a batch runs on
-    slot k % depth (own stream, workspace and gradient buffer), so one view's
-    latency-bound preprocess / loss / chain kernels overlap another view's
-    raster backward.  Slot gradients are summed into the caller's buffer at
-    :meth:`end` (summation order differs from one-at-a-time accumulation only
-    at the rounding level)."""
+    slot k % depth (own stream and workspace), so one view's latency-bound
+    preprocess / loss / chain kernels overlap another view's raster backward.
+    Views are dispatched in groups of ``group`` that share one preprocess
+    launch (``ubs_preprocess_views``: the scene statics are read once per
+    group).  Every view's per-primitive chain (``prim_bwd``) runs on one
+    gradient stream in view order, adding straight into the batch gradient:
+    the sum is formed in exactly the order of one-at-a-time accumulation, and
+    a slot is reused only after the gradient stream is done with it."""
 
     def __init__(self, ds: engine.DeviceScene, precision: str = "fp32", settings=DEFAULT_SETTINGS,
-                 grad_dtype=torch.float32, depth: int = 1):
+                 grad_dtype=torch.float32, depth: int = 1, group: int = 1):
         self.ds = ds
         self.settings = settings
         self.grad_dtype = grad_dtype
         self.depth = max(1, int(depth))
+        self.group = max(1, min(int(group), self.depth))
         self.workspaces = [engine.Workspace(ds.device, precision) for _ in range(self.depth)]
         self.ws = self.workspaces[0]
-        self.streams = [torch.cuda.Stream(ds.device) for _ in range(self.depth)] if self.depth > 1 else None
-        self.slot_grads = [None] * self.depth
+        multi = self.depth > 1
+        self.streams = [torch.cuda.Stream(ds.device) for _ in range(self.depth)] if multi else None
+        self.lead = torch.cuda.Stream(ds.device) if multi else None  # shared preprocess of a group
+        self.gstream = torch.cuda.Stream(ds.device) if multi else None  # prim_bwd of every view, in order
+        self.slot_free = [None] * self.depth  # gradient-stream event after the slot's last chain
         self._k = 0
         self._grad = None
         self._rec = None
+        self._queue = []
 
     def new_grad(self) -> torch.Tensor:
         return torch.zeros(self.ds.params.shape, dtype=self.grad_dtype, device=self.ds.device)
@@ -78,6 +86,10 @@ class GpuViewBackend:
         ws.loss_parts.zero_()
         g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
         engine.backward_frame(fr, self.ds, g_img, grad)
+        return self._term(fr, parts, cfg)
+
+    @staticmethod
+    def _term(fr, parts, cfg: LossConfig):
         size = fr.width * fr.height * 3
         return (1.0 - cfg.lambda_ssim) * parts[0] / size + cfg.lambda_ssim * (1.0 - parts[1] / size)
 
@@ -93,35 +105,80 @@ class GpuViewBackend:
         self._k = 0
         self._grad = grad
         self._rec = torch.zeros(self.depth, dtype=torch.float64, device=grad.device)
-        for i in range(1, self.depth):
-            if self.slot_grads[i] is None or self.slot_grads[i].shape != grad.shape:
-                self.slot_grads[i] = torch.zeros_like(grad)
-            else:
-                self.slot_grads[i].zero_()
+        self._queue = []
+        if self.depth > 1:
+            self.gstream.wait_stream(torch.cuda.current_stream())  # the caller zeroed grad there
 
     def view(self, cam, query, target, cfg: LossConfig, scale: float, sync: bool = False):
-        i = self._k % self.depth
-        self._k += 1
         if self.depth == 1:
             self._rec[0] += self._view(self.ws, cam, query, target, cfg, scale, self._grad, sync)
             return
-        self.ds.statics_ptr(self.settings)  # on the caller's stream, before any slot reads them
-        s = self.streams[i]
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            g = self._grad if i == 0 else self.slot_grads[i]
-            term = self._view(self.workspaces[i], cam, query, target, cfg, scale, g, sync)
-            self._rec[i:i + 1] += term
+        self._queue.append((cam, query, target, cfg, scale, sync))
+        if len(self._queue) >= self.group or sync:
+            self._flush()
+
+    def _flush(self):
+        queue, self._queue = self._queue, []
+        if not queue:
+            return
+        ds, settings = self.ds, self.settings
+        sync = any(item[5] for item in queue)
+        slots = [(self._k + j) % self.depth for j in range(len(queue))]
+        self._k += len(queue)
+        statics = ds.statics_ptr(settings)  # on the caller's stream, before any slot reads them
+        lead = self.lead
+        lead.wait_stream(torch.cuda.current_stream())
+        for i in slots:
+            lead.wait_stream(self.streams[i])
+            if self.slot_free[i] is not None:
+                lead.wait_event(self.slot_free[i])
+        grouped = bool(statics) and len(queue) > 1 and not sync
+        if grouped:  # one preprocess for the group
+            vs, pbs = [], []
+            with torch.cuda.stream(lead):
+                for (cam, query, *_), i in zip(queue, slots):
+                    v, pb = engine._frame_begin(self.workspaces[i], ds, cam, query, settings, False)
+                    vs.append(v)
+                    pbs.append(pb)
+                ws0 = self.workspaces[slots[0]]
+                engine.check(ws0.lib.ubs_preprocess_views((_lib.UbsView * len(vs))(*vs),
+                                                          (_lib.UbsPrimBuffers * len(pbs))(*pbs), len(vs),
+                                                          0 if ws0.f64 else 1, lead.cuda_stream),
+                             "ubs_preprocess_views")
+        ready = torch.cuda.Event()
+        ready.record(lead)
+        for j, ((cam, query, target, cfg, scale, _), i) in enumerate(zip(queue, slots)):
+            ws, s = self.workspaces[i], self.streams[i]
+            s.wait_event(ready)
+            with torch.cuda.stream(s):
+                if grouped:
+                    fr = engine._frame_end(ws, ds, vs[j], pbs[j], cam, query, settings, False, None, False, False)
+                else:
+                    fr = engine.render_frame(ws, ds, cam, query, settings, sync=sync or ws.pair_cap == 0)
+                ws.loss_parts.zero_()
+                g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
+                gb = engine.backward_raster(fr, ds, g_img, self._grad)
+                self._rec[i:i + 1] += self._term(fr, parts, cfg)
+                done = torch.cuda.Event()
+                done.record(s)
+            if gb is None:
+                continue
+            self.gstream.wait_event(done)
+            with torch.cuda.stream(self.gstream):
+                engine.backward_chain(fr, gb)
+                free = torch.cuda.Event()
+                free.record(self.gstream)
+            self.slot_free[i] = free
 
     def end(self) -> torch.Tensor:
-        """Join the slots, fold their gradients into the batch buffer; returns
-        the summed reconstruction terms (0-d device tensor)."""
+        """Join the slots and the gradient stream; returns the summed
+        reconstruction terms (0-d device tensor)."""
         if self.depth > 1:
+            self._flush()
             cur = torch.cuda.current_stream()
             for s in self.streams:
                 cur.wait_stream(s)
-            for i in range(1, min(self.depth, self._k)):
-                self._grad += self.slot_grads[i]
+            cur.wait_stream(self.gstream)
         return self._rec.sum()
 
     def status(self) -> torch.Tensor:
