@@ -294,7 +294,8 @@ def run_train(a, rank, world, local_rank):
 def run_other_configs(a, dev, frames=64):
     """BASELINE.json configs 1 and 2 on this GPU (informational, single rank):
     3D static 1M primitives and 6D view-dependent 2M primitives, each a
-    64-view 1080p orbit through a FramePipeline of a.inflight frames."""
+    64-view 1080p orbit through a FramePipeline of a.inflight frames, in
+    groups of a.group sharing one preprocess."""
     import torch
     from paper_2510_03312_b200 import engine, synthetic as S
     from paper_2510_03312_b200.types import DEFAULT_SETTINGS
@@ -314,8 +315,12 @@ def run_other_configs(a, dev, frames=64):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ds.invalidate_statics()
             e0.record()
-            for k in range(frames):
-                pipe.render(cams[k], qs[k], DEFAULT_SETTINGS)
+            g = max(a.group, 1)
+            for k0 in range(0, frames, g):
+                if g > 1:
+                    pipe.render_group(list(zip(cams[k0:k0 + g], qs[k0:k0 + g])), DEFAULT_SETTINGS)
+                else:
+                    pipe.render(cams[k0], qs[k0], DEFAULT_SETTINGS)
             pipe.join()
             e1.record()
             torch.cuda.synchronize()
@@ -325,7 +330,7 @@ def run_other_configs(a, dev, frames=64):
             for k in range(frames):
                 pipe.render(cams[k], qs[k], DEFAULT_SETTINGS, sync=True)
         out[name] = {"value": frames / (ms / 1e3), "unit": "frames/s", "frames": frames,
-                     "frames_in_flight": pipe.depth}
+                     "frames_in_flight": pipe.depth, "frames_per_preprocess": max(a.group, 1)}
         del pipe, ds
         torch.cuda.empty_cache()
     return out
