@@ -117,3 +117,32 @@ def test_preprocess_views_matches_per_view(case, precision):
         assert torch.equal(ws.counters[:3], ref_ws.counters[:3])
         assert torch.equal(fr.n_contrib, want.n_contrib)
         assert torch.equal(fr.image, want.image)
+
+
+def test_preprocess_views_rejects_mixed_scenes():
+    """ubs_preprocess_views serves views of ONE scene: a view of another
+    scene, a view without statics and an empty group are argument errors."""
+    from paper_2510_03312_b200 import _lib
+    lib = _lib.load()
+    a = engine.DeviceScene.from_scene(S.synth(7, 500, seed=1), device="cuda")
+    b = engine.DeviceScene.from_scene(S.synth(7, 500, seed=2), device="cuda")
+    cam = S.bench_camera(64, 48)
+    q = S.bench_query(7, cam, 0.5)
+    wss = [engine.Workspace("cuda", "fp32") for _ in range(2)]
+    s = torch.cuda.current_stream().cuda_stream
+
+    def call(scenes):
+        vs, pbs = [], []
+        for ds, ws in zip(scenes, wss):
+            v, pb = engine._frame_begin(ws, ds, cam, q, DEFAULT_SETTINGS, False)
+            vs.append(v)
+            pbs.append(pb)
+        return lib.ubs_preprocess_views((_lib.UbsView * len(vs))(*vs), (_lib.UbsPrimBuffers * len(pbs))(*pbs),
+                                        len(vs), 1, s)
+
+    assert call([a, a]) == 0
+    assert call([a, b]) == _lib.UBS_E_ARGS
+    a.use_statics = False
+    assert call([a, a]) == _lib.UBS_E_ARGS
+    assert lib.ubs_preprocess_views(None, None, 0, 1, s) == _lib.UBS_E_ARGS
+    torch.cuda.synchronize()
