@@ -300,13 +300,10 @@ template <int C, typename PT>
 static int launch_views(const PreViews &m, cudaStream_t s) {
     using L = StaticLayout<C>;
     constexpr size_t kBlockBytes = (size_t)kStaticBlock * (8 * L::D + sizeof(PT) * L::R);
-    static bool attr = false;  // per process; the attribute is per function
-    if (!attr) {
-        if (cudaFuncSetAttribute(preprocess_views_kernel<C, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kBlockBytes) != cudaSuccess)
-            return UBS_E_CUDA;
-        attr = true;
-    }
+    // (a host-side attribute write, once per group launch; no cached state)
+    if (cudaFuncSetAttribute(preprocess_views_kernel<C, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kBlockBytes) != cudaSuccess)
+        return UBS_E_CUDA;
     const int64_t blocks = (m.v[0].n + kPreThreads - 1) / kPreThreads;
     preprocess_views_kernel<C, PT><<<(unsigned)blocks, kPreThreads, kBlockBytes, s>>>(m);
     return UBS_OK;
