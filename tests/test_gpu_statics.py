@@ -86,14 +86,15 @@ def test_statics_follow_parameter_updates():
     assert ds.statics_ptr(DEFAULT_SETTINGS) and ds._statics_key[1] == ds.params._version
 
 
-@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("precision,dtype", [("fp32", torch.float32), ("fp64", torch.float32),
+                                             ("fp64", torch.float64)])
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
-def test_preprocess_views_matches_per_view(case, precision):
+def test_preprocess_views_matches_per_view(case, precision, dtype):
     """ubs_preprocess_views (one statics read for a group of frames) gives
     every frame exactly the bits of its own ubs_preprocess: per-primitive
     outputs, counters and the rendered frame.  10 views: two launches."""
     _, sc, cam, q = case
-    ds = engine.DeviceScene.from_scene(sc, dtype=torch.float32, device="cuda")
+    ds = engine.DeviceScene.from_scene(sc, dtype=dtype, device="cuda")
     nd = sc.n_dims
     views = [(cam, q)]  # the case's own view, then an orbit with a time sweep
     for k in range(1, 10):
