@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--inflight", type=int, default=16, help="frames in flight (engine.FramePipeline depth)")
+    ap.add_argument("--slot-priority", type=int, default=0, help="CUDA stream priority of the frame slots")
+    ap.add_argument("--lead-priority", type=int, default=0, help="CUDA stream priority of the group preprocess")
     ap.add_argument("--group", type=int, default=4,
                     help="frames per shared preprocess (FramePipeline.render_group; 0: frame by frame)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -351,7 +353,8 @@ def run_ours(a, rank, world, local_rank):
     # the sweep renders through a pipeline of `inflight` frames (own stream and
     # workspace each); the per-stage breakdown uses one extra single-stream
     # workspace so its event times are not inflated by the overlap
-    pipe = engine.FramePipeline(ds, max(a.inflight, 1), a.precision, dev)
+    pipe = engine.FramePipeline(ds, max(a.inflight, 1), a.precision, dev, slot_priority=a.slot_priority,
+                                lead_priority=a.lead_priority)
     ws = engine.Workspace(dev, a.precision)
 
     def frame(k, timers=None, sync=False):

@@ -509,16 +509,17 @@ class FramePipeline:
     again (``depth`` frames later); consume it on ``stream_of(frame)`` or
     after :meth:`join`."""
 
-    def __init__(self, ds: DeviceScene, depth: int = 3, precision: str = "fp32", device=None):
+    def __init__(self, ds: DeviceScene, depth: int = 3, precision: str = "fp32", device=None,
+                 slot_priority: int = 0, lead_priority: int = 0):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         dev = _require_cuda(device if device is not None else ds.device)
         self.ds = ds
         self.workspaces = [Workspace(dev, precision) for _ in range(depth)]
-        self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
+        self.streams = [torch.cuda.Stream(dev, priority=slot_priority) for _ in range(depth)]
         self.pending = [None] * depth  # event a slot's next frame must wait for (a consumer of its buffers)
         self.k = 0
-        self.lead = torch.cuda.Stream(dev)  # render_group's shared preprocess
+        self.lead = torch.cuda.Stream(dev, priority=lead_priority)  # render_group's shared preprocess
 
     @property
     def depth(self) -> int:
