@@ -51,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 3
+#define UBS_ABI_VERSION 4
 #define UBS_TILE 16
 
 enum {
@@ -184,6 +184,9 @@ typedef struct UbsGradBuffers {
     const uint16_t *flags; /* UbsPrimBuffers.flags of this view (for the skip test), or NULL */
     uint32_t *active;    /* n scratch: primitives the chain must visit, or NULL (visit all) */
     uint32_t *active_count; /* [1] scratch counter */
+    int32_t bwd_pixels_per_lane; /* fp32 raster backward layout: 0 or 2 = two pixels per lane (fastest
+                                    alone), 4 = four pixels per lane in smaller CTAs (fastest beside
+                                    other frames' kernels, e.g. views in flight); same results */
 } UbsGradBuffers;
 
 /* --- entry points --- */

@@ -68,10 +68,11 @@ class UbsImageBuffers(Structure):
 class UbsGradBuffers(Structure):
     _fields_ = [("g_image", c_void_p), ("grad2d", c_void_p), ("grad_params", c_void_p), ("grad_f64", c_int32),
                 ("grad2d_f64", c_int32), ("reg_opacity", c_double), ("reg_scale", c_double),
-                ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p)]
+                ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p),
+                ("bwd_pixels_per_lane", c_int32)]
 
 
-ABI_VERSION = 3  # UBS_ABI_VERSION in include/ubs_b200.h
+ABI_VERSION = 4  # UBS_ABI_VERSION in include/ubs_b200.h
 MAX_VIEWS = 8  # UBS_MAX_VIEWS
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares

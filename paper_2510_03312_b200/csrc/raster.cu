@@ -716,9 +716,12 @@ raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 // 8x4 blocks wide at the benchmark scales, so the union visits far fewer
 // (warp, splat) pairs than the blocks separately, and the reduce + atomic --
 // more than half of a visit's instructions -- is paid once per pair.  NP = 2
-// (7D 3M view: 5.2 M -> 2.84 M reductions, 843 -> 737 us); NP = 4 removes
-// another 20% of the instructions but at 92 registers runs no faster.
-constexpr int kBwdPixels = 2;
+// (7D 3M view: 5.2 M -> 2.84 M reductions, 843 -> 737 us).  NP = 4 (64
+// threads per tile, 128-record batches, the pixels' read-only state in
+// shared memory) removes another 20% of the instructions: alone it runs ~8%
+// slower (fewer, longer warps), beside other views' kernels (the training
+// backend's views in flight) ~2% of the step faster; the caller picks
+// (UbsGradBuffers.bwd_pixels_per_lane).
 
 
 struct BwdPixel {
@@ -726,7 +729,7 @@ struct BwdPixel {
     int cnt;
 };
 
-__device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float4 r0, const float4 r1, uint32_t ra, float tau,
+__device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float g0, const float g1, const float g2, const float4 r0, const float4 r1, uint32_t ra, float tau,
                                           float inv_tau, float clamp, float one_minus_clamp, float (&v)[16]) {
     constexpr float kLn2 = 0.6931471805599453f;
     const float dx = (p.pxf - r0.x) + r0.z;
@@ -749,10 +752,10 @@ __device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float4 r0, const fl
     const float iom = rcp_approx(om);
     const float ti = p.T * iom;
     const float w = a * ti;
-    v[7] += w * p.g0;
-    v[8] += w * p.g1;
-    v[9] += w * p.g2;
-    const float gc = fmaf(p.g0, r2.y, fmaf(p.g1, r2.z, p.g2 * r2.w));
+    v[7] += w * g0;
+    v[8] += w * g1;
+    v[9] += w * g2;
+    const float gc = fmaf(g0, r2.y, fmaf(g1, r2.z, g2 * r2.w));
     const float ga = fmaf(gc, ti, -p.suffix * iom);
     p.suffix = fmaf(gc, w, p.suffix);
     p.T = ti;
@@ -774,20 +777,24 @@ __device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float4 r0, const fl
 }
 
 template <int NP>
-__global__ void __launch_bounds__(kTileThreads / NP, 8)  // 64 registers: 8 CTAs per SM
+__global__ void __launch_bounds__(kTileThreads / NP, 4 * NP)  // 64 registers: 4 NP CTAs per SM
 raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                     const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
                     float *__restrict__ grad2d) {
     constexpr int kThreads = kTileThreads / NP;
     constexpr int kWarps = kThreads / 32;
-    constexpr int kBatch = 256;  // 2 records per thread: half the barriers of a 128 batch
+    constexpr int kBatch = NP >= 4 ? 128 : 256;  // NP = 2: 2 records per thread, half the barriers of 128
     constexpr int kWords = kBatch / 32;
     constexpr int kBlocks = kTileThreads / 32;  // the forward's 8x4 blocks per tile
     __shared__ Rec32 srec[kBatch];
     __shared__ uint32_t sid[kBatch];
     __shared__ uint32_t swm[kBlocks][kWords];  // [8x4 block][batch word] ballot words
     __shared__ int smax;
+    // NP >= 4: each pixel's read-only state (g_image, contributor count) lives
+    // in shared memory instead of registers
+    constexpr bool kSmemG = NP >= 4;
+    __shared__ float4 sg[kSmemG ? NP : 1][kSmemG ? kThreads : 1];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
@@ -818,6 +825,7 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         }
         p.suffix = (p.g0 * (float)P.bg[0] + p.g1 * (float)P.bg[1] + p.g2 * (float)P.bg[2]) * p.T;
         my_max = max(my_max, p.cnt);
+        if constexpr (kSmemG) sg[h][threadIdx.x] = make_float4(p.g0, p.g1, p.g2, __int_as_float(p.cnt));
     }
     int warp_cnt = my_max;  // this warp's largest contributor count: splats beyond it are skipped
 #pragma unroll
@@ -874,9 +882,18 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 float v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
                 bool contrib = false;
 #pragma unroll
-                for (int h = 0; h < NP; ++h)
-                    if ((wr[h] & bm) && lo + jj < px[h].cnt)
-                        contrib |= bwd_visit(px[h], r0, r1, ra, tau, inv_tau, clamp, one_minus_clamp, v);
+                for (int h = 0; h < NP; ++h) {
+                    if (!(wr[h] & bm)) continue;
+                    if constexpr (kSmemG) {
+                        const float4 gq = sg[h][threadIdx.x];
+                        if (lo + jj < __float_as_int(gq.w))
+                            contrib |= bwd_visit(px[h], gq.x, gq.y, gq.z, r0, r1, ra, tau, inv_tau, clamp,
+                                                 one_minus_clamp, v);
+                    } else if (lo + jj < px[h].cnt) {
+                        contrib |= bwd_visit(px[h], px[h].g0, px[h].g1, px[h].g2, r0, r1, ra, tau, inv_tau, clamp,
+                                             one_minus_clamp, v);
+                    }
+                }
                 if (__any_sync(0xffffffffu, contrib)) {
                     int idx = 0;
                     float mine = 0.0f;
@@ -933,6 +950,8 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
                                    const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t stream) {
     if (!v || !pb || !bb || !ib || !gb || !gb->g_image || !gb->grad2d) return UBS_E_ARGS;
     if ((gb->grad2d_f64 != 0) != (ib->raster_f64 != 0)) return UBS_E_ARGS;
+    if (gb->bwd_pixels_per_lane != 0 && gb->bwd_pixels_per_lane != 2 && gb->bwd_pixels_per_lane != 4)
+        return UBS_E_ARGS;
     const RasterParams P = make_params(*v, *pb, *bb);
     const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
     cudaStream_t s = (cudaStream_t)stream;
@@ -941,9 +960,14 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
             P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
             (const double *)gb->g_image, (double *)gb->grad2d);
     } else {
-        raster_bwd32_kernel<kBwdPixels><<<n_tiles, kTileThreads / kBwdPixels, 0, s>>>(
-            P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
-            (const float *)gb->g_image, (float *)gb->grad2d);
+        if (gb->bwd_pixels_per_lane == 4)
+            raster_bwd32_kernel<4><<<n_tiles, kTileThreads / 4, 0, s>>>(
+                P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
+                (const float *)gb->g_image, (float *)gb->grad2d);
+        else
+            raster_bwd32_kernel<2><<<n_tiles, kTileThreads / 2, 0, s>>>(
+                P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
+                (const float *)gb->g_image, (float *)gb->grad2d);
     }
     UBS_CUDA_CHECK();
     return UBS_OK;

@@ -667,10 +667,12 @@ def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_param
 
 
 def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
-                    reg_opacity: float = 0.0, reg_scale: float = 0.0):
+                    reg_opacity: float = 0.0, reg_scale: float = 0.0, pixels_per_lane: int = 2):
     """First half of :func:`backward_frame` on the current stream: the
     raster backward into the frame's screen-space sums (ws.grad2d).  Returns
-    the UbsGradBuffers for :func:`backward_chain` (None for an empty scene)."""
+    the UbsGradBuffers for :func:`backward_chain` (None for an empty scene).
+    ``pixels_per_lane`` picks the fp32 raster backward's layout (2: fastest
+    alone, 4: fastest beside other views' kernels; same results)."""
     ws = fr.ws
     n = fr.n
     if n == 0:
@@ -696,6 +698,7 @@ def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_para
     gb.flags = _ptr(ws.flags)
     gb.active = _ptr(ws.active)
     gb.active_count = _ptr(ws.active_count)
+    gb.bwd_pixels_per_lane = int(pixels_per_lane)
     check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb,
                                      _stream_ptr()), "ubs_raster_backward")
     return gb

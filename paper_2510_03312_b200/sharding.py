@@ -157,7 +157,8 @@ class GpuViewBackend:
                     fr = engine.render_frame(ws, ds, cam, query, settings, sync=sync or ws.pair_cap == 0)
                 ws.loss_parts.zero_()
                 g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
-                gb = engine.backward_raster(fr, ds, g_img, self._grad)
+                # four pixels per lane: the layout that runs best beside the other views in flight
+                gb = engine.backward_raster(fr, ds, g_img, self._grad, pixels_per_lane=4)
                 self._rec[i:i + 1] += self._term(fr, parts, cfg)
                 done = torch.cuda.Event()
                 done.record(s)

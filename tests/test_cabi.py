@@ -27,7 +27,7 @@ def header_functions():
 def test_library_builds_and_loads():
     build.build()
     lib = _lib.load(build_if_needed=False)
-    assert lib.ubs_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.ubs_abi_version() == _lib.ABI_VERSION == 4
     assert b"sm_100a" in lib.ubs_build_info()
 
 

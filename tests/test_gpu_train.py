@@ -63,3 +63,29 @@ def test_batched_backend_trains():
         losses.append(float(loss))
         adam.step(grad)
     assert np.isfinite(losses).all() and losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("w,h", [(77, 53), (160, 120), (33, 17)])
+def test_backward_layouts_agree(w, h):
+    """The fp32 raster backward's two layouts (2 or 4 pixels per lane) give
+    the same gradient up to float-atomic summation order, on ragged images
+    whose last tiles are partly outside; an invalid layout is an error."""
+    from paper_2510_03312_b200 import _lib
+    nd = 7
+    ds = engine.DeviceScene.from_scene(S.synth(nd, 4000, seed=9), device="cuda")
+    cam = S.bench_camera(w, h)
+    q = S.bench_query(nd, cam, 0.4)
+    ws = engine.Workspace("cuda", "fp32")
+    fr = engine.render_frame(ws, ds, cam, q)
+    g_img = torch.randn(h, w, 3, device="cuda")
+    grads = []
+    for ppl in (2, 4):
+        g = torch.zeros(ds.params.shape, device="cuda")
+        gb = engine.backward_raster(fr, ds, g_img, g, pixels_per_lane=ppl)
+        engine.backward_chain(fr, gb)
+        grads.append(g.double())
+    a, b = grads
+    assert float(b.norm()) > 0.0
+    assert float((a - b).norm()) <= 1e-5 * float(b.norm())
+    with pytest.raises(_lib.UbsError):
+        engine.backward_raster(fr, ds, g_img, torch.zeros(ds.params.shape, device="cuda"), pixels_per_lane=3)
