@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--train-views-per-gpu", type=int, default=8)
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-inflight", type=int, default=8, help="views in flight per GPU in the training step")
-    ap.add_argument("--train-group", type=int, default=4, help="training views per shared preprocess")
+    ap.add_argument("--train-group", type=int, default=8, help="training views per shared preprocess")
     ap.add_argument("--train-only", action="store_true",
                     help="only the config-5 training step (its own JSON line; for profiling)")
     return ap.parse_args()
