@@ -490,14 +490,28 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ds.invalidate_statics()
-    f0.record()
-    submit(0, a.steps)
-    pipe.join()
-    torch.cuda.current_stream().wait_stream(sink.copy_stream)
-    f1.record()
-    torch.cuda.synchronize()
-    pipe.check_status()
+    for attempt in range(3):
+        ds.invalidate_statics()
+        f0.record()
+        submit(0, a.steps)
+        pipe.join()
+        torch.cuda.current_stream().wait_stream(sink.copy_stream)
+        f1.record()
+        torch.cuda.synchronize()
+        # as in the headline sweep: an asynchronous frame that outgrew its slot
+        # (frames land on other slots than in that sweep) means re-time after growing
+        bad = pipe.status().to(torch.int32)
+        if world > 1:
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()) == 0:
+            break
+        pipe.clear_status()
+        for k in range(a.steps):
+            frame(k, sync=True)
+        sink.synchronize()
+        torch.cuda.synchronize()
+    else:
+        raise RuntimeError("pair-buffer overflow persisted in the end-to-end sweep")
     barrier()
     te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
     if world > 1:
