@@ -329,8 +329,7 @@ def run_other_configs(a, dev, frames=64):
             ms = e0.elapsed_time(e1)
             if int(pipe.status().item()) == 0:
                 break
-            for k in range(frames):
-                pipe.render(cams[k], qs[k], DEFAULT_SETTINGS, sync=True)
+            pipe.grow()
         out[name] = {"value": frames / (ms / 1e3), "unit": "frames/s", "frames": frames,
                      "frames_in_flight": pipe.depth, "frames_per_preprocess": max(a.group, 1)}
         del pipe, ds
@@ -426,7 +425,7 @@ def run_ours(a, rank, world, local_rank):
 
     # the headline sweep carries no per-stage events (they cost ~3.5%); a second,
     # instrumented sweep below gives the stage breakdown
-    for attempt in range(2):
+    for attempt in range(3):
         ms, _, clocks, fr = timed_sweep()
         host_enqueue_ms = host_ms[0]
         # no async frame may have outgrown its pair buffers (decided jointly by all ranks)
@@ -435,9 +434,7 @@ def run_ours(a, rank, world, local_rank):
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()) == 0:
             break
-        pipe.clear_status()
-        for k in range(a.steps):  # grow the buffers with synchronous frames, then re-time
-            frame(k, sync=True)
+        pipe.grow()  # every slot sized for what any slot needed, then re-time
     else:
         raise RuntimeError("pair-buffer overflow persisted")
     fixed = fr.n_fixed
@@ -505,9 +502,7 @@ def run_ours(a, rank, world, local_rank):
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()) == 0:
             break
-        pipe.clear_status()
-        for k in range(a.steps):
-            frame(k, sync=True)
+        pipe.grow()
         sink.synchronize()
         torch.cuda.synchronize()
     else:

@@ -618,6 +618,31 @@ class FramePipeline:
         for ws in self.workspaces:
             ws.status.zero_()
 
+    def grow(self) -> int:
+        """After asynchronous frames outgrew their slots (``status()`` nonzero):
+        give every slot the largest tile-list cap any slot has -- doubled if a
+        list was truncated -- and pair buffers for the largest tile-pair count
+        any slot last saw, then clear the status.  A frame may land on any
+        slot, so growing only the slot that overflowed is not enough.  Syncs;
+        returns the status that was cleared."""
+        self.join()
+        torch.cuda.current_stream().synchronize()
+        st = 0
+        for ws in self.workspaces:
+            st |= int(ws.status.item())
+        cap = max(ws.list_cap for ws in self.workspaces)
+        if st & _lib.S_LIST_TRUNC:
+            cap *= 2
+        k = max(int(ws.counters[0].item()) for ws in self.workspaces)
+        if st & _lib.S_PAIR_OVERFLOW:  # the overflowing frame need not be any slot's last one
+            k = max(k, int(max(ws.pair_cap for ws in self.workspaces) * 1.3) + 1)
+        for ws in self.workspaces:
+            ws.list_cap = cap
+            if ws.temp_bytes:
+                ws.ensure_pairs(k)
+            ws.status.zero_()
+        return st
+
     def status(self) -> torch.Tensor:
         """OR of the slots' device status words (no sync)."""
         out = self.workspaces[0].status.clone()

@@ -385,3 +385,42 @@ def test_grouped_pipeline_zero_copy_host_sink():
     assert pipe.check_status() == 0
     for a, b in zip(ref, outs):
         assert torch.equal(a, b)
+
+
+def test_pipeline_grow_sizes_every_slot():
+    # a frame that needs a larger tile-list cap than its slot has sets
+    # UBS_S_LIST_TRUNC; grow() gives every slot the doubled cap, so the same
+    # frames re-rendered asynchronously on any slot no longer overflow
+    import torch
+    from paper_2510_03312_b200 import engine, _lib
+    sc = quantize_f32(S.random_scene(7, 4000, seed=81))
+    cam = S.random_camera(64, 82)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    qs = [S.random_query(7, 83 + k) for k in range(5)]
+    ref = [engine.render_frame(ws, ds, cam, q, RenderSettings(transmittance_min=0.0)).image.clone() for q in qs]
+    pipe = engine.FramePipeline(ds, depth=2)
+    for w in pipe.workspaces:
+        w.list_cap = 8  # far below what these tiles need
+    settings = RenderSettings(transmittance_min=0.0)  # no early exit: every list is walked to its end
+    for q in qs:
+        pipe.render(cam, q, settings, sync=True)  # sizes pair buffers (and grows the caps) slot by slot
+    for w in pipe.workspaces:
+        w.list_cap = 8
+    for q in qs:
+        pipe.render(cam, q, settings)
+    pipe.join()
+    assert int(pipe.status().item()) & _lib.S_LIST_TRUNC
+    for _ in range(12):  # the cap doubles per round: 8 -> 32768
+        pipe.grow()
+        got = []
+        for q in qs:
+            fr = pipe.render(cam, q, settings)
+            with torch.cuda.stream(pipe.stream_of(fr)):
+                got.append(fr.image.clone())
+        pipe.join()
+        if int(pipe.status().item()) == 0:
+            break
+    assert int(pipe.status().item()) == 0
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
