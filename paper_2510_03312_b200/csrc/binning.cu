@@ -18,6 +18,12 @@
 
 #include "ubs_common.cuh"
 
+// At most 2^20 depth buckets: their 4 MB of cursors stay L2-resident under the
+// scatter's one random atomic per element (2^24 buckets at 10M primitives:
+// depth scatter 656 us; capped: bin_depth 0.98 -> 0.59 ms, 390 -> 457 fps).
+#ifndef UBS_SORT_MAX_LOG
+#define UBS_SORT_MAX_LOG 20
+#endif
 namespace ubs {
 
 // Depth order = lexsort((ids, depth)) (raster.py:274-275) as a bucket sort.
@@ -33,7 +39,7 @@ constexpr uint64_t kNoRect = ~0ull;  // rect_sorted entry of a primitive that to
 
 __host__ __device__ inline int sort_log_buckets(int64_t n) {
     int l = 12;
-    while (l < 24 && ((int64_t)1 << l) < n) ++l;
+    while (l < UBS_SORT_MAX_LOG && ((int64_t)1 << l) < n) ++l;
     return l;
 }
 
