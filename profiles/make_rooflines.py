@@ -12,7 +12,10 @@ issue.json: per kernel, warp instructions / duration against the issue peak
 148 SMs x 4 schedulers x 1 warp-instruction per clock at the captured SM
 clock (bench.py's ``issue_roofline`` for the dominant stage).
 
-    python profiles/make_rooflines.py profiles/r01_ncu_full_v5_raw.csv
+    python profiles/make_rooflines.py profiles/r01_ncu_full_v5_raw.csv [more captures ...]
+
+Several captures may be given (e.g. the frame's kernels and the training
+step's raster backward); a kernel is taken from the first file holding it.
 """
 
 from __future__ import annotations
@@ -30,6 +33,7 @@ STAGES = [
     (r"bucket_|tile_lists", "bin_tiles"),
     (r"raster_fwd", "raster"),
     (r"raster_fixup", "fixup"),
+    (r"raster_bwd", "train_raster_bwd"),
 ]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3, "us": 1.0,
          "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "hz": 1.0, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9,
@@ -48,7 +52,24 @@ def short(name: str) -> str:
     return re.sub(r"\(.*$", "", name)
 
 
-def main(path: str):
+def main(paths):
+    traffic, issue, seen = {}, {}, set()
+    for path in paths:
+        scan(path, traffic, issue, seen)
+    src = ", ".join(f"profiles/{Path(p).name}" for p in paths)
+    traffic["_source"] = (f"{src}: dram__bytes_read.sum + dram__bytes_write.sum per launch, summed over "
+                          "the stage's kernels, each kernel counted once (profiles/make_rooflines.py)")
+    issue["_source"] = f"{src} (profiles/make_rooflines.py)"
+    out = Path(__file__).resolve().parent
+    (out / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    (out / "issue.json").write_text(json.dumps(issue, indent=1) + "\n")
+    for k, v in issue.items():
+        if isinstance(v, dict):
+            print(f"{k[:60]:60s} {v['stage']:16s} {v['duration_us']:8.1f} us  issue {v['frac']:.2f}")
+    print({k: round(v / 1e6, 1) for k, v in traffic.items() if not k.startswith("_")}, "MB")
+
+
+def scan(path, traffic, issue, seen):
     rows = list(csv.reader(open(path)))
     head, units = rows[0], rows[1]
 
@@ -56,7 +77,6 @@ def main(path: str):
         i = head.index(key)
         return float(row[i].replace(",", "")) * SCALE.get(units[i], 1.0)
 
-    traffic, issue, seen = {}, {}, set()
     for row in rows[2:]:
         name = short(row[head.index("Kernel Name")])
         st = stage_of(name)
@@ -71,18 +91,7 @@ def main(path: str):
         issue[name] = {"stage": st, "warp_instructions": inst, "duration_us": dur_us, "sm_clock_hz": clk,
                        "achieved_warp_inst_per_s": inst / (dur_us * 1e-6), "peak_warp_inst_per_s": peak,
                        "frac": inst / (dur_us * 1e-6) / peak}
-    src = Path(path).name
-    traffic["_source"] = (f"profiles/{src}: dram__bytes_read.sum + dram__bytes_write.sum per launch, summed over "
-                          "the stage's kernels, each kernel counted once (profiles/make_rooflines.py)")
-    issue["_source"] = f"profiles/{src} (profiles/make_rooflines.py)"
-    out = Path(__file__).resolve().parent
-    (out / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
-    (out / "issue.json").write_text(json.dumps(issue, indent=1) + "\n")
-    for k, v in issue.items():
-        if isinstance(v, dict):
-            print(f"{k[:60]:60s} {v['stage']:10s} {v['duration_us']:8.1f} us  issue {v['frac']:.2f}")
-    print({k: round(v / 1e6, 1) for k, v in traffic.items() if not k.startswith("_")}, "MB")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1:])
