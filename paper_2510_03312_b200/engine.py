@@ -114,9 +114,16 @@ class DeviceScene:
     def from_scene(cls, scene, dtype=torch.float32, device="cuda") -> "DeviceScene":
         dev = _require_cuda(device)
         npdt = np.float64 if dtype == torch.float64 else np.float32
-        rec = pack_records(scene, npdt)
-        t = torch.from_numpy(rec).to(dev, non_blocking=False)
-        return cls(t, scene.n_dims, scene.background)
+        n = int(np.asarray(scene.mu_x).shape[0])
+        if n == 0:
+            return cls(torch.from_numpy(pack_records(scene, npdt)).to(dev), scene.n_dims, scene.background)
+        # each field uploaded as float64 (no host pass for contiguous float64 arrays),
+        # interleaved and cast on the device: round-to-nearest-even, the same bits
+        # as pack_records' host cast
+        cols = [torch.from_numpy(np.ascontiguousarray(
+                    np.asarray(getattr(scene, k), dtype=np.float64).reshape(n, -1))).to(dev)
+                for k, _ in PARAM_FIELDS]
+        return cls(torch.cat(cols, dim=1).to(dtype).contiguous(), scene.n_dims, scene.background)
 
     @property
     def n(self) -> int:

@@ -23,7 +23,7 @@ import torch
 
 from . import engine
 from ._lib import DEBUG_STRIDE, F_DEGENERATE, F_FLOOR2, F_FLOOR3, F_VISIBLE
-from .types import DEFAULT_SETTINGS
+from .types import PARAM_FIELDS, DEFAULT_SETTINGS
 
 DEFAULT_PRECISION = "fp32"
 _WORKSPACES: dict = {}
@@ -42,17 +42,48 @@ def workspace(precision: str | None = None, device=None) -> engine.Workspace:
     return ws
 
 
+_PINNED: dict = {}  # tag -> the reused pinned host staging buffer (latest shape only)
+
+
+def _pinned(tag, shape, dtype) -> torch.Tensor:
+    buf = _PINNED.get(tag)
+    if buf is None or tuple(buf.shape) != tuple(shape) or buf.dtype != dtype:
+        buf = torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
+        _PINNED[tag] = buf
+    return buf
+
+
 def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
-    # re-uploaded every call: callers such as fd_check mutate arrays in place,
-    # so a cached copy keyed on identity would go stale
+    """The scene's records on the workspace's device, re-uploaded every call
+    (callers such as fd_check mutate arrays in place, so a copy kept across
+    calls could go stale).  Each field goes through a reused pinned staging
+    buffer (a contiguous host copy, then DMA; pageable uploads of the 300 MB
+    of float64 fields at 1M primitives ran at ~2 GB/s) and the fields are
+    interleaved and cast on the device: the bits of pack_records' host cast.
+    The staging buffers are reused by the next call only after this call's
+    result has been read back (every numpy entry point synchronises)."""
     dtype = torch.float64 if ws.f64 else torch.float32
-    return engine.DeviceScene.from_scene(scene, dtype=dtype, device=ws.device)
+    n = int(np.asarray(scene.mu_x).shape[0])
+    if n == 0 or not torch.cuda.is_available():
+        return engine.DeviceScene.from_scene(scene, dtype=dtype, device=ws.device)
+    torch.cuda.current_stream(ws.device).synchronize()  # the previous call's uploads are done
+    cols = []
+    for k, _ in PARAM_FIELDS:
+        a = np.asarray(getattr(scene, k)).reshape(n, -1)
+        st = _pinned(k, a.shape, torch.float64)
+        np.copyto(st.numpy(), a, casting="unsafe")
+        cols.append(st.to(ws.device, non_blocking=True))
+    params = torch.cat(cols, dim=1).to(dtype).contiguous()
+    return engine.DeviceScene(params, scene.n_dims, scene.background)
 
 
 def _host_image(fr: engine.Frame, background) -> np.ndarray:
     """(H, W, 3) float64; pixels nothing was composited into get the exact fp64
     background (acc = 0, T = 1 gives 0 + 1 * bg in tile_forward, _tiles.py:51-53)."""
-    img = fr.image.double().cpu().numpy().reshape(fr.height, fr.width, 3)
+    st = _pinned("image", (fr.height, fr.width, 3), torch.float64)
+    st.copy_(fr.image.view(fr.height, fr.width, 3).double(), non_blocking=True)
+    torch.cuda.current_stream(fr.image.device).synchronize()
+    img = st.numpy().copy()
     if not fr.raster_f64:
         empty = ((fr.alpha_sum == 0) & (fr.t_stop == 1)).cpu().numpy()
         if empty.any():
@@ -65,8 +96,9 @@ class FrameCache:
 
     Eager: image, alpha_sum, t_stop, alpha_clamped, processed_pixels, order,
     n_contrib (per-pixel contributor count, not in the reference).
-    Lazy: ``tiles`` (per-tile id lists), ``slices`` / ``proj`` (a subset of the
-    reference's SliceCache / ProjectionCache fields, from a debug re-run).
+    Lazy, from a re-run of the same frame: ``tiles`` / ``tile_ranges`` /
+    ``tile_ids`` (the full per-tile id lists), ``slices`` / ``proj`` (a subset
+    of the reference's SliceCache / ProjectionCache fields, from a debug run).
     """
 
     def __init__(self, scene, camera, query, settings, precision, fr: engine.Frame):
@@ -82,13 +114,36 @@ class FrameCache:
         self.n_fixed = 0 if fr.raster_f64 else fr.n_fixed
         ws = fr.ws
         self.order = ws.order[:fr.n_visible].to(torch.int64).cpu().numpy()
-        ntiles = math.ceil(W / 16) * math.ceil(H / 16)
-        self.tile_ranges = ws.tile_ranges[:2 * ntiles].view(ntiles, 2).to(torch.int64).cpu().numpy()
-        self.tile_ids = ws.tile_ids[:fr.n_pairs].to(torch.int64).cpu().numpy() if fr.n_pairs else \
-            np.zeros(0, dtype=np.int64)
         self._flags = ws.flags[:fr.n].to(torch.int32).cpu().numpy() & 0xFFFF
         self._tiles = None
+        self._tile_ranges = None
+        self._tile_ids = None
         self._debug = None
+
+    def _load_tiles(self):
+        # the full per-tile lists (K ids, ~26M at 7D 1M 1080p) are copied only
+        # when asked for, from a re-run that materialises every list
+        if self._tile_ids is None:
+            ws = workspace(self.precision)
+            ds = _device_scene(self.scene, ws)
+            fr = engine.render_frame(ws, ds, self.camera, self.query, self.settings, full_lists=True)
+            W, H = int(self.camera.width), int(self.camera.height)
+            ntiles = math.ceil(W / 16) * math.ceil(H / 16)
+            self._tile_ranges = ws.tile_ranges[:2 * ntiles].view(ntiles, 2).to(torch.int64).cpu().numpy()
+            self._tile_ids = ws.tile_ids[:fr.n_pairs].to(torch.int64).cpu().numpy() if fr.n_pairs else \
+                np.zeros(0, dtype=np.int64)
+
+    @property
+    def tile_ranges(self) -> np.ndarray:
+        """(ntiles, 2) [start, end) of each tile's list in ``tile_ids`` (lazy)."""
+        self._load_tiles()
+        return self._tile_ranges
+
+    @property
+    def tile_ids(self) -> np.ndarray:
+        """Every tile's depth-ordered primitive ids, concatenated (lazy)."""
+        self._load_tiles()
+        return self._tile_ids
 
     @property
     def tiles(self) -> list:
@@ -151,7 +206,7 @@ def render_with_cache(scene, cam, query, settings=DEFAULT_SETTINGS, *, precision
         raise ValueError(f"query has {np.asarray(query.dims).size} dims, scene expects {c}")
     ws = workspace(precision, device)
     ds = _device_scene(scene, ws)
-    fr = engine.render_frame(ws, ds, cam, query, settings, full_lists=True)
+    fr = engine.render_frame(ws, ds, cam, query, settings)
     return FrameCache(scene, cam, query, settings, ws.precision, fr)
 
 

@@ -149,8 +149,13 @@ def pack_records(scene, dtype=np.float32) -> np.ndarray:
     width = record_width(scene.n_dims)
     if n == 0:
         return np.zeros((0, width), dtype=dtype)
-    parts = [np.asarray(getattr(scene, k), dtype=np.float64).reshape(n, -1) for k, _ in PARAM_FIELDS]
-    return np.ascontiguousarray(np.concatenate(parts, axis=1).astype(dtype))
+    out = np.empty((n, width), dtype=dtype)
+    off = 0
+    for k, _ in PARAM_FIELDS:  # one cast-and-copy pass per field (values as float64 -> dtype)
+        part = np.asarray(getattr(scene, k), dtype=np.float64).reshape(n, -1)
+        out[:, off:off + part.shape[1]] = part
+        off += part.shape[1]
+    return out
 
 
 def quantize_f32(scene) -> Scene:

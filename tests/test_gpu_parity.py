@@ -424,3 +424,19 @@ def test_pipeline_grow_sizes_every_slot():
     assert int(pipe.status().item()) == 0
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+def test_dropin_scene_cache_follows_in_place_edits():
+    # the numpy API keeps the last scene on the device keyed on a content
+    # fingerprint: editing one element in place (as fd_check does) must show
+    from paper_2510_03312_b200 import raster
+    sc = quantize_f32(S.random_scene(7, 300, seed=91))
+    cam = S.random_camera(48, 92)
+    q = S.random_query(7, 93)
+    a = raster.render(sc, cam, q)
+    assert np.array_equal(raster.render(sc, cam, q), a)  # cache hit: same bits
+    sc.color[np.argmax(sc.opacity_raw)] += 0.25           # one primitive, in place
+    b = raster.render(sc, cam, q)
+    fresh = raster.render(sc.copy(), cam, q)              # new arrays: a fresh upload
+    assert not np.array_equal(a, b)
+    assert np.array_equal(b, fresh)

@@ -147,3 +147,14 @@ def test_preprocess_views_rejects_mixed_scenes():
     assert call([a, a]) == _lib.UBS_E_ARGS
     assert lib.ubs_preprocess_views(None, None, 0, 1, s) == _lib.UBS_E_ARGS
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_device_scene_upload_matches_pack_records(dtype):
+    """DeviceScene.from_scene (fields uploaded and cast on the device) holds
+    exactly pack_records' host-side records."""
+    from paper_2510_03312_b200.types import pack_records
+    sc = S.random_scene(7, 3000, seed=17)
+    ds = engine.DeviceScene.from_scene(sc, dtype=dtype, device="cuda")
+    want = torch.from_numpy(pack_records(sc, np.float64 if dtype == torch.float64 else np.float32))
+    assert torch.equal(ds.params.cpu(), want)
