@@ -269,6 +269,12 @@ int ubs_adam_step(void *params, int32_t param_f64, const void *grads, int32_t gr
 int ubs_add_regularisers(const void *params, int32_t param_f64, void *grads, int32_t grad_f64, int64_t n,
                          int32_t n_dims, double reg_opacity, double reg_scale, ubs_stream_t s);
 
+/* regulariser value (gradients.py:120-123): sums[0] += sum sigmoid(opacity_raw),
+ * sums[1] += sum exp(s_x_raw) + sum exp(s_q_raw), fp64; the caller zeroes sums
+ * and forms lambda_o sums[0] + lambda_sigma sums[1] */
+int ubs_regulariser_value(const void *params, int32_t param_f64, int64_t n, int32_t n_dims, double *sums,
+                          ubs_stream_t s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,7 @@ SIGNATURES = [
                                 POINTER(c_double), c_int32, c_int32, c_void_p]),
     ("ubs_add_regularisers", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_int32, c_double,
                                        c_double, c_void_p]),
+    ("ubs_regulariser_value", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p]),
 ]
 
 _LIB = None

@@ -99,6 +99,35 @@ __global__ void regulariser_kernel(const PT *__restrict__ params, GT *__restrict
     for (int k = 0; k < C; ++k) g[o_sq + k] = (GT)((double)g[o_sq + k] + reg_s * exp((double)r[o_sq + k]));
 }
 
+// sums[0] += sum sigmoid(opacity_raw), sums[1] += sum exp(s_x_raw) + sum exp(s_q_raw)
+// (the regulariser value, gradients.py:120-123), fp64, one grid-stride pass
+template <typename PT>
+__global__ void regulariser_value_kernel(const PT *__restrict__ params, int64_t n, int C, double *__restrict__ sums) {
+    const int P = 14 + 6 * C;
+    const int o_sx = 3 + C + 3, o_sq = o_sx + 3 + 3 * C, o_op = o_sq + C + 1 + C;
+    double so = 0.0, ss = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const PT *r = params + i * P;
+        so += sigmoid64((double)r[o_op]);
+        for (int k = 0; k < 3; ++k) ss += exp((double)r[o_sx + k]);
+        for (int k = 0; k < C; ++k) ss += exp((double)r[o_sq + k]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        so += __shfl_xor_sync(0xffffffffu, so, o);
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    __shared__ double red[2][8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { red[0][w] = so; red[1][w] = ss; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { a += red[0][k]; b += red[1][k]; }
+        atomicAdd(sums, a);
+        atomicAdd(sums + 1, b);
+    }
+}
+
 }  // namespace ubs
 
 using namespace ubs;
@@ -176,6 +205,20 @@ extern "C" int ubs_add_regularisers(const void *params, int32_t param_f64, void 
         if (grad_f64) regulariser_kernel<float, double><<<blocks, 256, 0, s>>>((const float *)params, (double *)grads, n, C, reg_opacity, reg_scale);
         else regulariser_kernel<float, float><<<blocks, 256, 0, s>>>((const float *)params, (float *)grads, n, C, reg_opacity, reg_scale);
     }
+    UBS_CUDA_CHECK();
+    return UBS_OK;
+}
+
+extern "C" int ubs_regulariser_value(const void *params, int32_t param_f64, int64_t n, int32_t n_dims, double *sums,
+                                     ubs_stream_t stream) {
+    if (!params || !sums) return UBS_E_ARGS;
+    if (n_dims != 3 && n_dims != 6 && n_dims != 7) return UBS_E_ARGS;
+    if (n == 0) return UBS_OK;
+    const int C = n_dims - 3;
+    const unsigned blocks = (unsigned)min((int64_t)148 * 8, (n + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (param_f64) regulariser_value_kernel<double><<<blocks, 256, 0, s>>>((const double *)params, n, C, sums);
+    else regulariser_value_kernel<float><<<blocks, 256, 0, s>>>((const float *)params, n, C, sums);
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

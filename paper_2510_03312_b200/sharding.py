@@ -202,12 +202,16 @@ class GpuViewBackend:
                                             torch.cuda.current_stream().cuda_stream), "ubs_add_regularisers")
 
     def regulariser_value(self, cfg: LossConfig) -> torch.Tensor:
-        # only the opacity and scale columns, summed in fp64
-        sl = engine.field_slices(self.ds.n_dims)
+        """lambda_o sum sigmoid(o) + lambda_sigma sum exp(s) (gradients.py:120-123):
+        one fp64 pass over the opacity and scale columns (ubs_regulariser_value);
+        a 0-d device tensor."""
         p = self.ds.params
-        o = torch.sigmoid(p[:, sl["opacity_raw"][0]].double()).sum()
-        sc = torch.exp(p[:, sl["s_x_raw"][0]].double()).sum() + torch.exp(p[:, sl["s_q_raw"][0]].double()).sum()
-        return cfg.lambda_o * o + cfg.lambda_sigma * sc
+        sums = torch.zeros(2, dtype=torch.float64, device=p.device)
+        lib = _lib.load()
+        _lib.check(lib.ubs_regulariser_value(p.data_ptr(), int(p.dtype == torch.float64), int(p.shape[0]),
+                                             self.ds.n_dims, sums.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream), "ubs_regulariser_value")
+        return cfg.lambda_o * sums[0] + cfg.lambda_sigma * sums[1]
 
 
 class ViewShardedStep:

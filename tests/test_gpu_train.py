@@ -89,3 +89,17 @@ def test_backward_layouts_agree(w, h):
     assert float((a - b).norm()) <= 1e-5 * float(b.norm())
     with pytest.raises(_lib.UbsError):
         engine.backward_raster(fr, ds, g_img, torch.zeros(ds.params.shape, device="cuda"), pixels_per_lane=3)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_regulariser_value_kernel(dtype):
+    # the fused regulariser value against the torch fp64 formula
+    nd = 6
+    ds = engine.DeviceScene.from_scene(S.synth(nd, 5000, seed=4), dtype=dtype, device="cuda")
+    cfg = LossConfig(lambda_o=0.01, lambda_sigma=0.02)
+    got = float(sharding.GpuViewBackend(ds).regulariser_value(cfg))
+    sl = engine.field_slices(nd)
+    p = ds.params.double()
+    want = cfg.lambda_o * torch.sigmoid(p[:, sl["opacity_raw"][0]]).sum() + cfg.lambda_sigma * (
+        torch.exp(p[:, sl["s_x_raw"][0]]).sum() + torch.exp(p[:, sl["s_q_raw"][0]]).sum())
+    assert abs(got - float(want)) <= 1e-12 * abs(float(want))
