@@ -174,7 +174,9 @@ typedef struct UbsGradBuffers {
     void *grad2d;        /* n x 12 accumulators of per-pixel raw moments, h = g_alpha alpha / (1 - m/tau):
                             sum h dx, sum h dy, sum h dx dx, sum h dx dy, sum h dy dy, sum g_alpha alpha,
                             sum g_alpha alpha ln(1 - m/tau), g_color[3], pad[2]; ubs_prim_backward
-                            applies the per-primitive factors (-2 P, -beta/tau, 1/og) */
+                            applies the per-primitive factors (-2 P, -beta/tau, 1/og) and consumes
+                            the sums: it leaves the buffer all-zero for the next raster backward
+                            (which adds into it; the caller zeroes it once before first use) */
     void *grad_params;   /* n x (14+6C) += parameter gradients (f32, or f64 if grad_f64) */
     int32_t grad_f64;
     int32_t grad2d_f64;  /* grad2d accumulators are f64 (must equal UbsImageBuffers.raster_f64) */

@@ -104,7 +104,7 @@ prim_active_kernel(const GT *__restrict__ grad2d, const uint16_t *__restrict__ f
 
 template <int C, typename PT, typename GT, typename OT>
 __global__ void __launch_bounds__(128)
-prim_bwd_kernel(const UbsView v, const GT *__restrict__ grad2d, OT *__restrict__ out, int add_reg,
+prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, int add_reg,
                 double reg_o, double reg_s, uint32_t *__restrict__ nonfinite, const uint32_t *__restrict__ active,
                 const uint32_t *__restrict__ active_count) {
     constexpr int P = 14 + 6 * C;
@@ -125,7 +125,13 @@ prim_bwd_kernel(const UbsView v, const GT *__restrict__ grad2d, OT *__restrict__
     // factors of tile_backward (_tiles.py:114-127) are applied here once:
     //   g_mean2 = -2 c P sum(h d), g_P = c sum(h d d^T) (both off-diagonals get
     //   the dx dy moment), c = -beta / tau; g_og = sum(g_a a) / og
-    const GT *q = grad2d + i * kGrad2dStride;
+    GT *qp = grad2d + i * kGrad2dStride;
+    GT q[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+        q[k] = qp[k];
+        qp[k] = GT(0);  // consumed: every row the raster touched is active, so the buffer is left all-zero
+    }
     const double p00 = g.p2[0], p01 = g.p2[1], p11 = g.p2[2];
     const double cm = -g.beta_x / v.set.tau_sq;
     const double sx = q[0], sy = q[1];
@@ -404,17 +410,17 @@ static void launch_bwd(const UbsView &v, const UbsGradBuffers &gb, int add_reg, 
     if (g2d_f64) {
         if (gb.grad_f64)
             prim_bwd_kernel<C, PT, double, double><<<blocks, 128, 0, s>>>(
-                v, (const double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+                v, (double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
         else
             prim_bwd_kernel<C, PT, double, float><<<blocks, 128, 0, s>>>(
-                v, (const double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+                v, (double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
     } else {
         if (gb.grad_f64)
             prim_bwd_kernel<C, PT, float, double><<<blocks, 128, 0, s>>>(
-                v, (const float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+                v, (float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
         else
             prim_bwd_kernel<C, PT, float, float><<<blocks, 128, 0, s>>>(
-                v, (const float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+                v, (float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
     }
 }
 

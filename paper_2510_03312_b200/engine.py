@@ -243,6 +243,7 @@ class Workspace:
         self.bucket_start = None
         self.chunk_count = 0
         self.grad2d = None
+        self.grad2d_clean = False  # True while grad2d is all-zero (ubs_prim_backward consumed it)
         self.loss_scratch = None
         self.loss_parts = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -711,8 +712,13 @@ def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_para
         return None
     gdt = torch.float64 if fr.raster_f64 else torch.float32
     if ws.grad2d is None or ws.grad2d.numel() < n * GRAD2D_STRIDE or ws.grad2d.dtype != gdt:
-        ws.grad2d = torch.empty(ws.n_cap * GRAD2D_STRIDE, dtype=gdt, device=ws.device)
-    ws.grad2d[:n * GRAD2D_STRIDE].zero_()
+        ws.grad2d = torch.zeros(ws.n_cap * GRAD2D_STRIDE, dtype=gdt, device=ws.device)
+        ws.grad2d_clean = True
+    # ubs_prim_backward leaves the sums all-zero; zero them here only if the
+    # last raster backward was not followed by its chain (an error between them)
+    if not ws.grad2d_clean:
+        ws.grad2d[:n * GRAD2D_STRIDE].zero_()
+    ws.grad2d_clean = False
     g_img = g_image.to(device=ws.device, dtype=fr.image.dtype).contiguous()
     if grad_params.shape != ds.params.shape or not grad_params.is_contiguous():
         raise ValueError("grad_params must be a contiguous (n, 14+6C) tensor")
@@ -743,6 +749,7 @@ def backward_chain(fr: Frame, gb, add_regularisers: bool = False):
     so the workspace must not be reused before it completes."""
     check(fr.ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, _stream_ptr()),
           "ubs_prim_backward")
+    fr.ws.grad2d_clean = True  # the chain consumed (zeroed) every sum the raster added
 
 
 def field_slices(n_dims: int) -> dict:

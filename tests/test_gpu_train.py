@@ -103,3 +103,25 @@ def test_regulariser_value_kernel(dtype):
     want = cfg.lambda_o * torch.sigmoid(p[:, sl["opacity_raw"][0]]).sum() + cfg.lambda_sigma * (
         torch.exp(p[:, sl["s_x_raw"][0]]).sum() + torch.exp(p[:, sl["s_q_raw"][0]]).sum())
     assert abs(got - float(want)) <= 1e-12 * abs(float(want))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_chain_leaves_screen_space_sums_zero(precision):
+    # ubs_prim_backward consumes grad2d (zeroes it), so back-to-back backwards
+    # on one workspace need no zeroing pass and give the same gradient
+    nd = 7
+    dtype = torch.float64 if precision == "fp64" else torch.float32
+    ds = engine.DeviceScene.from_scene(S.synth(nd, 3000, seed=12), dtype=dtype, device="cuda")
+    cam = S.bench_camera(96, 64)
+    q = S.bench_query(nd, cam, 0.6)
+    ws = engine.Workspace("cuda", precision)
+    fr = engine.render_frame(ws, ds, cam, q)
+    g_img = torch.randn(64, 96, 3, device="cuda", dtype=fr.image.dtype)
+    grads = []
+    for _ in range(3):
+        g = torch.zeros(ds.params.shape, device="cuda", dtype=dtype)
+        engine.backward_frame(fr, ds, g_img, g)
+        grads.append(g.double())
+        assert ws.grad2d_clean and float(ws.grad2d.abs().max()) == 0.0
+    for g in grads[1:]:
+        assert float((g - grads[0]).norm()) <= 1e-5 * float(grads[0].norm())
