@@ -294,27 +294,34 @@ class DeviceAdam:
 
 
 def render_views(ws: engine.Workspace, ds: engine.DeviceScene, views, settings=DEFAULT_SETTINGS, group=None,
-                 sink: engine.HostFrameSink | None = None, pipeline: engine.FramePipeline | None = None):
+                 sink: engine.HostFrameSink | None = None, pipeline: engine.FramePipeline | None = None,
+                 frames_per_preprocess: int = 1):
     """Forward-render this rank's share of ``views`` [(cam, query), ...]; no
     communication.  With ``pipeline`` the frames go through its slots (several
-    frames in flight; ``ws`` is unused).  Returns the number of frames
-    rendered by this rank."""
+    frames in flight; ``ws`` is unused), ``frames_per_preprocess`` > 1 of them
+    at a time sharing one preprocess launch (``FramePipeline.render_group``).
+    Returns the number of frames rendered by this rank."""
     rank, world = dist_rank_world(group)
-    k = 0
-    for cam, query in shard(views, rank, world):
-        if pipeline is None:
+    mine = list(shard(views, rank, world))
+    if pipeline is None:
+        for cam, query in mine:
             fr = engine.render_frame(ws, ds, cam, query, settings)
             if sink is not None:
                 sink.submit(fr)
-        else:
-            fr = pipeline.render(cam, query, settings)
+        return len(mine)
+    g = max(1, min(int(frames_per_preprocess), pipeline.depth))
+    k = 0
+    for g0 in range(0, len(mine), g):
+        chunk = mine[g0:g0 + g]
+        frs = pipeline.render_group(chunk, settings) if g > 1 else [pipeline.render(*chunk[0], settings)]
+        for fr in frs:
             if sink is not None and pipeline.depth > 1:
                 sink.submit(fr, source_stream=pipeline.stream_of(fr))
                 pipeline.hold(fr, sink.last_copy)
             elif sink is not None:
                 with torch.cuda.stream(pipeline.stream_of(fr)):
                     sink.submit(fr)
-        k += 1
+            k += 1
     if pipeline is not None:
         pipeline.join()
     return k

@@ -440,3 +440,32 @@ def test_dropin_scene_cache_follows_in_place_edits():
     fresh = raster.render(sc.copy(), cam, q)              # new arrays: a fresh upload
     assert not np.array_equal(a, b)
     assert np.array_equal(b, fresh)
+
+
+def test_render_views_grouped_through_sink():
+    # sharding.render_views over a pipeline, 3 frames per shared preprocess,
+    # every image streamed to the host sink: equal to frame-by-frame renders
+    import torch
+    from paper_2510_03312_b200 import engine, sharding
+    sc = quantize_f32(S.random_scene(7, 2500, seed=95))
+    cam = S.random_camera(80, 96)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    ws = engine.Workspace("cuda", "fp32")
+    views = [(cam, S.random_query(7, 100 + k)) for k in range(7)]
+    ref = [engine.render_frame(ws, ds, c, q).image.cpu() for c, q in views]
+    pipe = engine.FramePipeline(ds, depth=6)
+    for c, q in views:
+        pipe.render(c, q, sync=True)
+    sink = engine.HostFrameSink(80, 80, slots=len(views))
+    outs = []
+    orig = sink.submit
+
+    def keep(fr, source_stream=None):
+        outs.append(orig(fr, source_stream=source_stream))
+        return outs[-1]
+    sink.submit = keep
+    n = sharding.render_views(ws, ds, views, sink=sink, pipeline=pipe, frames_per_preprocess=3)
+    sink.synchronize()
+    assert n == len(views) and pipe.check_status() == 0
+    for a, b in zip(ref, outs):
+        assert torch.equal(a, b)
