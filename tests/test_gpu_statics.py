@@ -158,3 +158,28 @@ def test_device_scene_upload_matches_pack_records(dtype):
     ds = engine.DeviceScene.from_scene(sc, dtype=dtype, device="cuda")
     want = torch.from_numpy(pack_records(sc, np.float64 if dtype == torch.float64 else np.float32))
     assert torch.equal(ds.params.cpu(), want)
+
+
+def test_render_group_mixed_resolutions():
+    """One group may mix image sizes (each view its own tile grid and
+    buffers): every frame equals its own single-view render bit for bit."""
+    sc = S.synth(7, 4000, seed=21)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    sizes = [(64, 48), (33, 17), (100, 70), (16, 16)]
+    views = []
+    for k, (w, h) in enumerate(sizes):
+        cam = S.bench_camera(w, h, k, len(sizes))
+        views.append((cam, S.bench_query(7, cam, k / 3.0)))
+    pipe = engine.FramePipeline(ds, depth=4)
+    for cam, q in views:  # size every slot for every view
+        for _ in range(4):
+            pipe.render(cam, q, sync=True)
+    frames = pipe.render_group(views)
+    pipe.join()
+    torch.cuda.synchronize()
+    assert pipe.check_status() == 0
+    ref_ws = engine.Workspace("cuda", "fp32")
+    for (cam, q), fr in zip(views, frames):
+        want = engine.render_frame(ref_ws, ds, cam, q, sync=True)
+        assert fr.image.shape == want.image.shape
+        assert torch.equal(fr.image, want.image) and torch.equal(fr.n_contrib, want.n_contrib)
