@@ -610,14 +610,20 @@ __global__ void __launch_bounds__(kTileThreads)
 raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                   const Rec64 *__restrict__ recs, const double *__restrict__ tstop,
                   const int32_t *__restrict__ ncontrib, const double *__restrict__ g_image, double *__restrict__ grad2d) {
+    constexpr int kWarps = kTileThreads / 32;
     __shared__ Rec64 srec[kTileThreads];
     __shared__ uint32_t sid[kTileThreads];
+    __shared__ uint32_t swm[kWarps][kWarps];  // [walking warp][loading warp] ballot words
     __shared__ int smax;
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int tile = blockIdx.x;
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
-    const int px = tx * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty * kTile + (threadIdx.x >> 4);
+    // the forward kernels' 8x4-pixel warps, walking only the splats whose
+    // cover mask (from the fp64 conic, 1e-3 margin: raster_fwd64_kernel) has
+    // their bit -- a culled splat has alpha == 0 at every pixel of the warp
+    const int warp = threadIdx.x >> 5;
+    const int px = tx * kTile + (warp & 1) * 8 + (threadIdx.x & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + ((threadIdx.x & 31) >> 3);
     const bool inside = px < P.W && py < P.H;
     const uint32_t start = ranges[2 * tile];
     const int64_t pix = (int64_t)py * P.W + px;
@@ -645,13 +651,29 @@ raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         const int lo = hi > kTileThreads ? hi - kTileThreads : 0;
         __syncthreads();
         const int q = lo + (int)threadIdx.x;
+        uint32_t cover = 0;
         if (q < hi) {
             const uint32_t id = ids[start + q];
             sid[threadIdx.x] = id;
-            srec[threadIdx.x] = recs[id];
+            const Rec64 r = recs[id];
+            srec[threadIdx.x] = r;
+            cover = warp_cover_mask64(r, (float)tau, tx, ty);
+        }
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (cover >> w) & 1u);
+            if (lane == 0) swm[w][warp] = word;
         }
         __syncthreads();
-        for (int j = min(hi, warp_cnt) - 1; j >= lo; --j) {
+        const int top = min(hi, warp_cnt) - lo;  // splats [lo, lo + top) concern this warp
+        for (int kw = (top - 1) >> 5; kw >= 0; --kw) {
+          uint32_t bits = swm[warp][kw];
+          const int lim = top - 32 * kw;  // keep bits < lim
+          if (lim < 32) bits &= (1u << lim) - 1u;
+          while (bits) {
+            const int bpos = 31 - __clz(bits);
+            bits ^= 1u << bpos;
+            const int j = lo + 32 * kw + bpos;
             double v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             bool contrib = false;
             if (j < my_cnt) {
@@ -692,6 +714,7 @@ raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 if (warp_reduce10(v, lane, idx, mine) && mine != (double)0)
                     atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + idx, mine);
             }
+          }
         }
     }
 }
