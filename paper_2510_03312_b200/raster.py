@@ -53,6 +53,34 @@ def _pinned(tag, shape, dtype) -> torch.Tensor:
     return buf
 
 
+def _packed_records(scene, n: int):
+    """The (n, 14+6C) float64 record array every parameter field of ``scene``
+    is a view into, at its PARAM_FIELDS offset (scenes built by
+    Scene.from_records: UBS1 loading, quantize_f32, synth), else None."""
+    from .types import field_offsets
+    base = np.asarray(scene.mu_x).base
+    while base is not None and getattr(base, "base", None) is not None and base.ndim != 2:
+        base = base.base
+    width = 14 + 6 * (int(scene.n_dims) - 3)
+    if not isinstance(base, np.ndarray) or base.dtype != np.float64 or base.shape != (n, width) \
+            or not base.flags.c_contiguous:
+        return None
+    p0 = base.__array_interface__["data"][0]
+    item = base.itemsize
+    for name, (off, size, _shape) in field_offsets(int(scene.n_dims)).items():
+        a = np.asarray(getattr(scene, name))
+        if a.dtype != np.float64 or a.size != n * size or not np.shares_memory(a, base):
+            return None
+        if a.__array_interface__["data"][0] != p0 + off * item:
+            return None
+        # rows at the record stride, the field's values contiguous inside a row
+        if n > 1 and a.strides[0] != base.strides[0]:
+            return None
+        if a.ndim > 1 and not a[0].flags.c_contiguous:  # one row of the view, no copy
+            return None
+    return base
+
+
 def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
     """The scene's records on the workspace's device, re-uploaded every call
     (callers such as fd_check mutate arrays in place, so a copy kept across
@@ -67,6 +95,12 @@ def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
     if n == 0 or not torch.cuda.is_available():
         return engine.DeviceScene.from_scene(scene, dtype=dtype, device=ws.device)
     torch.cuda.current_stream(ws.device).synchronize()  # the previous call's uploads are done
+    rec = _packed_records(scene, n)
+    if rec is not None:  # every field is a view into one packed record array: one contiguous copy
+        st = _pinned("records", rec.shape, torch.float64)
+        np.copyto(st.numpy(), rec)
+        params = st.to(ws.device, non_blocking=True).to(dtype).contiguous()
+        return engine.DeviceScene(params, scene.n_dims, scene.background)
     cols = []
     for k, _ in PARAM_FIELDS:
         a = np.asarray(getattr(scene, k)).reshape(n, -1)

@@ -469,3 +469,21 @@ def test_render_views_grouped_through_sink():
     assert n == len(views) and pipe.check_status() == 0
     for a, b in zip(ref, outs):
         assert torch.equal(a, b)
+
+
+def test_dropin_packed_record_scenes():
+    # scenes whose fields are views into one record array (UBS1 loading,
+    # quantize_f32) upload through the packed fast path: same bits as a scene
+    # of separate arrays, and in-place edits through the views still show
+    from paper_2510_03312_b200 import raster
+    from paper_2510_03312_b200.types import pack_records, Scene
+    packed = quantize_f32(S.random_scene(7, 400, seed=97))
+    loose = packed.copy()
+    assert raster._packed_records(packed, 400) is not None and raster._packed_records(loose, 400) is None
+    cam, q = S.random_camera(40, 98), S.random_query(7, 99)
+    a = raster.render(packed, cam, q)
+    assert np.array_equal(a, raster.render(loose, cam, q))
+    packed.opacity_raw[3] += 1.0
+    loose.opacity_raw[3] += 1.0
+    b = raster.render(packed, cam, q)
+    assert np.array_equal(b, raster.render(loose, cam, q)) and not np.array_equal(a, b)
