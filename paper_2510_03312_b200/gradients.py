@@ -14,8 +14,23 @@ import numpy as np
 import torch
 
 from . import _lib, engine
-from .raster import _device_scene, workspace
-from .types import DEFAULT_SETTINGS, LossConfig, SceneGrads, sigmoid
+from .raster import _device_scene, _pinned, workspace
+from .types import DEFAULT_SETTINGS, LossConfig, SceneGrads, field_offsets, sigmoid
+
+
+def _host_grads(grads: torch.Tensor, n_dims: int) -> SceneGrads:
+    """The (n, 14+6C) fp64 device gradient as one contiguous host array per
+    field: split on the device, DMA'd through reused pinned buffers, copied
+    out once (a pageable read of the interleaved buffer plus per-field
+    strided copies cost ~0.3 s at 1M primitives)."""
+    n = grads.shape[0]
+    stage = {}
+    for name, (off, size, shape) in field_offsets(n_dims).items():
+        st = _pinned("grad_" + name, (n, size), torch.float64)
+        st.copy_(grads[:, off:off + size], non_blocking=True)
+        stage[name] = (st, shape)
+    torch.cuda.current_stream(grads.device).synchronize()
+    return SceneGrads(**{name: st.numpy().reshape((n,) + shape).copy() for name, (st, shape) in stage.items()})
 
 
 def _regularizers(scene, cfg: LossConfig) -> float:
@@ -50,7 +65,7 @@ def backward(scene, frames, cfg: LossConfig = LossConfig(), settings=DEFAULT_SET
                                         grads.data_ptr(), 1, ds.n, ds.n_dims, cfg.loss_scale * cfg.lambda_o,
                                         cfg.loss_scale * cfg.lambda_sigma, torch.cuda.current_stream().cuda_stream),
                "ubs_add_regularisers")
-    out = SceneGrads.from_records(scene.n_dims, grads.cpu().numpy())
+    out = _host_grads(grads, scene.n_dims)
     out.check_finite()
     total = cfg.loss_scale * (rec + _regularizers(scene, cfg))
     return total, out
