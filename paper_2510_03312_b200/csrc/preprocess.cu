@@ -146,17 +146,19 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         const bool in_range = fabs(g.mean2[0]) < 4.0e6 && fabs(g.mean2[1]) < 4.0e6 && isfinite(u11);
         // E bounds |m32 - m64| over the support (m < tau => |dx| < rx, |dy| < ry,
         // |y0|, |y1| < sqrt(tau)), with u = 2^-24 the fp32 unit roundoff:
-        //   dx = (px - fx) + ox        |d dx| <= u (|dx| + 0.5)   (ox rounded, one add)
-        //   y0 = fma(u01, dy, u00 dx)  |d y0| <= u (|u00|(3|dx| + .5) + |u01|(3|dy| + .5) + |y0|)
+        //   dx = ((tx 16 - fx) + ox) + lx   |d dx| <= u (2|dx| + 15.5)
+        //        (ox rounded; the tile offset, |.| <= |dx| + 15, and the add of
+        //        the pixel's column lx in 0..15 rounded once each: raster.cu tile_offset)
+        //   y0 = fma(u01, dy, u00 dx)  |d y0| <= u (|u00|(4|dx| + 16) + |u01|(4|dy| + 16) + |y0|)
         //                              (either product may be the separately rounded one)
-        //   y1 = u11 dy                |d y1| <= u (|u11|(2|dy| + .5) + |y1|)
+        //   y1 = u11 dy                |d y1| <= u (|u11|(3|dy| + 16) + |y1|)
         //   m  = fma(y0, y0, y1 y1)    |d m|  <= 2|y0||d y0| + 2|y1||d y1| + 2 u tau
         // (u.. rounded to fp32 included), times a 1.25 safety factor.
         const double u = 5.9604644775390625e-08;
         const double st = sqrt(v.set.tau_sq);
         const double rx = g.radii[0], ry = g.radii[1];
-        double E = 1.25 * u * (2.0 * st * (fabs(u00) * (3.0 * rx + 0.5) + fabs(u01) * (3.0 * ry + 0.5) + st) +
-                               2.0 * st * (fabs(u11) * (2.0 * ry + 0.5) + st) + 2.0 * v.set.tau_sq);
+        double E = 1.25 * u * (2.0 * st * (fabs(u00) * (4.0 * rx + 16.0) + fabs(u01) * (4.0 * ry + 16.0) + st) +
+                               2.0 * st * (fabs(u11) * (3.0 * ry + 16.0) + st) + 2.0 * v.set.tau_sq);
         double eb = in_range ? g.beta_x * E : INFINITY;
         if (!isfinite(eb)) fl |= UBS_F_THIN;
         Rec32 r;

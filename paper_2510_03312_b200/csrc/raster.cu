@@ -137,11 +137,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // terms, above the fp32 rounding of this test and of the per-pixel m), is
 // still >= (tau + E)(1 + 1e-4): every pixel of the warp would have skipped
 // the splat without raising its edge flag, so culling never changes a bit.
-__device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float4 r1, int tx, int ty) {
+// Splat offset from the tile origin, (tx 16 - fx) + ox: the integer part is
+// exact, so this is one rounding; a pixel's dx is then xa + lx (lx = 0..15 its
+// column in the tile), the formula the preprocess error bound E covers
+// (|d dx| <= u (2 |dx| + 15.5)).  fwd32 and bwd32 both stage it in shared
+// memory so their in-support tests agree bit for bit.
+__device__ __forceinline__ float2 tile_offset(const float4 r0, int tx, int ty) {
+    return make_float2(((float)(tx * kTile) - r0.x) + r0.z, ((float)(ty * kTile) - r0.y) + r0.w);
+}
+
+__device__ __forceinline__ uint32_t warp_cover_mask(const float xa0, const float ya0, const float4 r1) {
     const float u00 = r1.x, u01 = r1.y, u11 = r1.z;
     const float thr = r1.w * (1.0f + 1.0e-4f);
-    const float xa0 = ((float)(tx * kTile) - r0.x) + r0.z;
-    const float ya0 = ((float)(ty * kTile) - r0.y) + r0.w;
     if (!isfinite(u00 + u01 + u11 + thr + xa0 + ya0)) return 0xffu;  // fmaxf would drop a NaN
     float clo[2], chi[2], cs[2];
 #pragma unroll
@@ -166,6 +173,11 @@ __device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float
         }
     }
     return mask;
+}
+
+__device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float4 r1, int tx, int ty) {
+    const float2 o = tile_offset(r0, tx, ty);
+    return warp_cover_mask(o.x, o.y, r1);
 }
 
 // Per visit (in support): alpha = 2^(beta * lg2(1 - m/tau) + log2(og)) with
@@ -197,7 +209,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
     const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
-    const float pxf = (float)px, pyf = (float)py;
+    const float lxf = (float)(px - tx * kTile), lyf = (float)(py - ty * kTile);
     const bool inside = px < P.W && py < P.H;
     uint32_t start, end;
     bool capped;
@@ -227,11 +239,12 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             float4 *d = reinterpret_cast<float4 *>(srec + threadIdx.x);
             sid[threadIdx.x] = id;
             const float4 r0 = __ldg(r), r1 = __ldg(r + 1);
-            d[0] = r0;
+            const float2 o = tile_offset(r0, tx, ty);
+            d[0] = make_float4(o.x, o.y, r0.z, r0.w);
             d[1] = r1;
             d[2] = __ldg(r + 2);
             d[3] = __ldg(r + 3);
-            cover = warp_cover_mask(r0, r1, tx, ty);
+            cover = warp_cover_mask(o.x, o.y, r1);
         }
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
@@ -250,8 +263,8 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     bits ^= bit_at(p);
                     const uint32_t ra = stop - (p << 6);
                     const float4 r0 = lds128<0>(ra), r1 = lds128<16>(ra);
-                    const float dx = (pxf - r0.x) + r0.z;
-                    const float dy = (pyf - r0.y) + r0.w;
+                    const float dx = r0.x + lxf;  // tile_offset + column in the tile
+                    const float dy = r0.y + lyf;
                     const float y0 = fmaf(r1.x, dx, r1.y * dy);
                     const float y1 = r1.z * dy;
                     const float m = fmaf(y0, y0, y1 * y1);
@@ -755,8 +768,8 @@ struct BwdPixel {
 __device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float g0, const float g1, const float g2, const float4 r0, const float4 r1, uint32_t ra, float tau,
                                           float inv_tau, float clamp, float one_minus_clamp, float (&v)[16]) {
     constexpr float kLn2 = 0.6931471805599453f;
-    const float dx = (p.pxf - r0.x) + r0.z;
-    const float dy = (p.pyf - r0.y) + r0.w;
+    const float dx = r0.x + p.pxf;  // tile_offset + column in the tile (p.pxf is tile-local)
+    const float dy = r0.y + p.pyf;
     const float y0 = fmaf(r1.x, dx, r1.y * dy);
     const float y1 = r1.z * dy;
     const float m = fmaf(y0, y0, y1 * y1);
@@ -834,8 +847,8 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         const int x = tx * kTile + (blk & 1) * 8 + (lane & 7);
         const int y = ty * kTile + (blk >> 1) * 4 + (lane >> 3);
         BwdPixel &p = px[h];
-        p.pxf = (float)x;
-        p.pyf = (float)y;
+        p.pxf = (float)(x - tx * kTile);
+        p.pyf = (float)(y - ty * kTile);
         p.cnt = 0;
         p.T = p.g0 = p.g1 = p.g2 = 0.f;
         if (x < P.W && y < P.H) {
@@ -873,11 +886,12 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                 float4 *d = reinterpret_cast<float4 *>(srec + jl);
                 sid[jl] = id;
                 const float4 r0 = __ldg(r), r1 = __ldg(r + 1);
-                d[0] = r0;
+                const float2 o = tile_offset(r0, tx, ty);
+                d[0] = make_float4(o.x, o.y, r0.z, r0.w);
                 d[1] = r1;
                 d[2] = __ldg(r + 2);
                 d[3] = __ldg(r + 3);
-                cover = warp_cover_mask(r0, r1, tx, ty);
+                cover = warp_cover_mask(o.x, o.y, r1);
             }
 #pragma unroll
             for (int w = 0; w < kBlocks; ++w) {
