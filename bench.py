@@ -208,7 +208,9 @@ def run_reference(a, rank, world):
     sample = (f"{done} of {a.steps} requested frames timed (budget {a.cpu_budget_s:.0f} s); oracle port of "
               f"betasplat render_with_cache: numpy fp64 slice/project + C (OpenMP) build_tiles/tile_forward")
     return {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": done,
-            "warmup": min(a.warmup, 1), "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
+            "warmup": min(a.warmup, 1),
+            "warmup_note": "one full CPU frame (after a 2000-primitive frame) warms the oracle; more would only "
+                           "lengthen a run bounded to a few minutes", "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(a), "impl": "reference",
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
