@@ -160,6 +160,17 @@ def test_1080p_parity(nd, count):
     assert got.n_fixed < 0.02 * cam.width * cam.height
 
 
+@pytest.mark.slow
+def test_4k_parity_far_tiles():
+    # tiles up to 3840 px from the origin: the fp32 raster's per-tile splat
+    # offset (raster.cu tile_offset) and the error bound E that covers it
+    sc = S.synth(7, 40_000, seed=5)
+    cam = S.bench_camera(3840, 2160)
+    q = S.bench_query(7, cam, 0.25)
+    got, _ = assert_frame_parity(sc, cam, q, DEFAULT_SETTINGS, "fp32")
+    assert got.n_fixed < 0.02 * cam.width * cam.height
+
+
 # --- gradients ----------------------------------------------------------------
 
 def _frames(scene, size, seed, count):
@@ -201,6 +212,23 @@ def test_backward_config1(precision):
     l_got, g_got = backward(sc, frames, LossConfig(), DEFAULT_SETTINGS, precision=precision)
     assert abs(l_got - l_ref) <= 1e-5 * abs(l_ref)
     bad = grad_close(g_got.arrays(), g_ref, rel=1e-6 if precision == "fp64" else 1e-3)
+    assert not bad, bad
+
+
+@pytest.mark.slow
+def test_backward_wide_frame():
+    # 40 x 23 tiles of a 640x360 view: the fp32 backward's tile-local pixel
+    # offsets away from the origin tile (raster.cu tile_offset)
+    from paper_2510_03312_b200.gradients import backward
+    sc = S.synth(7, 1500, seed=9)
+    cam = S.bench_camera(640, 360)
+    q = S.bench_query(7, cam, 0.7)
+    tgt = np.clip(O.render_frame(S.synth(7, 800, seed=10), cam, q, DEFAULT_SETTINGS)["image"], 0.0, 1.0)
+    frames = [(cam, q, tgt)]
+    l_ref, g_ref = O.backward(sc, frames, LossConfig(), DEFAULT_SETTINGS)
+    l_got, g_got = backward(sc, frames, LossConfig(), DEFAULT_SETTINGS, precision="fp32")
+    assert abs(l_got - l_ref) <= 1e-5 * abs(l_ref)
+    bad = grad_close(g_got.arrays(), g_ref, rel=1e-3)
     assert not bad, bad
 
 
