@@ -76,6 +76,16 @@ def test_exact_settings_no_early_out(precision):
     assert_frame_parity(sc, cam, q, RenderSettings(transmittance_min=0.0), precision)
 
 
+@pytest.mark.parametrize("tau_sq", [6.5, 4.0])
+def test_support_threshold_parity(tau_sq):
+    # non-default support thresholds: E, the cover masks and the alpha bound
+    # all scale with tau
+    sc = quantize_f32(S.random_scene(7, 3000, seed=17))
+    cam = S.random_camera(96, 18)
+    q = S.random_query(7, 19)
+    assert_frame_parity(sc, cam, q, RenderSettings(tau_sq=tau_sq), "fp32")
+
+
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_branch_coverage_parity(precision):
     sc = branch_scene()
