@@ -592,8 +592,61 @@ def run_ours(a, rank, world, local_rank):
     return out
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(a) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: check that N GPUs exist, then run
+    this script under torch.distributed.run with one rank per GPU (the
+    launch the driver itself uses).  Fails loudly rather than timing fewer GPUs."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"bench.py: --gpus {a.gpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr,
+              flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def nccl_init(world: int, local_rank: int) -> dict:
+    """NCCL process group with INIT-level debug output captured to a per-rank
+    file; returns the communicator facts rank 0 reports (every rank's
+    communicator must have nRanks == world)."""
+    import glob
+    import re
+    import torch
+    import torch.distributed as dist
+    logdir = Path(tempfile.mkdtemp(prefix="ubs_nccl_"))
+    if "NCCL_DEBUG" not in os.environ:
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ["NCCL_DEBUG_FILE"] = str(logdir / "nccl.%h.%p.log")
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    t = torch.ones(1, device=f"cuda:{local_rank}")
+    dist.all_reduce(t)  # forces communicator creation on every rank
+    torch.cuda.synchronize()
+    lines = []
+    for f in glob.glob(str(logdir / "nccl.*.log")):
+        lines += [ln.strip() for ln in Path(f).read_text(errors="replace").splitlines()
+                  if "nRanks" in ln or "NVLS" in ln or "Init COMPLETE" in ln]
+    nr = [int(m.group(1)) for ln in lines for m in [re.search(r"nRanks (\d+)", ln)] if m]
+    ok = torch.tensor([1 if (nr and all(x == world for x in nr)) else 0], device=t.device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return {"world_size": world, "allreduce_sum": float(t.item()), "comm_nranks_ok": bool(ok.item()),
+            "log_lines": lines[:6]}
+
+
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1 and a.impl == "ours":
+        return relaunch(a)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -603,13 +656,20 @@ def main():
         res = run_reference(a, rank, world)
         print(json.dumps(res), flush=True)
         return 0
+    if world != a.gpus:
+        print(f"bench.py: launched with WORLD_SIZE={world} but --gpus {a.gpus}", file=sys.stderr, flush=True)
+        return 2
+    nccl = None
     if world > 1:
         import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if torch.cuda.device_count() < world:
+            print(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s)", file=sys.stderr)
+            return 2
+        nccl = nccl_init(world, local_rank)
     res = run_train(a, rank, world, local_rank) if a.train_only else run_ours(a, rank, world, local_rank)
     if rank == 0:
+        if nccl is not None:
+            res["nccl"] = nccl
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist

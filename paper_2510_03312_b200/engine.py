@@ -87,14 +87,24 @@ class DeviceScene:
         f64 = 1 if self._params.dtype == torch.float64 else 0
         return _lib.load().ubs_statics_bytes(1 << 20, self.n_dims, f64) / float(1 << 20)
 
-    def statics_ptr(self, settings) -> int:
+    def statics_ptr(self, settings, readers=()) -> int:
         """Device pointer of up-to-date scene statics (recomputed on the
-        current stream when the parameters changed), or 0 when disabled."""
+        current stream when the parameters changed), or 0 when disabled.
+
+        ``readers``: streams that may still be reading the current statics
+        (a pipeline's slot / lead streams).  Before the buffer is recomputed
+        in place (or reallocated) the current stream waits for all of them,
+        so a frame in flight never sees statics change under it."""
         if not self.use_statics or self.n == 0:
             return 0
         p = self._params
         key = (p.data_ptr(), p._version, float(settings.psd_floor_scale))
         if key != self._statics_key:
+            if self._statics is not None:
+                cur = torch.cuda.current_stream(p.device)
+                for s in readers:
+                    if s is not None and s != cur:
+                        cur.wait_stream(s)
             lib = _lib.load()
             f64 = 1 if p.dtype == torch.float64 else 0
             nbytes = int(lib.ubs_statics_bytes(self.n, self.n_dims, f64))
@@ -533,11 +543,15 @@ class FramePipeline:
     def depth(self) -> int:
         return len(self.streams)
 
+    def readers(self) -> list:
+        """Every stream of this pipeline that reads the scene statics."""
+        return self.streams + [self.lead]
+
     def render(self, cam, query, settings=DEFAULT_SETTINGS, *, sync: bool = False, timers: dict | None = None,
                full_lists: bool = False) -> Frame:
         i = self.k % self.depth
         self.k += 1
-        self.ds.statics_ptr(settings)  # (re)computed on the caller's stream if stale
+        self.ds.statics_ptr(settings, self.readers())  # (re)computed on the caller's stream if stale
         s = self.streams[i]
         s.wait_stream(torch.cuda.current_stream())
         if self.pending[i] is not None:
@@ -561,7 +575,7 @@ class FramePipeline:
         if len(views) > self.depth:
             raise ValueError("a group cannot exceed the pipeline depth")
         ds = self.ds
-        if not ds.statics_ptr(settings):  # no statics (empty scene, use_statics=False): frame by frame
+        if not ds.statics_ptr(settings, self.readers()):  # no statics (empty scene, use_statics=False): frame by frame
             return [self.render(cam, q, settings) for cam, q in views]
         slots = [(self.k + j) % self.depth for j in range(len(views))]
         self.k += len(views)

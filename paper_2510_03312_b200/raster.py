@@ -55,20 +55,28 @@ def _pinned(tag, shape, dtype) -> torch.Tensor:
 
 def _packed_records(scene, n: int):
     """The (n, 14+6C) float64 record array every parameter field of ``scene``
-    is a view into, at its PARAM_FIELDS offset (scenes built by
-    Scene.from_records: UBS1 loading, quantize_f32, synth), else None."""
+    is a view into, at its PARAM_FIELDS offset, else None.  Scenes built by
+    Scene.from_records (UBS1 loading -- here and in betasplat, whose
+    ``frombuffer(...).astype(f8).reshape(n, w)`` leaves a 1-D owner --,
+    quantize_f32, synth) qualify: the owner is either the 2-D record array or
+    a C-contiguous 1-D buffer of exactly n * (14+6C) floats."""
     from .types import field_offsets
     base = np.asarray(scene.mu_x).base
-    while base is not None and getattr(base, "base", None) is not None and base.ndim != 2:
+    while base is not None and getattr(base, "base", None) is not None and base.ndim not in (1, 2):
         base = base.base
     width = 14 + 6 * (int(scene.n_dims) - 3)
-    if not isinstance(base, np.ndarray) or base.dtype != np.float64 or base.shape != (n, width) \
-            or not base.flags.c_contiguous:
+    if not isinstance(base, np.ndarray) or base.dtype != np.float64 or not base.flags.c_contiguous:
+        return None
+    if base.ndim == 1 and base.size == n * width:
+        base = base.reshape(n, width)  # a view of the contiguous owner, no copy
+    if base.shape != (n, width):
         return None
     p0 = base.__array_interface__["data"][0]
     item = base.itemsize
     for name, (off, size, _shape) in field_offsets(int(scene.n_dims)).items():
         a = np.asarray(getattr(scene, name))
+        if size == 0 and a.size == 0:  # mu_q / l_qx / s_q_raw / b_q of a 3D scene
+            continue
         if a.dtype != np.float64 or a.size != n * size or not np.shares_memory(a, base):
             return None
         if a.__array_interface__["data"][0] != p0 + off * item:

@@ -125,7 +125,9 @@ class GpuViewBackend:
         sync = any(item[5] for item in queue)
         slots = [(self._k + j) % self.depth for j in range(len(queue))]
         self._k += len(queue)
-        statics = ds.statics_ptr(settings)  # on the caller's stream, before any slot reads them
+        # on the caller's stream, before any slot reads them (after every stream
+        # that may still read the previous statics, if they must be recomputed)
+        statics = ds.statics_ptr(settings, self.streams + [self.lead, self.gstream])
         lead = self.lead
         lead.wait_stream(torch.cuda.current_stream())
         for i in slots:

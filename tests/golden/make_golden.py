@@ -3,7 +3,7 @@
 Run in the build container, which has /root/reference (it does not exist on
 the GPU box; the fixtures travel as committed .npz files):
 
-    NUMBA_CACHE_DIR=/tmp/ubs_numba python tests/golden/make_golden.py [--decomposition]
+    NUMBA_CACHE_DIR=/tmp/ubs_numba python tests/golden/make_golden.py [--decomposition | --branches]
 
 Each case records the reference's own outputs (betasplat.raster.render_with_cache
 and betasplat.gradients.backward) on seeded fixture scenes, plus checksums of
@@ -79,6 +79,12 @@ def cam_arrays(cam):
     return np.array([cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height], dtype=np.float64), cam.world_to_cam
 
 
+def settings_array(st):
+    """RenderSettings as stored in the fixtures (tests/test_golden.py reads it back)."""
+    return np.array([st.tile_size, st.tau_sq, st.alpha_clamp, st.transmittance_min, st.near_plane, st.cull_margin,
+                     st.screen_cov_floor, st.psd_floor_scale, float(st.gate_symmetric)], dtype=np.float64)
+
+
 def forward_case(name, scene, cam, q, settings):
     c = R.render_with_cache(scene, cam, q, settings)
     lens, ids = flat_tiles(c)
@@ -90,19 +96,24 @@ def forward_case(name, scene, cam, q, settings):
                         processed_pixels=c.processed_pixels, counts=pixel_counts(c),
                         visible=c.proj.visible, floored3=c.slices.floored, floored2=c.proj.floored,
                         mean2=c.proj.mean2, depth=c.proj.depth, gated_opacity=c.slices.gated_opacity,
-                        tmin=settings.transmittance_min)
-    print("fwd", name, c.image.shape, int(lens.sum()), c.processed_pixels)
+                        tmin=settings.transmittance_min, in_settings=settings_array(settings),
+                        floored2_any=bool(c.proj.floored.any()))
+    print("fwd", name, c.image.shape, int(lens.sum()), c.processed_pixels, "visible", int(c.proj.visible.sum()),
+          "floor3", int(c.slices.floored.sum()), "floor2", int(c.proj.floored.sum()),
+          "degenerate", int((~c.slices.valid).sum()), "clamped", int(c.alpha_clamped.sum()))
+    return c
 
 
-def backward_case(name, scene, frames, cfg):
-    loss, g = G.backward(scene, frames, cfg, bs.RenderSettings())
+def backward_case(name, scene, frames, cfg, settings=None):
+    settings = settings or bs.RenderSettings()
+    loss, g = G.backward(scene, frames, cfg, settings)
     np.savez_compressed(OUT / f"bwd_{name}.npz", loss=loss, in_records=records(scene), in_n_dims=scene.n_dims,
                         in_background=scene.background,
                         in_intr=np.stack([cam_arrays(f[0])[0] for f in frames]),
                         in_w2c=np.stack([f[0].world_to_cam for f in frames]),
                         in_query=np.stack([f[1].dims for f in frames]),
                         cfg=np.array([cfg.lambda_ssim, cfg.lambda_o, cfg.lambda_sigma, cfg.loss_scale]),
-                        targets=np.stack([f[2] for f in frames]),
+                        targets=np.stack([f[2] for f in frames]), in_settings=settings_array(settings),
                         **{f"g_{k}": v for k, v in g.arrays().items()})
     print("bwd", name, loss)
 
@@ -157,6 +168,74 @@ def main():
     backward_case("grads_7_branches", br, [(cam, q, tgt)], G.LossConfig(lambda_ssim=0.5, loss_scale=2.0))
 
 
+def branch_cases():
+    """Round-2 branch fixtures: the gate_symmetric ablation (config.py:31,
+    slicing.py:226, gradients.py:228-232), the 2x2 screen-floor adjoint
+    (raster.py:116, gradients.py:179-204), a jitter-rescued query block
+    (covariance.py:143-148) and non-default near / margin / floor settings."""
+    from betasplat.camera import Camera
+    from betasplat.covariance import batched_blocks, invert_query_block
+    # gate_symmetric: |tanh| instead of max(tanh, 0) in the gate
+    sym = bs.RenderSettings(gate_symmetric=True)
+    sc = f32(T.random_scene(7, 80, seed=61))
+    forward_case("gatesym_7", sc, T.random_camera(56, 62), T.random_query(7, 63), sym)
+    backward_case("grads_7_gatesym", sc, T.random_frames(sc, 32, seed=64, count=2), G.LossConfig(), sym)
+    sc6 = f32(T.random_scene(6, 60, seed=65))
+    backward_case("grads_6_gatesym", sc6, T.random_frames(sc6, 32, seed=66, count=1), G.LossConfig(), sym)
+
+    # 3D needles that engage the 1e-6 px^2 screen-space floor at a small size
+    n = 6
+    sc = bs.Scene(n_dims=3, mu_x=np.array([[0.0, 0.0, 0.0], [0.1, 0.05, 0.0], [0.0, 0.2, 0.1], [-0.1, -0.1, 0.05],
+                                           [0.05, -0.2, -0.1], [0.2, 0.1, 0.1]]),
+                  mu_q=np.zeros((n, 0)), rot=np.array([[0, 0, 0], [0, 0, 0], [0.1, 0, 0], [0, 0.05, 0],
+                                                        [0, 0, 0.2], [0, 0, 0]], dtype=np.float64),
+                  s_x_raw=np.log(np.array([[1e-3, 1e-7, 1e-3], [0.05, 0.05, 0.05], [2e-3, 1e-7, 1e-3],
+                                           [1e-3, 1e-7, 2e-3], [3e-3, 1e-7, 1e-3], [0.04, 0.06, 0.05]])),
+                  l_qx=np.zeros((n, 0, 3)), s_q_raw=np.zeros((n, 0)), b_x=np.array([0, 0.3, -0.2, 0.1, 0, 0.5]),
+                  b_q=np.zeros((n, 0)), opacity_raw=np.array([2.0, 1.0, 1.5, 0.5, 1.0, 0.8]),
+                  color=np.array([[0.9, 0.2, 0.1], [0.1, 0.8, 0.3], [0.3, 0.3, 0.9], [0.7, 0.6, 0.1],
+                                  [0.2, 0.9, 0.9], [0.5, 0.5, 0.5]]), background=np.array([0.1, 0.1, 0.1]))
+    sc = f32(sc)
+    cam = Camera.look_at((3.0, 0.0, 0.0), (0.0, 0.0, 0.0), (0.0, 0.0, 1.0), 0.9, 96, 64)
+    c = forward_case("screenfloor_3", sc, cam, bs.Query.static(), bs.RenderSettings())
+    assert c.proj.floored.any()
+    tgt = np.clip(0.5 + 0.3 * np.sin(np.arange(64 * 96 * 3).reshape(64, 96, 3) * 0.37), 0, 1)
+    backward_case("grads_3_screenfloor", sc, [(cam, bs.Query.static(), tgt)], G.LossConfig())
+
+    # jitter-rescued query block: a zero L_qx row with s_q -> 0 makes sigma_q
+    # singular; one 1e-8 jitter restores it (not degenerate).  mu_q of that
+    # dimension equals the query's, so its huge M entry multiplies delta = 0.
+    sc = T.random_scene(7, 60, seed=67)
+    cam = T.random_camera(48, 68)
+    q = bs.Query.view_time(0.5, cam.forward)
+    sc.l_qx[:6, 0, :] = 0.0
+    sc.s_q_raw[:6, 0] = -400.0
+    sc.mu_q[:6, 0] = 0.5
+    sc = f32(sc)
+    _, _, sq, _ = batched_blocks(sc.rot, np.exp(sc.s_x_raw), sc.l_qx, np.exp(sc.s_q_raw))
+    try:
+        np.linalg.cholesky(sq[:6])
+        raise AssertionError("blocks are not singular")
+    except np.linalg.LinAlgError:
+        pass
+    _, bad = invert_query_block(sq)
+    assert not bad.any()
+    forward_case("jitter_7", sc, cam, q, bs.RenderSettings())
+    frames = []
+    for k in range(2):  # query time 0.5 in every view: delta = 0 along the rescued dimension
+        cam_k = T.random_camera(32, 69 + k)
+        q_k = bs.Query.view_time(0.5, cam_k.forward)
+        frames.append((cam_k, q_k, np.clip(R.render(f32(T.random_scene(7, 30, seed=1046 + k)), cam_k, q_k), 0, 1)))
+    backward_case("grads_7_jitter", sc, frames, G.LossConfig())
+
+    # non-default near plane / cull margin / screen floor / PSD floor scale / support
+    st = bs.RenderSettings(near_plane=2.7, cull_margin=0.0, screen_cov_floor=9.0, psd_floor_scale=0.3, tau_sq=6.5)
+    sc = f32(T.random_scene(7, 120, seed=71))
+    cam = T.random_camera(64, 72)
+    forward_case("settings_7", sc, cam, T.random_query(7, 73), st)
+    backward_case("grads_7_settings", sc, T.random_frames(sc, 48, seed=74, count=2), G.LossConfig(), st)
+
+
 def decomposition_cases():
     """render_decomposition (raster.py:358-423) for every channel a scene supports."""
     st = bs.RenderSettings()
@@ -174,6 +253,9 @@ def decomposition_cases():
 if __name__ == "__main__":
     if "--decomposition" in sys.argv:
         decomposition_cases()
+    elif "--branches" in sys.argv:
+        branch_cases()
     else:
         main()
         decomposition_cases()
+        branch_cases()

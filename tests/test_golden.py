@@ -35,10 +35,18 @@ def _scene(d):
     return Scene.from_records(int(d["in_n_dims"]), d["in_records"], d["in_background"])
 
 
+def _settings(d):
+    """The fixture's RenderSettings (make_golden.settings_array), default when absent."""
+    if "in_settings" not in d:
+        return RenderSettings(transmittance_min=float(d["tmin"])) if "tmin" in d else RenderSettings()
+    ts, tau, clamp, tmin, near, margin, sfloor, psd, sym = d["in_settings"]
+    return RenderSettings(tile_size=int(ts), tau_sq=tau, alpha_clamp=clamp, transmittance_min=tmin, near_plane=near,
+                          cull_margin=margin, screen_cov_floor=sfloor, psd_floor_scale=psd, gate_symmetric=bool(sym))
+
+
 def _fwd_inputs(name):
     d = np.load(GOLD / f"fwd_{name}.npz")
-    st = RenderSettings(transmittance_min=float(d["tmin"]))
-    return d, _scene(d), _camera(d["in_intr"], d["in_w2c"]), Query(d["in_query"]), st
+    return d, _scene(d), _camera(d["in_intr"], d["in_w2c"]), Query(d["in_query"]), _settings(d)
 
 
 def _bwd_inputs(name):
@@ -46,7 +54,8 @@ def _bwd_inputs(name):
     frames = [(_camera(i, w), Query(q), t) for i, w, q, t in zip(d["in_intr"], d["in_w2c"], d["in_query"],
                                                                   d["targets"])]
     ls, lo, lsig, sc = d["cfg"]
-    return d, _scene(d), frames, LossConfig(lambda_ssim=ls, lambda_o=lo, lambda_sigma=lsig, loss_scale=sc)
+    return d, _scene(d), frames, LossConfig(lambda_ssim=ls, lambda_o=lo, lambda_sigma=lsig, loss_scale=sc), \
+        _settings(d)
 
 
 def _tile_lists(d):
@@ -55,7 +64,20 @@ def _tile_lists(d):
 
 
 def test_fixtures_present():
-    assert len(FWD) >= 6 and len(BWD) >= 4
+    assert len(FWD) >= 10 and len(BWD) >= 9
+
+
+def test_branch_fixtures_engage_their_branches():
+    # each round-2 fixture exercises the branch it was made for (make_golden.branch_cases)
+    assert _fwd_inputs("gatesym_7")[4].gate_symmetric and _bwd_inputs("grads_7_gatesym")[4].gate_symmetric
+    assert np.load(GOLD / "fwd_screenfloor_3.npz")["floored2"].any()
+    d, sc, cam, q, st = _fwd_inputs("settings_7")
+    assert d["floored2"].any() and d["floored3"].any() and not d["visible"].all()
+    assert st.near_plane != RenderSettings().near_plane and st.cull_margin != RenderSettings().cull_margin
+    # the jitter rows: singular query blocks that one 1e-8 jitter rescues (covariance.py:143-148)
+    d, sc, cam, q, st = _fwd_inputs("jitter_7")
+    sl = O.slice_scene(sc, q, st)
+    assert sl["valid"].all() and (np.abs(sl["m_inv"][:6]).max() > 1e7)
 
 
 def test_generators_match_reference_streams():
@@ -85,14 +107,15 @@ def test_oracle_forward_matches_reference(name):
     assert f["processed_pixels"] == int(d["processed_pixels"])
     assert np.array_equal(f["proj"]["visible"], d["visible"])
     assert np.array_equal(f["slices"]["floored"], d["floored3"])
+    assert np.array_equal(f["proj"]["floored"], d["floored2"])
     for k in ("image", "alpha_sum", "t_stop"):
         assert np.abs(f[k] - d[k]).max() <= 1e-12
 
 
 @pytest.mark.parametrize("name", BWD)
 def test_oracle_backward_matches_reference(name):
-    d, sc, frames, cfg = _bwd_inputs(name)
-    loss, g = O.backward(sc, frames, cfg, RenderSettings())
+    d, sc, frames, cfg, st = _bwd_inputs(name)
+    loss, g = O.backward(sc, frames, cfg, st)
     assert abs(loss - float(d["loss"])) <= 1e-10 * abs(float(d["loss"]))
     for k in O.FIELDS:
         ref = d[f"g_{k}"]
@@ -127,8 +150,8 @@ def test_gpu_forward_matches_reference(name, precision):
 @pytest.mark.parametrize("name", BWD)
 def test_gpu_backward_matches_reference(name, precision):
     from paper_2510_03312_b200.gradients import backward
-    d, sc, frames, cfg = _bwd_inputs(name)
-    loss, g = backward(sc, frames, cfg, RenderSettings(), precision=precision)
+    d, sc, frames, cfg, st = _bwd_inputs(name)
+    loss, g = backward(sc, frames, cfg, st, precision=precision)
     assert abs(loss - float(d["loss"])) <= (1e-10 if precision == "fp64" else 1e-5) * abs(float(d["loss"]))
     ref = {k: d[f"g_{k}"] for k in O.FIELDS}
     bad = grad_close(g.arrays(), ref, rel=1e-6 if precision == "fp64" else 1e-3)

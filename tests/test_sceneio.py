@@ -78,3 +78,18 @@ def test_device_loader_lands_records_and_renders(tmp_path, nd):
     with pytest.raises(sceneio.SceneFormatError):
         p.write_bytes(p.read_bytes()[:-4])
         sceneio.load_scene_device(p, "cuda")
+
+
+@pytest.mark.parametrize("nd", [3, 7])
+def test_loaded_scenes_take_the_single_copy_upload(tmp_path, nd):
+    # load_scene (here and in betasplat) leaves a 1-D float64 owner under the
+    # (n, width) record view: the drop-in's packed path must still find it
+    from paper_2510_03312_b200.raster import _packed_records
+    sc = quantize_f32(S.random_scene(nd, 40, seed=nd + 3))
+    p = tmp_path / "s.ubs"
+    sceneio.save_scene(sc, p)
+    back = sceneio.load_scene(p)
+    rec = _packed_records(back, 40)
+    assert rec is not None and rec.shape == (40, 14 + 6 * (nd - 3))
+    assert np.array_equal(rec, pack_records(back, np.float64))
+    assert _packed_records(back.copy(), 40) is None  # separate arrays: per-field path
