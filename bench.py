@@ -220,21 +220,32 @@ def run_reference(a, rank, world):
 # ---------------------------------------------------------------------------
 # ours
 # ---------------------------------------------------------------------------
-def algorithmic_bytes(stage, n, statics_per_prim, n_vis, entries, ids, npix, ntiles):
-    """Algorithmic HBM bytes of one launch of each stage.
+def algorithmic_bytes(stage, n, statics_per_prim, n_vis, entries, ids, npix, ntiles, k_pairs=0, P=38):
+    """Algorithmic HBM bytes of one launch of each stage, SURVEY §8(d) per-unit
+    figures: raster 48 B per visible record + 4 B per tile
+    pair + 20 B per pixel; the other stages by their own minimal traffic.
 
     entries: level-1 bucket entries of the frame; ids: tile-list ids
-    materialised (list prefixes up to the cap)."""
+    materialised (list prefixes up to the cap); k_pairs: K."""
     return {
-        # read the scene statics, write key 8 + rect 8 + count 4 + flags 2 + rec32 64 + rec64 80
+        # read the fp32 params (4P), write the raster record 48 + key 8 + count 4 + id 4 (§8d "4P + 64")
+        "preprocess": n * (4 * P + 64),
+        # §8(d) depth sort: one read + write pass of 12 B per visible primitive
+        "bin_depth": n_vis * 24 + ntiles * 8,
+        # §8(d) pair emit 12 + one sort pass 24 + range scan 8 per pair (the raster's 4 B id read is its own)
+        "bin_tiles": k_pairs * 44,
+        "raster": 48 * n_vis + 4 * k_pairs + 20 * npix,
+        "fixup": 0,
+    }[stage]
+
+
+def prefix_model_bytes(stage, n, statics_per_prim, n_vis, entries, ids, npix, ntiles):
+    """The bytes this design actually has to move (materialised list prefixes,
+    64 B records, statics): reported beside the §8(d) model."""
+    return {
         "preprocess": n * (statics_per_prim + 166),
-        # tile ranges 8/tile; depth keys read twice (histogram, scatter), (key, id) 12 written
-        # and read back, order 4 written
         "bin_depth": ntiles * 8 + n * 16 + n_vis * (12 + 12 + 4),
-        # order 4 + rect 8 + count 4 per visible rank (histogram and scatter passes), entries
-        # 8 written + 8 read, ids 4 written, ranges 8 per tile
         "bin_tiles": n_vis * 32 + entries * 16 + ids * 4 + ntiles * 8,
-        # ranges 8/tile, the consumed ids 4 each, every visible record 64 once, outputs 24 per pixel
         "raster": ntiles * 8 + 4 * ids + 64 * n_vis + 24 * npix,
         "fixup": 0,
     }[stage]
@@ -462,7 +473,8 @@ def run_ours(a, rank, world, local_rank):
     ent = stats["entries"] / stats["frames"]
     nids = stats["ids"] / stats["frames"]
     spp = ds.statics_bytes_per_prim()
-    b_dom = algorithmic_bytes(dominant, n, spp, n_vis, ent, nids, npix, ntiles)
+    b_dom = algorithmic_bytes(dominant, n, spp, n_vis, ent, nids, npix, ntiles, kk, P)
+    b_pre = prefix_model_bytes(dominant, n, spp, n_vis, ent, nids, npix, ntiles)
     peak, peak_src = measured_peak()
     achieved = b_dom / (stage_ms[dominant] / 1e3) / 1e9
     b_frame = n * (4 * P + 64) + 72 * n_vis + 48 * kk + 20 * npix  # SURVEY §8(d) B_fwd
@@ -567,7 +579,11 @@ def run_ours(a, rank, world, local_rank):
         "parallelism": f"view sharding over {world} GPU(s), no data-path collective",
         "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": b_dom, "launch_ms": stage_ms[dominant]},
+                     "algorithmic_bytes_per_launch": b_dom, "byte_model": "SURVEY 8(d): 48 N_vis + 4 K + 20 HW",
+                     "launch_ms": stage_ms[dominant],
+                     "prefix_model": {"bytes_per_launch": b_pre,
+                                      "frac": b_pre / (stage_ms[dominant] / 1e3) / 1e9 / peak,
+                                      "note": "64 B records, materialised list prefixes only, 24 B/px"}},
         "issue_roofline": ncu_issue(dominant) if a.precision == "fp32" else None,
         "frame_roofline": {"bytes_per_frame": b_frame, "achieved_gbs": b_frame / (ms_max / a.steps / 1e3) / 1e9,
                            "frac": b_frame / (ms_max / a.steps / 1e3) / 1e9 / peak,

@@ -108,15 +108,21 @@ _LIB = None
 
 
 def load(build_if_needed: bool = True):
-    """Load (building first if stale) the C-ABI library; raise if unavailable."""
+    """Load (building first if stale) the C-ABI library; raise if unavailable.
+
+    ``UBS_B200_LIB`` names another build of the same sources (e.g. a profiling
+    build with walk counters) to load instead of the in-tree library."""
     global _LIB
     if _LIB is not None:
         return _LIB
-    if build_if_needed and _build.needs_build():
+    import os
+    from pathlib import Path
+    path = Path(os.environ["UBS_B200_LIB"]) if os.environ.get("UBS_B200_LIB") else _build.OUT
+    if path == _build.OUT and build_if_needed and _build.needs_build():
         _build.build()
-    if not _build.OUT.exists():
-        raise UbsError(f"CUDA library {_build.OUT} is missing; run python -m paper_2510_03312_b200.build")
-    lib = ctypes.CDLL(str(_build.OUT))
+    if not path.exists():
+        raise UbsError(f"CUDA library {path} is missing; run python -m paper_2510_03312_b200.build")
+    lib = ctypes.CDLL(str(path))
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)
         fn.restype = res

@@ -27,6 +27,26 @@
 
 namespace ubs {
 
+#ifdef UBS_FWD_STATS
+// profiling build only (scratch tooling, not the product library): walk statistics
+// 0 warp-visits | 1 warp-visits with no lane in support | 2 lane-visits in support |
+// 3 active lanes over warp-visits | 4 warp-visits with a lane above clamp_lo |
+// 5 warp-visits with a lane below tmin_hi | 6 CTA batches | 7 warps whose walk ended by the cut
+__device__ unsigned long long g_fwd_stats[8];
+extern "C" int ubs_debug_fwd_stats(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, g_fwd_stats, sizeof(g_fwd_stats)) != cudaSuccess) return -2;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_fwd_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#define FWD_STAT(k, v) do { if ((threadIdx.x & 31) == (__ffs(__activemask()) - 1)) atomicAdd(&g_fwd_stats[k], (unsigned long long)(v)); } while (0)
+#else
+#define FWD_STAT(k, v) do { } while (0)
+#endif
+
 struct RasterParams {
     int W, H, TX;
     double tau, clamp, tmin;
@@ -231,6 +251,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
     for (uint32_t b = start; b < end; b += kTileThreads) {
         if (__syncthreads_count(done) == kTileThreads) break;
+        if (threadIdx.x == 0) FWD_STAT(6, 1);
         const uint32_t q = b + threadIdx.x;
         uint32_t cover = 0;
         if (q < end) {
@@ -268,6 +289,16 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const float y0 = fmaf(r1.x, dx, r1.y * dy);
                     const float y1 = r1.z * dy;
                     const float m = fmaf(y0, y0, y1 * y1);
+#ifdef UBS_FWD_STATS
+                    {
+                        const unsigned am = __activemask();
+                        const unsigned inb = __ballot_sync(am, m < tau);
+                        FWD_STAT(0, 1);
+                        FWD_STAT(1, inb == 0u);
+                        FWD_STAT(2, __popc(inb));
+                        FWD_STAT(3, __popc(am));
+                    }
+#endif
                     if (m >= tau) {
                         edge = fminf(edge, m - r1.w);  // support edge within the m-error band
                         continue;
@@ -278,6 +309,10 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     // relative alpha bound q = eb / (tau - m) + qc + 2.1e-7 |arg|
                     const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
                     float om = 1.0f - a;
+#ifdef UBS_FWD_STATS
+                    FWD_STAT(4, __any_sync(__activemask(), a > clamp_lo));
+                    FWD_STAT(5, __any_sync(__activemask(), T * om < tmin_hi));
+#endif
                     if (a > clamp_lo) {
                         if (a > clamp) {
                             if (a * (1.0f - qrel) > clamp) hit[sid[32 * k + 31 - (int)p]] = 1;

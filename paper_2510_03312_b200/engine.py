@@ -756,14 +756,39 @@ def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_para
     return gb
 
 
-def backward_chain(fr: Frame, gb, add_regularisers: bool = False):
+def backward_chain(fr: Frame, gb, add_regularisers: bool = False, rows: tuple | None = None):
     """Second half of :func:`backward_frame` on the current stream: the
     per-primitive chain rule from the screen-space sums into
     gb.grad_params.  It reads the frame's workspace (grad2d, flags, active),
-    so the workspace must not be reused before it completes."""
-    check(fr.ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, _stream_ptr()),
-          "ubs_prim_backward")
-    fr.ws.grad2d_clean = True  # the chain consumed (zeroed) every sum the raster added
+    so the workspace must not be reused before it completes.
+
+    ``rows=(r0, r1)`` chains only primitives r0 <= i < r1 (a sub-view whose
+    params / flags / sums / gradient pointers start at row r0): the chain is
+    per primitive, so a frame's chain split into row ranges writes the same
+    bits as one call, and a caller can start reducing finished rows early."""
+    if rows is None:
+        check(fr.ws.lib.ubs_prim_backward(fr.view, gb, 1 if add_regularisers else 0, _stream_ptr()),
+              "ubs_prim_backward")
+        fr.ws.grad2d_clean = True  # the chain consumed (zeroed) every sum the raster added
+        return
+    r0, r1 = int(rows[0]), int(rows[1])
+    if not 0 <= r0 <= r1 <= fr.n:
+        raise ValueError("row range outside the frame's primitives")
+    if r1 == r0:
+        return
+    v = UbsView.from_buffer_copy(fr.view)
+    P = record_width(v.n_dims)
+    v.params = v.params + r0 * P * (8 if v.param_f64 else 4)
+    v.n = r1 - r0
+    v.statics = 0  # the chain recomputes from params; statics are tiled per 128 rows
+    g = UbsGradBuffers.from_buffer_copy(gb)
+    g.grad2d = g.grad2d + r0 * GRAD2D_STRIDE * (8 if g.grad2d_f64 else 4)
+    g.grad_params = g.grad_params + r0 * P * (8 if g.grad_f64 else 4)
+    g.flags = g.flags + 2 * r0 if g.flags else 0
+    g.active = g.active + 4 * r0 if g.active else 0
+    check(fr.ws.lib.ubs_prim_backward(v, g, 1 if add_regularisers else 0, _stream_ptr()), "ubs_prim_backward")
+    if r1 == fr.n:
+        fr.ws.grad2d_clean = True
 
 
 def field_slices(n_dims: int) -> dict:

@@ -77,6 +77,7 @@ class GpuViewBackend:
         self._grad = None
         self._rec = None
         self._queue = []
+        self._pending = None  # (frame, grad buffers, slot) of the last view: its chain waits for end()
 
     def new_grad(self) -> torch.Tensor:
         return torch.zeros(self.ds.params.shape, dtype=self.grad_dtype, device=self.ds.device)
@@ -106,6 +107,7 @@ class GpuViewBackend:
         self._grad = grad
         self._rec = torch.zeros(self.depth, dtype=torch.float64, device=grad.device)
         self._queue = []
+        self._pending = None
         if self.depth > 1:
             self.gstream.wait_stream(torch.cuda.current_stream())  # the caller zeroed grad there
 
@@ -117,10 +119,33 @@ class GpuViewBackend:
         if len(self._queue) >= self.group or sync:
             self._flush()
 
+    def _chain(self, rows=None, hook=None):
+        """Issue the pending view's per-primitive chain on the gradient
+        stream; with ``rows`` = [(r0, r1), ...] in row-range chunks, calling
+        ``hook(r0, r1)`` on the gradient stream after each (the rows of the
+        batch's last view are final then: a reduction can start)."""
+        if self._pending is None:
+            return
+        fr, gb, i, done = self._pending
+        self._pending = None
+        self.gstream.wait_event(done)
+        with torch.cuda.stream(self.gstream):
+            if rows is None:
+                engine.backward_chain(fr, gb)
+            else:
+                for r0, r1 in rows:
+                    engine.backward_chain(fr, gb, rows=(r0, r1))
+                    if hook is not None:
+                        hook(r0, r1)
+            free = torch.cuda.Event()
+            free.record(self.gstream)
+        self.slot_free[i] = free
+
     def _flush(self):
         queue, self._queue = self._queue, []
         if not queue:
             return
+        self._chain()  # the previous group's last view: it is not the batch's last
         ds, settings = self.ds, self.settings
         sync = any(item[5] for item in queue)
         slots = [(self._k + j) % self.depth for j in range(len(queue))]
@@ -166,22 +191,35 @@ class GpuViewBackend:
                 done.record(s)
             if gb is None:
                 continue
-            self.gstream.wait_event(done)
-            with torch.cuda.stream(self.gstream):
-                engine.backward_chain(fr, gb)
-                free = torch.cuda.Event()
-                free.record(self.gstream)
-            self.slot_free[i] = free
+            self._chain()  # chains run in view order on the gradient stream
+            self._pending = (fr, gb, i, done)
 
-    def end(self) -> torch.Tensor:
+    def end(self, bucket_hook=None, buckets: int = 4) -> torch.Tensor:
         """Join the slots and the gradient stream; returns the summed
-        reconstruction terms (0-d device tensor)."""
+        reconstruction terms (0-d device tensor).
+
+        ``bucket_hook(r0, r1)``: called on the gradient stream as soon as
+        rows [r0, r1) of the batch gradient are final -- the last view's chain
+        runs in ``buckets`` row ranges -- so a collective on those rows (the
+        data-parallel all-reduce) overlaps the rest of the chain."""
         if self.depth > 1:
             self._flush()
+            n = self.ds.n
+            if bucket_hook is not None and self._pending is not None:
+                step = -(-n // max(1, int(buckets)))
+                step = -(-step // 128) * 128
+                self._chain([(r0, min(n, r0 + step)) for r0 in range(0, n, step)], bucket_hook)
+            else:
+                self._chain()
+                if bucket_hook is not None:  # no view had primitives to chain: every row is final
+                    with torch.cuda.stream(self.gstream):
+                        bucket_hook(0, n)
             cur = torch.cuda.current_stream()
             for s in self.streams:
                 cur.wait_stream(s)
             cur.wait_stream(self.gstream)
+        elif bucket_hook is not None:  # one view at a time: the gradient is final now
+            bucket_hook(0, self.ds.n)
         return self._rec.sum()
 
     def status(self) -> torch.Tensor:
@@ -223,33 +261,52 @@ class ViewShardedStep:
         self.backend = backend
         self.group = group
 
-    def loss_and_grad(self, views, cfg: LossConfig = LossConfig(), grad: torch.Tensor | None = None):
+    def loss_and_grad(self, views, cfg: LossConfig = LossConfig(), grad: torch.Tensor | None = None,
+                      buckets: int = 4):
+        """Batch loss and gradient.  Rank 0 adds the regulariser gradient
+        first (gradients.py:120-123: once per step), every rank adds its
+        views', and the gradient is summed over ranks: with a batched
+        backend in ``buckets`` row-range all-reduces issued while the last
+        view's chain still runs (no host synchronisation before them).  The
+        overflow flag of asynchronous views is checked once the reductions
+        are queued; a flagged batch is recomputed with synchronous views."""
+        import torch.distributed as dist
         if not views:
             raise ValueError("empty batch")
         rank, world = dist_rank_world(self.group)
         b = self.backend
         scale = cfg.loss_scale / len(views)
+        multi = world > 1 and dist.is_available() and dist.is_initialized()
         for attempt in range(2):
             sync = attempt > 0  # retry with synchronous frames if a view outgrew the pair buffers
             grad = b.new_grad() if grad is None else grad.zero_()
+            if rank == 0:
+                b.add_regularisers(grad, cfg)
             rec = torch.zeros(2, dtype=torch.float64, device=grad.device)
+            works = []
             if hasattr(b, "begin"):  # batched backend: views may be in flight concurrently
                 b.begin(grad)
                 for cam, query, target in shard(views, rank, world):
                     b.view(cam, query, target, cfg, scale, sync=sync)
-                rec[0] += b.end()
+
+                def hook(r0, r1, grad=grad):
+                    if multi:
+                        works.append(dist.all_reduce(grad[r0:r1], op=dist.ReduceOp.SUM, group=self.group,
+                                                     async_op=True))
+                rec[0] += b.end(bucket_hook=hook if multi else None, buckets=buckets)
             else:
                 for cam, query, target in shard(views, rank, world):
                     rec[0] += b.view_loss_grad(cam, query, target, cfg, scale, grad, sync=sync)
+                if multi:
+                    works.append(dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
             if hasattr(b, "status"):
                 rec[1] = b.status().to(torch.float64)[0]
             allreduce_sum_(rec, self.group)  # loss term and overflow flag in one collective
+            for w in works:
+                w.wait()
             if float(rec[1]) == 0.0:
                 break
             b.clear_status()
-        if rank == 0:
-            b.add_regularisers(grad, cfg)
-        allreduce_sum_(grad, self.group)
         loss = cfg.loss_scale * (rec[0] / len(views) + b.regulariser_value(cfg))
         return loss, grad
 

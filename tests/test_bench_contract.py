@@ -28,9 +28,12 @@ def test_sweep_order_visits_every_frame_once():
 
 
 def test_algorithmic_bytes_raster_model():
-    n, n_vis, ids, npix, ntiles = 1000, 800, 5000, 4096, 16
-    got = bench.algorithmic_bytes("raster", n, 352.0, n_vis, 0, ids, npix, ntiles)
-    assert got == 8 * ntiles + 4 * ids + 64 * n_vis + 24 * npix
+    # 48 B per visible record + 4 B per tile pair + 20 B per pixel
+    n, n_vis, ids, npix, ntiles, k = 1000, 800, 5000, 4096, 16, 7000
+    got = bench.algorithmic_bytes("raster", n, 352.0, n_vis, 0, ids, npix, ntiles, k)
+    assert got == 48 * n_vis + 4 * k + 20 * npix
+    pre = bench.prefix_model_bytes("raster", n, 352.0, n_vis, 0, ids, npix, ntiles)
+    assert pre == 8 * ntiles + 4 * ids + 64 * n_vis + 24 * npix
 
 
 @pytest.mark.timeout(600)
