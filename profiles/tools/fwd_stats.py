@@ -1,6 +1,6 @@
 import ctypes, os, sys, json
 sys.path.insert(0, "/root/repo")
-os.environ["UBS_B200_LIB"] = "/root/repo/scratch/libubs_stats.so"
+os.environ["UBS_B200_LIB"] = "/root/repo/profiles/tools/libubs_stats.so"
 import torch
 from paper_2510_03312_b200 import engine, synthetic as S, _lib
 from paper_2510_03312_b200.types import DEFAULT_SETTINGS
