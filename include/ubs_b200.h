@@ -51,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 4
+#define UBS_ABI_VERSION 5
 #define UBS_TILE 16
 
 enum {
@@ -122,10 +122,31 @@ typedef struct UbsPrimBuffers {
     unsigned long long *depth_range; /* [2] min / max visible depth key (initialised by ubs_preprocess) */
 } UbsPrimBuffers;
 
-/* debug row: 0 depth | 1-2 mean2 | 3-5 p2 00,01,11 | 6-7 radii | 8 gated opacity | 9 beta_x |
+/* debug row (FrameCache.slices / .proj: SliceCache slicing.py:153-182, ProjectionCache raster.py:46-60):
+ * 0 depth | 1-2 mean2 | 3-5 p2 00,01,11 | 6-7 radii | 8 gated opacity | 9 beta_x |
  * 10-12 cov2 00,01,11 | 13-18 cov3 xx,xy,xz,yy,yz,zz | 19-21 t_cam | 22-24 mean3 | 25 gate |
- * 26 opacity | 27-30 s_tanh[4] | 31 floor_eps */
-#define UBS_DEBUG_STRIDE 32
+ * 26 opacity | 27-30 s_tanh[4] | 31 floor_eps | then the offsets below (C-sized fields hold 4 slots,
+ * matrices row-major; eigenvalues ascending, eigenvectors as columns, up to sign).  The query-
+ * invariant fields (l_x, rotation, s_x, s_q, cov3 eigen pair) are filled only when the view has
+ * no statics (flags bit 16). */
+#define UBS_DEBUG_VMAT 32       /* (2, 3) jacobian @ rotation */
+#define UBS_DEBUG_COV2_EIG 38   /* eigval[2], eigvec (2, 2) of the pre-floor cov2 */
+#define UBS_DEBUG_COV3_EIG 44   /* eigval[3], eigvec (3, 3) of the symmetrised pre-floor cov3 */
+#define UBS_DEBUG_BETA_Q 56
+#define UBS_DEBUG_DELTA 60
+#define UBS_DEBUG_M_INV 64      /* (4, 4) */
+#define UBS_DEBUG_U 80
+#define UBS_DEBUG_V 84
+#define UBS_DEBUG_SIGMA_XQ 88   /* (3, 4) */
+#define UBS_DEBUG_D_RAW 100
+#define UBS_DEBUG_D_GATE 104
+#define UBS_DEBUG_LX 108        /* (3, 3) */
+#define UBS_DEBUG_ROT 117       /* (3, 3) */
+#define UBS_DEBUG_SX 126
+#define UBS_DEBUG_SQ 129
+#define UBS_DEBUG_COLOR 133
+#define UBS_DEBUG_FLAGS 136     /* 1 valid | 2 floored3 | 4 floored2 | 8 visible | 16 inline route */
+#define UBS_DEBUG_STRIDE 144
 
 /* Binning buffers. */
 typedef struct UbsBinBuffers {
@@ -189,6 +210,17 @@ typedef struct UbsGradBuffers {
     int32_t bwd_pixels_per_lane; /* fp32 raster backward layout: 0 or 2 = two pixels per lane (fastest
                                     alone), 4 = four pixels per lane in smaller CTAs (fastest beside
                                     other frames' kernels, e.g. views in flight); same results */
+    /* Deterministic mode (raster.py:1-8, gradients.py:164-173: bit-identical gradients run to run):
+     * one warp per tile writes each splat's tile partial to a slot of its own (primitive i owns
+     * det_slot_off[i] .. + tile_count[i], its rect's tiles in row-major order) and every primitive
+     * adds its partials in slot order -- no float atomics.  Needs det_capacity >= K slots of 10
+     * floats (f64 for the fp64 raster) and det_temp of ubs_det_temp_bytes(n) bytes. */
+    int32_t deterministic;
+    uint32_t *det_slot_off; /* n: exclusive prefix of tile_count */
+    void *det_partials;     /* det_capacity x 10 */
+    int64_t det_capacity;
+    void *det_temp;
+    size_t det_temp_bytes;
 } UbsGradBuffers;
 
 /* --- entry points --- */
@@ -249,6 +281,7 @@ int ubs_loss_image_grad(const void *image, const void *target, int32_t height, i
 size_t ubs_loss_scratch_bytes(int32_t height, int32_t width, int32_t f64);
 
 /* reverse replay of the blend -> per-primitive 2D gradients (grad2d, +=) */
+size_t ubs_det_temp_bytes(int64_t n); /* UbsGradBuffers.det_temp bytes for n primitives */
 int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, const UbsBinBuffers *bb,
                         const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t s);
 

@@ -17,7 +17,10 @@ UBS_OK, UBS_E_ARGS, UBS_E_CUDA, UBS_E_CAPACITY = 0, -1, -2, -3
 S_PAIR_OVERFLOW, S_LIST_TRUNC = 1, 2
 FULL_LISTS = 0xFFFFFFFF
 F_VISIBLE, F_DEGENERATE, F_FLOOR3, F_FLOOR2, F_THIN, F_GATE_SAT = 1, 2, 4, 8, 16, 32
-DEBUG_STRIDE = 32
+DEBUG_STRIDE = 144
+# UBS_DEBUG_* row offsets (include/ubs_b200.h)
+DEBUG = dict(vmat=32, cov2_eig=38, cov3_eig=44, beta_q=56, delta=60, m_inv=64, u=80, v=84, sigma_xq=88,
+             d_raw=100, d_gate=104, l_x=108, rot=117, s_x=126, s_q=129, color=133, flags=136)
 GRAD2D_STRIDE = 12
 REC32_BYTES, REC64_BYTES = 64, 80
 
@@ -69,10 +72,12 @@ class UbsGradBuffers(Structure):
     _fields_ = [("g_image", c_void_p), ("grad2d", c_void_p), ("grad_params", c_void_p), ("grad_f64", c_int32),
                 ("grad2d_f64", c_int32), ("reg_opacity", c_double), ("reg_scale", c_double),
                 ("nonfinite", c_void_p), ("flags", c_void_p), ("active", c_void_p), ("active_count", c_void_p),
-                ("bwd_pixels_per_lane", c_int32)]
+                ("bwd_pixels_per_lane", c_int32), ("deterministic", c_int32), ("det_slot_off", c_void_p),
+                ("det_partials", c_void_p), ("det_capacity", c_int64), ("det_temp", c_void_p),
+                ("det_temp_bytes", c_size_t)]
 
 
-ABI_VERSION = 4  # UBS_ABI_VERSION in include/ubs_b200.h
+ABI_VERSION = 5  # UBS_ABI_VERSION in include/ubs_b200.h
 MAX_VIEWS = 8  # UBS_MAX_VIEWS
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares
@@ -94,6 +99,7 @@ SIGNATURES = [
     ("ubs_loss_image_grad", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_double, c_double,
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
     ("ubs_loss_scratch_bytes", c_size_t, [c_int32, c_int32, c_int32]),
+    ("ubs_det_temp_bytes", c_size_t, [c_int64]),
     ("ubs_raster_backward", c_int32, [POINTER(UbsView), POINTER(UbsPrimBuffers), POINTER(UbsBinBuffers),
                                       POINTER(UbsImageBuffers), POINTER(UbsGradBuffers), c_void_p]),
     ("ubs_prim_backward", c_int32, [POINTER(UbsView), POINTER(UbsGradBuffers), c_int32, c_void_p]),

@@ -18,6 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libubs_b200.so"
+TORCH_OUT = PKG / "libubs_torch.so"  # TORCH_LIBRARY(ubs) operators over the C ABI (csrc_torch/)
 BUILD = ROOT / "build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -72,5 +73,42 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return OUT
 
 
+def torch_ops_need_build() -> bool:
+    if not TORCH_OUT.exists():
+        return True
+    t = TORCH_OUT.stat().st_mtime
+    deps = list((PKG / "csrc_torch").glob("*")) + [ROOT / "include" / "ubs_b200.h", OUT, Path(__file__)]
+    return any(p.exists() and p.stat().st_mtime > t for p in deps)
+
+
+def build_torch_ops(force: bool = False, verbose: bool = False) -> Path:
+    """g++ the TORCH_LIBRARY(ubs) extension (csrc_torch/ubs_torch.cpp) in-tree,
+    linked against libubs_b200.so (rpath $ORIGIN) and the installed torch."""
+    if not force and not torch_ops_need_build():
+        return TORCH_OUT
+    build(verbose=verbose)
+    import torch
+    import torch.utils.cpp_extension as ce
+    inc = ce.include_paths(device_type="cuda") if "device_type" in ce.include_paths.__code__.co_varnames \
+        else ce.include_paths(cuda=True)
+    libs = ce.library_paths(device_type="cuda") if "device_type" in ce.library_paths.__code__.co_varnames \
+        else ce.library_paths(cuda=True)
+    abi = 1 if torch.compiled_with_cxx11_abi() else 0
+    tmp = TORCH_OUT.with_suffix(f".{os.getpid()}.tmp.so")
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-D_GLIBCXX_USE_CXX11_ABI={abi}",
+           str(PKG / "csrc_torch" / "ubs_torch.cpp"), "-o", str(tmp), f"-I{ROOT / 'include'}",
+           *[f"-I{d}" for d in inc], *[f"-L{d}" for d in libs], f"-L{PKG}", "-lubs_b200", "-ltorch",
+           "-ltorch_cpu", "-ltorch_cuda", "-lc10", "-lc10_cuda", "-Wl,-rpath,$ORIGIN",
+           *[f"-Wl,-rpath,{d}" for d in libs]]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"torch ops build failed:\n{r.stderr[-6000:]}")
+    os.replace(tmp, TORCH_OUT)
+    if verbose:
+        print(f"built {TORCH_OUT}")
+    return TORCH_OUT
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    build_torch_ops(force="--force" in sys.argv, verbose=True)

@@ -157,9 +157,9 @@ __global__ void ssim_vblur_map_kernel(const T *__restrict__ a, const T *__restri
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
             sm += __shfl_xor_sync(0xffffffffu, sm, o);
         }
-        if (lane == 0) {
-            atomicAdd(sums, l1);
-            atomicAdd(sums + 1, sm);
+        if (lane == 0) {  // per-block partials, summed in block order by loss_sums_kernel
+            sums[2 * blockIdx.x] = l1;
+            sums[2 * blockIdx.x + 1] = sm;
         }
     }
 }
@@ -372,8 +372,9 @@ ssim_fwd_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, int H, in
     if (threadIdx.x == 0) {
         double t0 = 0.0, t1 = 0.0;
         for (int q = 0; q < kSsimThreads / 32; ++q) { t0 += red[0][q]; t1 += red[1][q]; }
-        atomicAdd(sums, t0);
-        atomicAdd(sums + 1, t1);
+        const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;  // per-block partials
+        sums[2 * bid] = t0;
+        sums[2 * bid + 1] = t1;
     }
 }
 
@@ -537,6 +538,39 @@ ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *
     }
 }
 
+// The loss terms' per-block partials summed in block order by one CTA (a
+// fixed summation order: the loss value is bitwise reproducible, unlike
+// float atomics in arrival order), then added to the caller's sums.
+__global__ void __launch_bounds__(256) loss_sums_kernel(const double *__restrict__ part, int64_t nb,
+                                                        double *__restrict__ sums) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int64_t i = threadIdx.x; i < nb; i += 256) {
+        t0 += part[2 * i];
+        t1 += part[2 * i + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    }
+    __shared__ double red[2][8];
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = t0;
+        red[1][threadIdx.x >> 5] = t1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) { a += red[0][w]; b += red[1][w]; }
+        sums[0] += a;
+        sums[1] += b;
+    }
+}
+
+static int64_t loss_part_offset(int H, int W, int elem) {
+    // partials live after the 11 N working maps, 16-byte aligned
+    return (((int64_t)11 * H * W * 3 * elem + 15) / 16) * 16;
+}
+
 static BlurTaps make_taps() {
     BlurTaps w;
     double s = 0.0;
@@ -557,18 +591,21 @@ static void run_loss(const T *a, const T *b, int H, int W, double lam, double sc
     const int thr = 256;
     const unsigned blocks = (unsigned)((N + thr - 1) / thr);
     T *h5 = scr, *g3 = scr + 5 * N, *v3 = scr + 8 * N;
+    double *part = reinterpret_cast<double *>(reinterpret_cast<char *>(scr) + loss_part_offset(H, W, sizeof(T)));
     if (H >= 12 && W >= 12) {
         const dim3 grid((W + kSsimTW - 1) / kSsimTW, (H + kSsimTH - 1) / kSsimTH);
         const size_t fwd_smem = sizeof(T) * (5 * kSsimHaloRows * kSsimCols + 2 * kSsimHaloRows * kSsimHaloCols);
         const size_t adj_smem = sizeof(T) * 3 * (kSsimHaloRows + kSsimTH) * kSsimHaloCols;
         cudaFuncSetAttribute(ssim_fwd_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
         cudaFuncSetAttribute(ssim_adj_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem);
-        ssim_fwd_tile_kernel<T><<<grid, kSsimThreads, fwd_smem, s>>>(a, b, H, W, w, g3, sums);
+        ssim_fwd_tile_kernel<T><<<grid, kSsimThreads, fwd_smem, s>>>(a, b, H, W, w, g3, part);
+        loss_sums_kernel<<<1, 256, 0, s>>>(part, (int64_t)grid.x * grid.y, sums);
         ssim_adj_tile_kernel<T><<<grid, kSsimThreads, adj_smem, s>>>(a, b, g3, H, W, w, lam, scale, g);
         return;
     }
     ssim_hblur_kernel<T><<<blocks, thr, 0, s>>>(a, b, H, W, w, h5);
-    ssim_vblur_map_kernel<T><<<blocks, thr, 0, s>>>(a, b, h5, H, W, w, g3, sums);
+    ssim_vblur_map_kernel<T><<<blocks, thr, 0, s>>>(a, b, h5, H, W, w, g3, part);
+    loss_sums_kernel<<<1, 256, 0, s>>>(part, (int64_t)blocks, sums);
     ssim_vadj_kernel<T><<<blocks, thr, 0, s>>>(g3, H, W, w, v3);
     ssim_hadj_combine_kernel<T><<<blocks, thr, 0, s>>>(a, b, v3, H, W, w, lam, scale, g);
 }
@@ -578,7 +615,9 @@ static void run_loss(const T *a, const T *b, int H, int W, double lam, double sc
 using namespace ubs;
 
 extern "C" size_t ubs_loss_scratch_bytes(int32_t height, int32_t width, int32_t f64) {
-    return (size_t)11 * height * width * 3 * (f64 ? 8 : 4);
+    // 11 N working maps + two fp64 partials per block (at most one block per 256 elements)
+    const int64_t N = (int64_t)height * width * 3;
+    return (size_t)loss_part_offset(height, width, f64 ? 8 : 4) + (size_t)16 * ((N + 255) / 256 + 1);
 }
 
 extern "C" int ubs_loss_image_grad(const void *image, const void *target, int32_t height, int32_t width,

@@ -49,21 +49,23 @@ struct PreAgg {
 
 __device__ __forceinline__ void preprocess_aggregate(PreAgg &agg, const UbsPrimBuffers &pb, bool vis,
                                                      uint32_t my_count, unsigned long long my_key) {
-    unsigned ballot = __ballot_sync(0xffffffffu, vis);
-    unsigned long long wsum = my_count;
-    unsigned long long kmin = vis ? my_key : ~0ull, kmax = vis ? my_key : 0ull;
-    for (int o = 16; o > 0; o >>= 1) {
-        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-        kmin = min(kmin, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmax, o));
-    }
+    // warp totals with single-instruction reductions (REDUX): the visible
+    // count, the tile pairs (< 2^32 per warp), and the depth range at the
+    // granularity of the keys' high 32 bits (lo rounded down, hi up: still
+    // bounds every visible key, which is all the depth bucketing needs)
+    const uint32_t full = 0xffffffffu;
+    const unsigned ballot = __ballot_sync(full, vis);
+    const uint32_t wsum = __reduce_add_sync(full, my_count);
+    const uint32_t khi = (uint32_t)(my_key >> 32);
+    const uint32_t kmin = __reduce_min_sync(full, vis ? khi : 0xffffffffu);
+    const uint32_t kmax = __reduce_max_sync(full, vis ? khi : 0u);
     if ((threadIdx.x & 31) == 0) {
         if (ballot) {
             atomicAdd(&agg.vis, (uint32_t)__popc(ballot));
-            atomicMin(&agg.dmin, kmin);
-            atomicMax(&agg.dmax, kmax);
+            atomicMin(&agg.dmin, (unsigned long long)kmin << 32);
+            atomicMax(&agg.dmax, ((unsigned long long)kmax << 32) | 0xffffffffull);
         }
-        if (wsum) atomicAdd(&agg.pairs, wsum);
+        if (wsum) atomicAdd(&agg.pairs, (unsigned long long)wsum);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -85,8 +87,8 @@ __device__ __forceinline__ void preprocess_aggregate(PreAgg &agg, const UbsPrimB
 // rect's corners in the 2D difference array), flags, raster records.
 template <int C>
 __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimBuffers &pb, int want_rec32,
-                                                int64_t i, const PrimGeom<C> &g, bool &vis, uint32_t &my_count,
-                                                unsigned long long &my_key) {
+                                                int64_t i, const PrimGeom<C> &g, double sqrt_tau, bool &vis,
+                                                uint32_t &my_count, unsigned long long &my_key) {
     const int W = v.cam.width, H = v.cam.height;
     const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
     uint32_t count = 0;
@@ -98,8 +100,10 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         const double lox = g.mean2[0] - g.radii[0], hix = g.mean2[0] + g.radii[0];
         const double loy = g.mean2[1] - g.radii[1], hiy = g.mean2[1] + g.radii[1];
         if (hix >= 0.0 && lox <= (double)W && hiy >= 0.0 && loy <= (double)H) {
-            double tx0 = fmax(0.0, ceil(lox / kTile) - 1.0), tx1 = fmin((double)(TX - 1), floor(hix / kTile));
-            double ty0 = fmax(0.0, ceil(loy / kTile) - 1.0), ty1 = fmin((double)(TY - 1), floor(hiy / kTile));
+            // x / 16 == x * 0.0625 exactly (a power-of-two scale)
+            constexpr double kInvTile = 1.0 / kTile;
+            double tx0 = fmax(0.0, ceil(lox * kInvTile) - 1.0), tx1 = fmin((double)(TX - 1), floor(hix * kInvTile));
+            double ty0 = fmax(0.0, ceil(loy * kInvTile) - 1.0), ty1 = fmin((double)(TY - 1), floor(hiy * kInvTile));
             if (tx1 >= tx0 && ty1 >= ty0) {
                 uint64_t a = (uint64_t)tx0, b = (uint64_t)ty0, c = (uint64_t)tx1, d = (uint64_t)ty1;
                 rect = a | (b << 16) | (c << 32) | (d << 48);
@@ -128,8 +132,10 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         }
     }
 
-    // raster records (only read for visible primitives)
-    if (pb.rec64) {
+    // raster records: only visible primitives' are ever read (the depth order,
+    // the tile lists and the backward hold visible ids only), so invisible
+    // ones are not written
+    if (vis && pb.rec64) {
         Rec64 r;
         r.mx = g.mean2[0]; r.my = g.mean2[1];
         r.p00 = g.p2[0]; r.p01 = g.p2[1]; r.p11 = g.p2[2];
@@ -137,7 +143,7 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         r.cr = g.color[0]; r.cg = g.color[1]; r.cb = g.color[2];
         reinterpret_cast<Rec64 *>(pb.rec64)[i] = r;
     }
-    if (want_rec32 && pb.rec32) {
+    if (vis && want_rec32 && pb.rec32) {
         // P = U^T U with U upper triangular (Cholesky of P, transposed)
         const double u00 = sqrt(g.p2[0]);
         const double u01 = g.p2[1] / u00;
@@ -155,7 +161,7 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         //   m  = fma(y0, y0, y1 y1)    |d m|  <= 2|y0||d y0| + 2|y1||d y1| + 2 u tau
         // (u.. rounded to fp32 included), times a 1.25 safety factor.
         const double u = 5.9604644775390625e-08;
-        const double st = sqrt(v.set.tau_sq);
+        const double st = sqrt_tau;
         const double rx = g.radii[0], ry = g.radii[1];
         double E = 1.25 * u * (2.0 * st * (fabs(u00) * (4.0 * rx + 16.0) + fabs(u01) * (4.0 * ry + 16.0) + st) +
                                2.0 * st * (fabs(u11) * (3.0 * ry + 16.0) + st) + 2.0 * v.set.tau_sq);
@@ -170,30 +176,16 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
         // relative error 2^-22, og / log2(og) representation; the |arg|-relative
         // parts are added per visit in the raster (2.1e-7 |arg|)
         const double qc = 0.6931471805599453 * g.beta_x * 1.6e-7 + 4.0e-7;
-        r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2(g.og));
+        // log2(og) = log2(opacity) + lsum log2(e): the gate's log is already
+        // formed and log2(opacity) is query-invariant (a scene static); the
+        // fp64 result differs from log2(og) by ~1e-16 relative, far below
+        // the fp32 rounding the per-visit 2.1e-7 |arg| term covers
+        const double log2_og = g.log2_op + g.lsum * 1.4426950408889634;
+        r.r3 = make_float4((float)eb, (float)g.og, (float)qc, (float)log2_og);
         reinterpret_cast<Rec32 *>(pb.rec32)[i] = r;
     }
     pb.flags[i] = fl;
 
-    if (pb.debug) {
-        double *d = pb.debug + i * UBS_DEBUG_STRIDE;
-        d[0] = g.tcam[2];
-        d[1] = g.mean2[0]; d[2] = g.mean2[1];
-        d[3] = g.p2[0]; d[4] = g.p2[1]; d[5] = g.p2[2];
-        d[6] = g.radii[0]; d[7] = g.radii[1];
-        d[8] = g.og; d[9] = g.beta_x;
-        d[10] = g.cov2[0]; d[11] = g.cov2[1]; d[12] = g.cov2[2];
-        d[13] = g.cov3[0][0]; d[14] = g.cov3[0][1]; d[15] = g.cov3[0][2];
-        d[16] = g.cov3[1][1]; d[17] = g.cov3[1][2]; d[18] = g.cov3[2][2];
-        d[19] = g.tcam[0]; d[20] = g.tcam[1]; d[21] = g.tcam[2];
-        d[22] = g.mean3[0]; d[23] = g.mean3[1]; d[24] = g.mean3[2];
-        d[25] = g.gate; d[26] = g.opacity;
-        for (int k = 0; k < 4; ++k) d[27 + k] = 0.0;
-        if constexpr (C > 0) {
-            for (int k = 0; k < C; ++k) d[27 + k] = g.s_tanh[k];
-        }
-        d[31] = g.floor_eps;
-    }
 }
 
 // kStatic: the query-invariant half comes from v.statics (ubs_scene_statics)
@@ -224,11 +216,11 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
         if constexpr (kStatic) {
             double mu_q[PrimGeom<C>::CC];
             load_statics<C, PT>(v.statics, i, g, mu_x, mu_q);
-            prim_view<C>(g, mu_x, mu_q, v, pb.debug != nullptr);
+            prim_view<C>(g, mu_x, mu_q, v, false);
         } else {
             prim_geom<C, PT>(stage + t * P, v, g, mu_x);
         }
-        preprocess_emit<C>(v, pb, want_rec32, i, g, vis, my_count, my_key);
+        preprocess_emit<C>(v, pb, want_rec32, i, g, sqrt(v.set.tau_sq), vis, my_count, my_key);
     }
     preprocess_aggregate(agg, pb, vis, my_count, my_key);
 }
@@ -244,6 +236,7 @@ constexpr int kMaxViews = UBS_MAX_VIEWS;
 struct PreViews {
     UbsView v[kMaxViews];
     UbsPrimBuffers pb[kMaxViews];
+    double sqrt_tau;  // sqrt(tau_sq) of the group (same settings), host-computed: IEEE sqrt, same bits
     int nv;
     int want_rec32;
 };
@@ -290,12 +283,112 @@ preprocess_views_kernel(const __grid_constant__ PreViews m) {
             PrimGeom<C> g;
             double mu_x[3], mu_q[PrimGeom<C>::CC];
             load_statics<C, PT, false>(st_block, t, g, mu_x, mu_q);  // slot t of the staged block
-            prim_view<C>(g, mu_x, mu_q, v, pb.debug != nullptr);
-            preprocess_emit<C>(v, pb, m.want_rec32, base + t, g, vis, my_count, my_key);
+            prim_view<C>(g, mu_x, mu_q, v, false);
+            preprocess_emit<C>(v, pb, m.want_rec32, base + t, g, m.sqrt_tau, vis, my_count, my_key);
         }
         preprocess_aggregate(agg, pb, vis, my_count, my_key);
         __syncthreads();  // agg reset by thread 0 before the next view adds to it
     }
+}
+
+// FrameCache.slices / .proj (slicing.py:153-182, raster.py:46-60): a
+// separate kernel that recomputes each primitive's geometry on the frame's
+// own route (statics or inline) and writes the include/ubs_b200.h
+// UBS_DEBUG_* row.  Fields of the query-invariant half (l_x, rotation, s_x,
+// s_q, the cov3 eigen pair) are only known on the inline route; d_raw and
+// both eigen pairs are recomputed with prim_view's / eigh's own arithmetic.
+// Kept out of the preprocess kernels so the debug path's eigen solvers cost
+// their hot path no registers.
+template <int C, typename PT, bool kStatic>
+__global__ void __launch_bounds__(kPreThreads)
+preprocess_debug_kernel(const UbsView v, double *__restrict__ debug) {
+    constexpr int P = 14 + 6 * C;
+    const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
+    if (i >= v.n) return;
+    PrimGeom<C> g;
+    double mu_x[3];
+    if constexpr (kStatic) {
+        double mu_q[PrimGeom<C>::CC];
+        load_statics<C, PT>(v.statics, i, g, mu_x, mu_q);
+        prim_view<C>(g, mu_x, mu_q, v, true);
+    } else {
+        prim_geom<C, PT>(reinterpret_cast<const PT *>(v.params) + i * P, v, g, mu_x);
+    }
+    const bool vis = g.visible;
+    double *d = debug + i * UBS_DEBUG_STRIDE;
+    for (int k = 0; k < UBS_DEBUG_STRIDE; ++k) d[k] = 0.0;
+    d[0] = g.tcam[2];
+    d[1] = g.mean2[0]; d[2] = g.mean2[1];
+    d[3] = g.p2[0]; d[4] = g.p2[1]; d[5] = g.p2[2];
+    d[6] = g.radii[0]; d[7] = g.radii[1];
+    d[8] = g.og; d[9] = g.beta_x;
+    d[10] = g.cov2[0]; d[11] = g.cov2[1]; d[12] = g.cov2[2];
+    d[13] = g.cov3[0][0]; d[14] = g.cov3[0][1]; d[15] = g.cov3[0][2];
+    d[16] = g.cov3[1][1]; d[17] = g.cov3[1][2]; d[18] = g.cov3[2][2];
+    d[19] = g.tcam[0]; d[20] = g.tcam[1]; d[21] = g.tcam[2];
+    d[22] = g.mean3[0]; d[23] = g.mean3[1]; d[24] = g.mean3[2];
+    d[25] = g.gate; d[26] = g.opacity;
+    d[31] = g.floor_eps;
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c) d[UBS_DEBUG_VMAT + 3 * r + c] = g.V[r][c];
+    {
+        double w[2], E[2][2];
+        eigh2(g.raw2[0], g.raw2[1], g.raw2[2], w, E);
+        d[UBS_DEBUG_COV2_EIG] = w[0]; d[UBS_DEBUG_COV2_EIG + 1] = w[1];
+        for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 2; ++c) d[UBS_DEBUG_COV2_EIG + 2 + 2 * r + c] = E[r][c];
+    }
+    if (!v.statics) {
+        double w[3], E[3][3];
+        eigh3(g.sym3, w, E);
+        for (int k = 0; k < 3; ++k) d[UBS_DEBUG_COV3_EIG + k] = w[k];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                d[UBS_DEBUG_COV3_EIG + 3 + 3 * r + c] = E[r][c];
+                d[UBS_DEBUG_LX + 3 * r + c] = g.Lx[r][c];
+                d[UBS_DEBUG_ROT + 3 * r + c] = g.R[r][c];
+            }
+        for (int k = 0; k < 3; ++k) d[UBS_DEBUG_SX + k] = g.sx[k];
+    }
+    for (int k = 0; k < 3; ++k) d[UBS_DEBUG_COLOR + k] = g.color[k];
+    if constexpr (C > 0) {
+        for (int k = 0; k < C; ++k) {
+            d[27 + k] = g.s_tanh[k];
+            d[UBS_DEBUG_BETA_Q + k] = g.beta_q[k];
+            d[UBS_DEBUG_DELTA + k] = g.delta[k];
+            d[UBS_DEBUG_U + k] = g.u[k];
+            d[UBS_DEBUG_V + k] = g.v[k];
+            d[UBS_DEBUG_D_GATE + k] = g.d_gate[k];
+            double dr = 0.0;  // prim_view's d_raw, same accumulation order
+            for (int j = 0; j < C; ++j) dr += g.M[k][j] * g.delta[j];
+            d[UBS_DEBUG_D_RAW + k] = dr;
+            for (int j = 0; j < C; ++j) d[UBS_DEBUG_M_INV + 4 * k + j] = g.M[k][j];
+            for (int r = 0; r < 3; ++r) d[UBS_DEBUG_SIGMA_XQ + 4 * r + k] = g.Sxq[r][k];
+            if (!v.statics) d[UBS_DEBUG_SQ + k] = g.sq[k];
+        }
+    }
+    d[UBS_DEBUG_FLAGS] = (g.valid ? 1.0 : 0.0) + (g.floored3 ? 2.0 : 0.0) + (g.floored2 ? 4.0 : 0.0) +
+                         (vis ? 8.0 : 0.0) + (v.statics ? 0.0 : 16.0);
+}
+
+template <int C, typename PT>
+static void launch_debug(const UbsView &v, double *debug, cudaStream_t s) {
+    const int64_t blocks = (v.n + kPreThreads - 1) / kPreThreads;
+    if (v.statics)
+        preprocess_debug_kernel<C, PT, true><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, debug);
+    else
+        preprocess_debug_kernel<C, PT, false><<<(unsigned)blocks, kPreThreads, 0, s>>>(v, debug);
+}
+
+static int launch_debug_any(const UbsView &v, double *debug, cudaStream_t s) {
+    const bool f64 = v.param_f64 != 0;
+    switch (v.n_dims) {
+        case 3: f64 ? launch_debug<0, double>(v, debug, s) : launch_debug<0, float>(v, debug, s); break;
+        case 6: f64 ? launch_debug<3, double>(v, debug, s) : launch_debug<3, float>(v, debug, s); break;
+        case 7: f64 ? launch_debug<4, double>(v, debug, s) : launch_debug<4, float>(v, debug, s); break;
+        default: return UBS_E_ARGS;
+    }
+    return UBS_OK;
 }
 
 template <int C, typename PT>
@@ -374,6 +467,7 @@ extern "C" int ubs_preprocess(const UbsView *v, const UbsPrimBuffers *pb, int32_
                     : launch_pre<4, float>(*v, *pb, want_rec32, s); break;
         default: return UBS_E_ARGS;
     }
+    if (pb->debug && launch_debug_any(*v, pb->debug, s) != UBS_OK) return UBS_E_ARGS;
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
@@ -401,6 +495,7 @@ extern "C" int ubs_preprocess_views(const UbsView *views, const UbsPrimBuffers *
         PreViews m;
         m.nv = min(kMaxViews, n_views - k0);
         m.want_rec32 = want_rec32;
+        m.sqrt_tau = sqrt(v0.set.tau_sq);
         for (int k = 0; k < m.nv; ++k) {
             m.v[k] = views[k0 + k];
             m.pb[k] = pbs[k0 + k];
@@ -415,6 +510,8 @@ extern "C" int ubs_preprocess_views(const UbsView *views, const UbsPrimBuffers *
         }
         if (rc != UBS_OK) return rc;
     }
+    for (int k = 0; k < n_views; ++k)
+        if (pbs[k].debug && launch_debug_any(views[k], pbs[k].debug, s) != UBS_OK) return UBS_E_ARGS;
     UBS_CUDA_CHECK();
     return UBS_OK;
 }

@@ -199,6 +199,7 @@ struct PrimGeom {
     double delta[CC], u[CC], v[CC], mean3[3];
     double sym3[3][3], cov3[3][3], floor_eps;
     double s_tanh[CC], d_gate[CC], gate, og;
+    double log2_op, lsum;  // log2(opacity) (query-invariant) and the gate's log: log2(og) = log2_op + lsum log2(e)
     bool valid, floored3;
     // projection
     double tcam[3], z, mean2[2], V[2][3], raw2[3], cov2[3], p2[3], radii[2];
@@ -255,6 +256,7 @@ __device__ inline void prim_static(const PT *rec, const UbsSettings &set, PrimGe
 
     g.beta_x = 4.0 * exp(bxr);
     g.opacity = sigmoid64(oraw);
+    g.log2_op = log2(g.opacity);
     g.valid = true;
     double raw[3][3];
     for (int i = 0; i < 3; ++i)
@@ -349,6 +351,7 @@ __device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const 
                                  const UbsView &v, bool exact_s = true) {
     double mean3[3] = {mu_x[0], mu_x[1], mu_x[2]};
     g.gate = 1.0;
+    g.lsum = 0.0;
     if constexpr (C > 0) {
         // conditional mean (slicing.py:205-208)
         for (int k = 0; k < C; ++k) {
@@ -383,6 +386,7 @@ __device__ inline void prim_view(PrimGeom<C> &g, const double (&mu_x)[3], const 
             lsum += 4.0 * g.beta_q[i] * log1p(-d);
         }
         g.gate = exp(lsum);
+        g.lsum = lsum;
     }
     for (int i = 0; i < 3; ++i) g.mean3[i] = mean3[i];
     g.og = g.opacity * g.gate;
@@ -459,7 +463,7 @@ __device__ inline void prim_geom(const PT *rec, const UbsView &v, PrimGeom<C> &g
 // precision, field-major inside the block (every field load of a warp is one
 // coalesced access at a constant offset from the block base).
 //   fp64: beta_q[C] | M upper triangle, row-major [C(C+1)/2] | Sxq[3][C] |
-//         cov3[3][3] | opacity | beta_x | floor_eps | flags
+//         cov3[3][3] | opacity | beta_x | floor_eps | flags | log2(opacity)
 //   raw:  mu_x[3] | mu_q[C] | color[3]
 // flags: 1 = valid (query block invertible), 2 = PSD-floored.
 constexpr int kStaticBlock = 128;
@@ -474,13 +478,14 @@ struct StaticLayout {
     static constexpr int kBetaX = kOpacity + 1;
     static constexpr int kFloorEps = kBetaX + 1;
     static constexpr int kFlags = kFloorEps + 1;
-    static constexpr int D = kFlags + 1;
+    static constexpr int kLog2Op = kFlags + 1;
+    static constexpr int D = kLog2Op + 1;
     static constexpr int R = 6 + C;
 };
 
 __host__ __device__ inline size_t static_block_bytes(int n_dims, int param_f64) {
     const int C = n_dims - 3;
-    const int D = C + C * (C + 1) / 2 + 3 * C + 13;
+    const int D = C + C * (C + 1) / 2 + 3 * C + 14;
     const int R = 6 + C;
     return (size_t)kStaticBlock * (size_t)(8 * D + (param_f64 ? 8 : 4) * R);
 }
@@ -520,6 +525,7 @@ __device__ inline void store_statics(void *buf, int64_t i, const PrimGeom<C> &g,
     d[L::kBetaX * S] = g.beta_x;
     d[L::kFloorEps * S] = g.floor_eps;
     d[L::kFlags * S] = (double)((g.valid ? 1 : 0) | (g.floored3 ? 2 : 0));
+    d[L::kLog2Op * S] = g.log2_op;
     for (int k = 0; k < 3; ++k) r[k * S] = (PT)mu_x[k];
     for (int k = 0; k < C; ++k) r[(3 + k) * S] = (PT)mu_q[k];
     for (int k = 0; k < 3; ++k) r[(3 + C + k) * S] = (PT)g.color[k];
@@ -559,6 +565,7 @@ __device__ inline void load_statics(const void *buf, int64_t i, PrimGeom<C> &g, 
     const int fl = (int)ld_statics<double, kGlobal>(d + L::kFlags * S);
     g.valid = (fl & 1) != 0;
     g.floored3 = (fl & 2) != 0;
+    g.log2_op = ld_statics<double, kGlobal>(d + L::kLog2Op * S);
     for (int k = 0; k < 3; ++k) mu_x[k] = (double)ld_statics<PT, kGlobal>(r + k * S);
     for (int k = 0; k < C; ++k) mu_q[k] = (double)ld_statics<PT, kGlobal>(r + (3 + k) * S);
     for (int k = 0; k < 3; ++k) g.color[k] = (double)ld_statics<PT, kGlobal>(r + (3 + C + k) * S);

@@ -144,20 +144,25 @@ class DeviceScene:
         return self.params.device
 
 
-def make_view(ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS) -> UbsView:
+def view_struct(n: int, n_dims: int, param_f64: bool, background, cam, query, settings=DEFAULT_SETTINGS,
+                params_ptr: int = 0, statics_ptr: int = 0) -> UbsView:
+    """The C-ABI UbsView of one frame from reference-shaped objects (host
+    only; duck-typed: betasplat's Camera / Query / RenderSettings work as well
+    as this package's mirrors and give the same bytes)."""
     if int(settings.tile_size) != TILE:
         raise ValueError("tile_size must be 16 on the device path")
-    c = ds.n_dims - 3
+    c = n_dims - 3
     q = np.asarray(query.dims, dtype=np.float64).reshape(-1)
     if q.shape[0] != c:
         raise ValueError(f"query has {q.shape[0]} dims, scene expects {c}")
     v = UbsView()
-    v.params = _ptr(ds.params)
-    v.n = ds.n
-    v.n_dims = ds.n_dims
-    v.param_f64 = 1 if ds.params.dtype == torch.float64 else 0
+    v.params = params_ptr
+    v.n = n
+    v.n_dims = n_dims
+    v.param_f64 = 1 if param_f64 else 0
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
     for k in range(3):
-        v.background[k] = ds.background[k]
+        v.background[k] = float(bg[k])
     for k in range(4):
         v.query[k] = float(q[k]) if k < c else 0.0
     w2c = np.asarray(cam.world_to_cam, dtype=np.float64).reshape(4, 4)
@@ -180,8 +185,15 @@ def make_view(ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS) -> UbsView
     st.gate_symmetric = 1 if settings.gate_symmetric else 0
     st.tile_size = TILE
     v.set = st
-    v.statics = ds.statics_ptr(settings)
+    v.statics = statics_ptr
     return v
+
+
+def make_view(ds: DeviceScene, cam, query, settings=DEFAULT_SETTINGS) -> UbsView:
+    if int(settings.tile_size) != TILE:
+        raise ValueError("tile_size must be 16 on the device path")
+    return view_struct(ds.n, ds.n_dims, ds.params.dtype == torch.float64, ds.background, cam, query, settings,
+                       params_ptr=_ptr(ds.params), statics_ptr=ds.statics_ptr(settings))
 
 
 @dataclass
@@ -260,6 +272,9 @@ class Workspace:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)  # UBS_S_* bits, sticky
         self.active = None
         self.active_count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.det_partials = None  # deterministic backward: K x 10 tile partials, slot offsets, scan scratch
+        self.det_slot_off = None
+        self.det_temp = None
         # materialised prefix of each tile list (grows x2 when a frame needs more)
         self.list_cap = 1024
         self.frame_list_cap = self.list_cap
@@ -706,20 +721,26 @@ def loss_image_grad(fr: Frame, target: torch.Tensor, lambda_ssim: float, scale: 
 
 
 def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
-                   add_regularisers: bool = False, reg_opacity: float = 0.0, reg_scale: float = 0.0):
+                   add_regularisers: bool = False, reg_opacity: float = 0.0, reg_scale: float = 0.0,
+                   deterministic: bool = False):
     """Accumulate d(loss)/d(params) of one frame into ``grad_params`` (n x P)."""
-    gb = backward_raster(fr, ds, g_image, grad_params, reg_opacity, reg_scale)
+    gb = backward_raster(fr, ds, g_image, grad_params, reg_opacity, reg_scale, deterministic=deterministic)
     if gb is not None:
         backward_chain(fr, gb, add_regularisers)
 
 
 def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
-                    reg_opacity: float = 0.0, reg_scale: float = 0.0, pixels_per_lane: int = 2):
+                    reg_opacity: float = 0.0, reg_scale: float = 0.0, pixels_per_lane: int = 2,
+                    deterministic: bool = False):
     """First half of :func:`backward_frame` on the current stream: the
     raster backward into the frame's screen-space sums (ws.grad2d).  Returns
     the UbsGradBuffers for :func:`backward_chain` (None for an empty scene).
     ``pixels_per_lane`` picks the fp32 raster backward's layout (2: fastest
-    alone, 4: fastest beside other views' kernels; same results)."""
+    alone, 4: fastest beside other views' kernels; same results).
+    ``deterministic``: per-(primitive, tile) partials reduced in a fixed
+    order instead of float atomics -- bit-identical sums on every run
+    (raster.py:1-8, gradients.py:164-173), at the cost of a K x 10 buffer
+    and a slower one-warp-per-tile walk."""
     ws = fr.ws
     n = fr.n
     if n == 0:
@@ -751,6 +772,22 @@ def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_para
     gb.active = _ptr(ws.active)
     gb.active_count = _ptr(ws.active_count)
     gb.bwd_pixels_per_lane = int(pixels_per_lane)
+    if deterministic:
+        esz = 8 if fr.raster_f64 else 4
+        need = ws.pair_cap * 10 * esz
+        if ws.det_partials is None or ws.det_partials.numel() < need:
+            ws.det_partials = torch.empty(max(need, 1), dtype=torch.uint8, device=ws.device)
+        if ws.det_slot_off is None or ws.det_slot_off.numel() < ws.n_cap + 1:
+            ws.det_slot_off = torch.empty(ws.n_cap + 1, dtype=torch.int32, device=ws.device)
+        tb = int(ws.lib.ubs_det_temp_bytes(ws.n_cap))
+        if ws.det_temp is None or ws.det_temp.numel() < tb:
+            ws.det_temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=ws.device)
+        gb.deterministic = 1
+        gb.det_slot_off = _ptr(ws.det_slot_off)
+        gb.det_partials = _ptr(ws.det_partials)
+        gb.det_capacity = ws.pair_cap
+        gb.det_temp = _ptr(ws.det_temp)
+        gb.det_temp_bytes = ws.det_temp.numel()
     check(ws.lib.ubs_raster_backward(fr.view, ws.prim_buffers(), ws.bin_buffers(), ws.image_buffers(), gb,
                                      _stream_ptr()), "ubs_raster_backward")
     return gb

@@ -40,8 +40,13 @@ def _regularizers(scene, cfg: LossConfig) -> float:
 
 
 def backward(scene, frames, cfg: LossConfig = LossConfig(), settings=DEFAULT_SETTINGS, *,
-             precision: str | None = None, device=None):
-    """Loss over the batch plus gradients for every primitive field."""
+             precision: str | None = None, device=None, deterministic: bool = False):
+    """Loss over the batch plus gradients for every primitive field.
+
+    ``deterministic=True``: the raster backward reduces per-(primitive, tile)
+    partials in a fixed order instead of with float atomics, so repeated
+    calls return bit-identical gradients (the reference's guarantee,
+    raster.py:1-8); the loss sums are always reduced in a fixed order."""
     if not frames:
         raise ValueError("empty batch")
     ws = workspace(precision, device)
@@ -54,7 +59,7 @@ def backward(scene, frames, cfg: LossConfig = LossConfig(), settings=DEFAULT_SET
         ws.loss_parts.zero_()
         tgt = torch.as_tensor(np.ascontiguousarray(target, dtype=np.float64))
         g_img, parts = engine.loss_image_grad(fr, tgt, cfg.lambda_ssim, scale)
-        engine.backward_frame(fr, ds, g_img, grads)
+        engine.backward_frame(fr, ds, g_img, grads, deterministic=deterministic)
         l1_sum, ssim_sum = parts.cpu().tolist()
         size = fr.width * fr.height * 3
         rec += (1.0 - cfg.lambda_ssim) * (l1_sum / size) + cfg.lambda_ssim * (1.0 - ssim_sum / size)

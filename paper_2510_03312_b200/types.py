@@ -294,6 +294,55 @@ DEFAULT_SETTINGS = RenderSettings()
 
 
 @dataclass
+class SliceCache:
+    """Per-primitive conditioning state (reference slicing.py:153-182), filled
+    from the device preprocess's debug dump (FrameCache.slices)."""
+
+    valid: np.ndarray          # (n,) False where the query block was singular
+    mean3: np.ndarray          # (n, 3)
+    cov3: np.ndarray           # (n, 3, 3) floored
+    beta_x: np.ndarray         # (n,)
+    gated_opacity: np.ndarray  # (n,)
+    color: np.ndarray          # (n, 3)
+    opacity: np.ndarray        # (n,)
+    gate: np.ndarray           # (n,)
+    beta_q: np.ndarray         # (n, C)
+    delta: np.ndarray          # (n, C)
+    m_inv: np.ndarray          # (n, C, C)
+    u: np.ndarray              # (n, C)
+    v: np.ndarray              # (n, C)
+    sigma_xq: np.ndarray       # (n, 3, C)
+    d_raw: np.ndarray          # (n, C)
+    s_tanh: np.ndarray         # (n, C)
+    d_gate: np.ndarray         # (n, C)
+    cov3_eigval: np.ndarray    # (n, 3) ascending
+    cov3_eigvec: np.ndarray    # (n, 3, 3) columns, up to sign
+    floor_eps: np.ndarray      # (n,)
+    floored: np.ndarray        # (n,) bool
+    l_x: np.ndarray            # (n, 3, 3)
+    rotation: np.ndarray       # (n, 3, 3)
+    s_x: np.ndarray            # (n, 3)
+    s_q: np.ndarray            # (n, C)
+
+
+@dataclass
+class ProjectionCache:
+    """Per-primitive projection state (reference raster.py:46-60)."""
+
+    t_cam: np.ndarray        # (n, 3)
+    depth: np.ndarray        # (n,)
+    mean2: np.ndarray        # (n, 2)
+    vmat: np.ndarray         # (n, 2, 3) jacobian @ rotation
+    cov2_eigval: np.ndarray  # (n, 2) ascending, of the pre-floor cov2
+    cov2_eigvec: np.ndarray  # (n, 2, 2) columns, up to sign
+    floored: np.ndarray      # (n,) screen floor engaged
+    cov2: np.ndarray         # (n, 2, 2)
+    p2: np.ndarray           # (n, 2, 2)
+    radii: np.ndarray        # (n, 2)
+    visible: np.ndarray      # (n,)
+
+
+@dataclass
 class LossConfig:
     """Composite objective weights (gradients.py:29-40)."""
 

@@ -27,7 +27,8 @@ def header_functions():
 def test_library_builds_and_loads():
     build.build()
     lib = _lib.load(build_if_needed=False)
-    assert lib.ubs_abi_version() == _lib.ABI_VERSION == 4
+    hdr = int(re.search(r"#define UBS_ABI_VERSION (\d+)", HEADER.read_text()).group(1))
+    assert lib.ubs_abi_version() == _lib.ABI_VERSION == hdr
     assert b"sm_100a" in lib.ubs_build_info()
 
 
@@ -83,3 +84,15 @@ def test_cpu_only_host_raises_no_fallback():
     from paper_2510_03312_b200 import synthetic as S
     with pytest.raises(Exception):
         raster.render(S.random_scene(3, 4, seed=0), S.random_camera(16, 0), S.random_query(3, 0))
+
+
+def test_debug_row_offsets_match_header():
+    # FrameCache.slices / .proj read the dump through _lib.DEBUG: every offset
+    # must be the header's UBS_DEBUG_* value
+    text = HEADER.read_text()
+    macros = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"#define UBS_DEBUG_([A-Z0-9_]+) (\d+)", text)}
+    assert macros.pop("stride") == _lib.DEBUG_STRIDE
+    names = {"vmat": "vmat", "cov2_eig": "cov2_eig", "cov3_eig": "cov3_eig", "beta_q": "beta_q", "delta": "delta",
+             "m_inv": "m_inv", "u": "u", "v": "v", "sigma_xq": "sigma_xq", "d_raw": "d_raw", "d_gate": "d_gate",
+             "lx": "l_x", "rot": "rot", "sx": "s_x", "sq": "s_q", "color": "color", "flags": "flags"}
+    assert {names[k]: v for k, v in macros.items()} == _lib.DEBUG

@@ -465,8 +465,8 @@ def test_pipeline_grow_sizes_every_slot():
 
 
 def test_dropin_scene_cache_follows_in_place_edits():
-    # the numpy API keeps the last scene on the device keyed on a content
-    # fingerprint: editing one element in place (as fd_check does) must show
+    # the numpy API re-stages the scene every call: editing one element in
+    # place (as fd_check does) must show
     from paper_2510_03312_b200 import raster
     sc = quantize_f32(S.random_scene(7, 300, seed=91))
     cam = S.random_camera(48, 92)
@@ -525,3 +525,60 @@ def test_dropin_packed_record_scenes():
     loose.opacity_raw[3] += 1.0
     b = raster.render(packed, cam, q)
     assert np.array_equal(b, raster.render(loose, cam, q)) and not np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("nd", [3, 6, 7])
+def test_framecache_has_every_reference_field(nd):
+    # FrameCache.slices / .proj carry every SliceCache / ProjectionCache field
+    # (slicing.py:153-182, raster.py:46-60) with the oracle's values;
+    # eigenvectors are compared up to sign (LAPACK's convention is arbitrary)
+    from dataclasses import fields
+    from paper_2510_03312_b200.types import ProjectionCache, SliceCache
+    sc = branch_scene(seed=7, n=160) if nd == 7 else quantize_f32(S.random_scene(nd, 160, seed=nd + 90))
+    cam = S.random_camera(64, nd + 91)
+    q = S.random_query(nd, nd + 92)
+    got = _render(sc, cam, q, DEFAULT_SETTINGS, "fp64")
+    sl = O.slice_scene(sc, q, DEFAULT_SETTINGS)
+    pr = O.project_scene(sl, cam, DEFAULT_SETTINGS)
+    ok = sl["valid"]
+    for cache, ref, cls in ((got.slices, sl, SliceCache), (got.proj, pr, ProjectionCache)):
+        assert isinstance(cache, cls)
+        for f in fields(cls):
+            a, b = np.asarray(getattr(cache, f.name)), np.asarray(ref[f.name])
+            assert a.shape == b.shape, (f.name, a.shape, b.shape)
+            if a.dtype == bool:
+                assert np.array_equal(a, b), f.name
+                continue
+            a, b = a[ok], b[ok]
+            if b.size == 0:
+                continue
+            if f.name.endswith("eigvec"):
+                # columns up to sign: |V^T V_ref| is the identity where eigenvalues are distinct
+                dots = np.abs(np.einsum("nij,nik->njk", a, b))
+                lam = ref[f.name.replace("vec", "val")][ok]
+                gap = np.min(np.diff(lam, axis=1), axis=1) > 1e-6 * np.abs(lam).max(axis=1)
+                eye = np.broadcast_to(np.eye(a.shape[-1]), dots.shape)
+                assert np.abs(dots[gap] - eye[gap]).max() <= 1e-8, f.name
+                continue
+            scale = max(1.0, float(np.abs(b).max()))
+            assert np.abs(a - b).max() <= 1e-9 * scale, (f.name, float(np.abs(a - b).max()))
+
+
+def test_resident_scene_is_reused_until_invalidated():
+    # raster.resident(scene): uploaded once, reused by every call on that
+    # object (same bits as a fresh upload); in-place edits need invalidate()
+    from paper_2510_03312_b200 import raster
+    sc = quantize_f32(S.random_scene(7, 300, seed=93))
+    cam = S.random_camera(48, 94)
+    qs = [S.random_query(7, 95 + k) for k in range(3)]
+    ref = [raster.render(sc, cam, q) for q in qs]
+    with raster.resident(sc):
+        assert all(np.array_equal(raster.render(sc, cam, q), r) for q, r in zip(qs, ref))
+        ds = raster._device_scene(sc, raster.workspace())
+        assert raster._device_scene(sc, raster.workspace()) is ds
+        sc.color[np.argmax(sc.opacity_raw)] += 0.25
+        assert np.array_equal(raster.render(sc, cam, qs[0]), ref[0])  # stale until invalidated
+        raster.invalidate(sc)
+        edited = raster.render(sc, cam, qs[0])
+    assert not np.array_equal(edited, ref[0])
+    assert np.array_equal(edited, raster.render(sc.copy(), cam, qs[0]))
