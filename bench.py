@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--dropin-frames", type=int, default=10)
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step measurement")
+    ap.add_argument("--no-train-batches", action="store_true", help="skip config-5 batches 16 and 32")
     ap.add_argument("--train-prims", type=int, default=3_000_000)
     ap.add_argument("--train-views-per-gpu", type=int, default=8)
     ap.add_argument("--train-steps", type=int, default=5)
@@ -308,6 +309,92 @@ def run_train(a, rank, world, local_rank):
             "steps": a.train_steps, "warmup": 2, "dtype": "f32 (fp64 geometry/chain)", "data": "synthetic",
             # the step's dominant kernel (raster backward, ~40% of it), from the committed ncu capture
             "issue_roofline": ncu_issue("train_raster_bwd")}
+
+
+def run_config1(a, dev, steps=200):
+    """BASELINE.json configs[0]: synthetic 7D scene, 10k primitives, one 128x128
+    view at t = 0.5, forward + backward (testing.random_scene(7, 10000, seed=1),
+    random_camera(128, seed=2), target from a second scene: SURVEY 8(d)).
+    A step = render + L1/SSIM image gradient + raster backward + chain into
+    the parameter gradient.  Timed three ways: the device engine step by
+    step (eager launches), the same step captured once in a CUDA graph and
+    replayed (the step is ~20 small launches: launch-latency bound), and the
+    reference-signature gradients.backward() with host arrays; next to the
+    CPU oracle port of the reference on the same step."""
+    import torch
+    from oracle import ubs_oracle as O
+    from paper_2510_03312_b200 import engine, synthetic as S
+    from paper_2510_03312_b200.gradients import backward
+    from paper_2510_03312_b200.types import DEFAULT_SETTINGS, LossConfig, Query, quantize_f32
+    sc = quantize_f32(S.random_scene(7, 10000, seed=1))
+    cam = S.random_camera(128, 2)
+    q = Query.view_time(0.5, cam.forward)
+    tgt = np.clip(O.render_frame(quantize_f32(S.random_scene(7, 5000, seed=978)), cam, q,
+                                 DEFAULT_SETTINGS)["image"], 0.0, 1.0)
+    cfg = LossConfig()
+    ds = engine.DeviceScene.from_scene(sc, device=dev)
+    ws = engine.Workspace(dev, "fp32")
+    target = torch.from_numpy(tgt).float().to(dev)
+    grad = torch.zeros(ds.params.shape, dtype=torch.float32, device=dev)
+    engine.render_frame(ws, ds, cam, q, sync=True)  # sizes the pair buffers
+    ws.ensure_pairs(int(ws.pair_cap * 1.5))
+
+    def step():
+        fr = engine.render_frame(ws, ds, cam, q, sync=False)
+        ws.loss_parts.zero_()
+        g_img, _ = engine.loss_image_grad(fr, target, cfg.lambda_ssim, cfg.loss_scale)
+        engine.backward_frame(fr, ds, g_img, grad)
+
+    def timed(fn, n):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    for _ in range(5):
+        step()
+    eager_ms = timed(step, steps)
+    engine.check_status(ws)
+    graph_ms, graph_err = None, None
+    try:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        graph_ms = timed(g.replay, steps)
+        engine.check_status(ws)
+    except Exception as e:  # report, keep the eager numbers
+        graph_err = f"{type(e).__name__}: {e}"[:200]
+    frames = [(cam, q, tgt)]
+    backward(sc, frames, cfg, DEFAULT_SETTINGS)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        backward(sc, frames, cfg, DEFAULT_SETTINGS)
+    dropin_ms = (time.perf_counter() - t0) / 10 * 1e3
+    O.set_threads(os.cpu_count() or 1)
+    O.backward(sc, frames, cfg, DEFAULT_SETTINGS)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        O.backward(sc, frames, cfg, DEFAULT_SETTINGS)
+    cpu_ms = (time.perf_counter() - t0) / 3 * 1e3
+    return {"workload": "config 1: 7D random_scene(7, 10000, seed=1), 128x128 random_camera(128, 2), t = 0.5, "
+                        "forward + L1/SSIM + backward to raw parameters",
+            "unit": "steps/s", "eager": {"value": 1e3 / eager_ms, "ms_per_step": eager_ms},
+            "cuda_graph": {"value": 1e3 / graph_ms, "ms_per_step": graph_ms} if graph_ms else {"error": graph_err},
+            "dropin_backward": {"value": 1e3 / dropin_ms, "ms_per_step": dropin_ms,
+                                "path": "gradients.backward(scene, [(cam, query, target)]) host arrays in, "
+                                        "SceneGrads out"},
+            "cpu_baseline": {"value": 1e3 / cpu_ms, "ms_per_step": cpu_ms, "cores": os.cpu_count() or 1,
+                             "kind": "port"}}
 
 
 def run_other_configs(a, dev, frames=64):
@@ -555,8 +642,6 @@ def run_ours(a, rank, world, local_rank):
     dropin = None
     if rank == 0 and not a.no_dropin:
         from paper_2510_03312_b200 import raster as R
-        del sink
-        torch.cuda.empty_cache()
         R.render(scene, cam, frame_query(a.nd, cam, 0), DEFAULT_SETTINGS)  # warm: workspace, pinned staging
         t0 = time.perf_counter()
         for k in range(a.dropin_frames):
@@ -593,7 +678,17 @@ def run_ours(a, rank, world, local_rank):
         torch.cuda.empty_cache()
         if world == 1:
             other = run_other_configs(a, dev)
+            other["config1"] = run_config1(a, dev)
         train = run_train(a, rank, world, local_rank)
+        if world == 1 and not a.no_train_batches:
+            train["batches"] = {str(a.train_views_per_gpu): train["value"]}
+            for b in (16, 32):  # BASELINE config 5 batches on one GPU
+                if b != a.train_views_per_gpu:
+                    import copy
+                    ab = copy.copy(a)
+                    ab.train_views_per_gpu = b
+                    torch.cuda.empty_cache()
+                    train["batches"][str(b)] = run_train(ab, rank, world, local_rank)["value"]
 
     if rank != 0:
         return None

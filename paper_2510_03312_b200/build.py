@@ -45,15 +45,25 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
-        return OUT
-    BUILD.mkdir(exist_ok=True)
+CHECKED_OUT = PKG / "libubs_b200_checked.so"  # -DUBS_CHECKED: device bounds guards (tests/test_gpu_checked.py)
+
+
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path:
+    """nvcc every csrc/*.cu for sm_100a and link the shared library.
+    ``variant="checked"`` builds the bounds-checked variant
+    (libubs_b200_checked.so, -DUBS_CHECKED) from the same sources."""
+    out = CHECKED_OUT if variant == "checked" else OUT
+    defines = ["-DUBS_CHECKED"] if variant == "checked" else []
+    if not force and out.exists() and not (variant == "" and needs_build()) and \
+            not (variant and any(p.stat().st_mtime > out.stat().st_mtime for p in CSRC.glob("*"))):
+        return out
+    bdir = BUILD / variant if variant else BUILD
+    bdir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
 
     def compile_one(src: Path):
-        obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = bdir / (src.stem + ".o")
+        cmd = [nvcc, *ARCH, *FLAGS, *defines, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stderr[-6000:]}")
@@ -61,16 +71,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         results = list(ex.map(compile_one, sources()))
-    (BUILD / "ptxas.log").write_text("".join(log for _, log in results))
-    tmp = OUT.with_suffix(f".{os.getpid()}.tmp.so")
+    (bdir / "ptxas.log").write_text("".join(log for _, log in results))
+    tmp = out.with_suffix(f".{os.getpid()}.tmp.so")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for o, _ in results], "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    os.replace(tmp, OUT)
+    os.replace(tmp, out)
     if verbose:
-        print(f"built {OUT}")
-    return OUT
+        print(f"built {out}")
+    return out
 
 
 def torch_ops_need_build() -> bool:

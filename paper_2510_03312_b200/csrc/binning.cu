@@ -83,6 +83,7 @@ __global__ void depth_scatter_kernel(const uint64_t *__restrict__ key64, const u
     if (k == kInvisibleKey) return;
     const uint32_t b = depth_bucket(depth_buckets(range, logB), k);
     const uint32_t pos = start[b] + atomicSub(hist + b, 1u) - 1u;
+    if (!UBS_GUARD(pos < (uint32_t)n, kChkRank)) return;
     tkey[pos] = k;
     tid[pos] = (uint32_t)i;
 }
@@ -105,6 +106,7 @@ __global__ void depth_rank_kernel(const unsigned long long *__restrict__ range, 
         const uint64_t kq = tkey[q];
         rank += (kq < k || (kq == k && tid[q] < id)) ? 1u : 0u;
     }
+    if (!UBS_GUARD(s0 + rank < s1 && s1 <= *n_visible, kChkRank)) return;
     order[s0 + rank] = id;
     rect_sorted[s0 + rank] = tile_count[id] != 0 ? rect[id] : kNoRect;
 }
@@ -357,7 +359,8 @@ __device__ __forceinline__ FlatBatch flat_batch(uint64_t q, bool has, uint32_t i
     st.excl[lane] = excl;
     st.id[lane] = id;
     if (fb.fast)
-        for (int i = 0; i < fb.nb; ++i) st.owner[excl + i] = (uint8_t)lane;
+        for (int i = 0; i < fb.nb; ++i)
+            if (UBS_GUARD(excl + i < kOwnerCap, kChkOwner)) st.owner[excl + i] = (uint8_t)lane;
     __syncwarp();
     return fb;
 }
@@ -377,6 +380,7 @@ __device__ __forceinline__ int flat_locate(const FlatBatch &fb, const FlatStage 
         }
         j = lo;  // first lane whose inclusive prefix exceeds f
     }
+    if (!UBS_GUARD(j >= 0 && j < 32, kChkLocate)) j = 0;
     q = st.q[j];
     const int excl = st.excl[j];
     const int b0 = (int)(q & 0xFFFF) / kBand, g0 = (int)((q >> 16) & 0xFFFF) / kRows;
@@ -391,7 +395,7 @@ __device__ __forceinline__ int flat_locate(const FlatBatch &fb, const FlatStage 
 
 // count the (rank, bucket) pairs of ranks [r0, r1) into cnt (shared atomics)
 __device__ __forceinline__ void count_slice(const uint64_t *__restrict__ rect_sorted, int64_t r0, int64_t r1,
-                                            int NB, uint32_t *cnt, int lane, FlatStage &st) {
+                                            int NB, int nbk, uint32_t *cnt, int lane, FlatStage &st) {
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int64_t r = rb + lane;
         uint64_t q = 0;
@@ -407,7 +411,7 @@ __device__ __forceinline__ void count_slice(const uint64_t *__restrict__ rect_so
             int j, band, grp;
             uint64_t q;
             const int k = flat_locate(fb, st, min(f, fb.total - 1), NB, j, q, band, grp);
-            if (f < fb.total) atomicAdd(&cnt[k], 1u);
+            if (f < fb.total && UBS_GUARD(k >= 0 && k < nbk, kChkBucket)) atomicAdd(&cnt[k], 1u);
         }
     }
 }
@@ -424,7 +428,7 @@ bucket_hist_kernel(const uint64_t *__restrict__ rect_sorted, const uint32_t *__r
     const int64_t nv = *n_visible;
     const int64_t c0 = (int64_t)blockIdx.x * kCtaRanks;
     const int64_t r0 = min(c0 + (int64_t)w * kChunkRanks, nv), r1 = min(r0 + kChunkRanks, nv);
-    count_slice(rect_sorted, r0, r1, NB, scnt_all + w * nbk, lane, stage[w]);
+    count_slice(rect_sorted, r0, r1, NB, nbk, scnt_all + w * nbk, lane, stage[w]);
     __syncthreads();
     // per-warp counts (the scatter's intra-chunk offsets) and the chunk totals
     uint32_t *hw = whist + (int64_t)blockIdx.x * kBinWarps * nbk;
@@ -561,7 +565,8 @@ bucket_scatter_kernel(const uint32_t *__restrict__ order, const uint64_t *__rest
             const uint32_t idj = st.id[j];
             const unsigned same = __match_any_sync(0xffffffffu, act ? k : -1);
             const uint32_t base = sfill[act ? k : 0];
-            if (act) entries[base + __popc(same & lt)] = bucket_entry(idj, qj, band, grp);
+            if (act && UBS_GUARD((int64_t)base + __popc(same & lt) < capacity && k < nbk, kChkEntry))
+                entries[base + __popc(same & lt)] = bucket_entry(idj, qj, band, grp);
             __syncwarp();
             if (act && (same >> lane) == 1u) sfill[k] = base + __popc(same);  // highest lane of the group
             __syncwarp();
@@ -624,7 +629,7 @@ tile_lists_kernel(const uint64_t *__restrict__ entries, const uint32_t *__restri
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t pos = written + __popc(bal[u] & lt);
-                if (p[u] && pos < want) dst[pos] = idv[u];
+                if (p[u] && pos < want && UBS_GUARD((int64_t)t0 + pos < capacity, kChkList)) dst[pos] = idv[u];
                 written += __popc(bal[u]);
             }
         }
@@ -742,3 +747,5 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
+
+UBS_CHECKED_ACCESSOR(binning)

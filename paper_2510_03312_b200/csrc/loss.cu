@@ -634,3 +634,5 @@ extern "C" int ubs_loss_image_grad(const void *image, const void *target, int32_
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
+
+UBS_CHECKED_ACCESSOR(loss)

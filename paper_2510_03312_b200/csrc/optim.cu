@@ -222,3 +222,5 @@ extern "C" int ubs_regulariser_value(const void *params, int32_t param_f64, int6
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
+
+UBS_CHECKED_ACCESSOR(optim)

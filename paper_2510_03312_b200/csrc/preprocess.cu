@@ -110,6 +110,7 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
                 count = (uint32_t)((c - a + 1) * (d - b + 1));
                 // 2D difference array: a prefix sum over it gives every tile's pair count
                 const int gw = TX + 1;
+                if (!UBS_GUARD(c + 1 <= (uint64_t)TX && d + 1 <= (uint64_t)TY, kChkGrid)) return;
                 atomicAdd(pb.tile_grid + (int)b * gw + (int)a, 1);
                 atomicAdd(pb.tile_grid + (int)b * gw + (int)c + 1, -1);
                 atomicAdd(pb.tile_grid + ((int)d + 1) * gw + (int)a, -1);
@@ -535,3 +536,5 @@ extern "C" int ubs_scene_statics(const UbsView *v, void *statics, ubs_stream_t s
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
+
+UBS_CHECKED_ACCESSOR(preprocess)

@@ -447,3 +447,5 @@ extern "C" int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int
     UBS_CUDA_CHECK();
     return UBS_OK;
 }
+
+UBS_CHECKED_ACCESSOR(prim_bwd)

@@ -256,7 +256,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         if (threadIdx.x == 0) FWD_STAT(6, 1);
         const uint32_t q = b + threadIdx.x;
         uint32_t cover = 0;
-        if (q < end) {
+        if (q < end && UBS_GUARD((int64_t)q < P.pair_capacity, kChkPair)) {
             const uint32_t id = ids[q];
             const float4 *r = reinterpret_cast<const float4 *>(recs + id);
             float4 *d = reinterpret_cast<float4 *>(srec + threadIdx.x);
@@ -334,7 +334,9 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     if (a > clamp_lo || Tn < tmin_hi) {
                         if (a > clamp_lo) {
                             if (a > clamp) {
-                                if (a * (1.0f - qrel) > clamp) hit[sid[32 * k + 31 - (int)p]] = 1;
+                                if (a * (1.0f - qrel) > clamp &&
+                                UBS_GUARD(32 * k + 31 - (int)p >= 0 && 32 * k + 31 - (int)p < kTileThreads, kChkSplat))
+                                hit[sid[32 * k + 31 - (int)p]] = 1;
                                 else flag = 1;
                                 a = clamp;
                                 om = one_minus_clamp;
@@ -368,7 +370,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     }
     if (capped && inside && !done) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
     if (D > kImgErrTol * T || edge < 0.0f) flag = 1;
-    if (inside) {
+    if (inside && UBS_GUARD((int64_t)py * P.W + px < (int64_t)P.W * P.H, kChkPixel)) {
         const int64_t pix = (int64_t)py * P.W + px;
         image[3 * pix] = fmaf(T, (float)P.bg[0], a0);
         image[3 * pix + 1] = fmaf(T, (float)P.bg[1], a1);
@@ -383,7 +385,8 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (fl) fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
+        if (fl && UBS_GUARD((int64_t)base + __popc(fb & ((1u << lane) - 1u)) < (int64_t)P.W * P.H, kChkFix))
+            fix_list[base + __popc(fb & ((1u << lane) - 1u))] = (uint32_t)((int64_t)py * P.W + px);
     }
     __syncthreads();
     const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
@@ -1020,7 +1023,7 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                         if constexpr (kDet) {
                             const uint32_t sl = sslot[jj];
                             if ((int64_t)sl < det.capacity) det.part[(int64_t)sl * 10 + idx] = mine;
-                        } else {
+                        } else if (UBS_GUARD(jj >= 0 && jj < kBatch && idx >= 0 && idx < 10, kChkGrad)) {
                             atomicAdd(grad2d + (int64_t)sid[jj] * kGrad2dStride + idx, mine);
                         }
                     }
@@ -1240,3 +1243,5 @@ extern "C" size_t ubs_det_temp_bytes(int64_t n) {
                                   (int)(n > 0 ? n : 1) + 1);
     return need;
 }
+
+UBS_CHECKED_ACCESSOR(raster)

@@ -15,6 +15,52 @@
 
 namespace ubs {
 
+// Bounds-checked build (-DUBS_CHECKED; tests/test_gpu_checked.py): every
+// guarded index is tested on the device, a failing test sets its bit in
+// g_checked_status (read with ubs_debug_checked_status) and the access is
+// skipped.  The product build compiles the guards away.  (compute-sanitizer
+// is not available on the GPU pool, so this is the memory-safety evidence.)
+#ifdef UBS_CHECKED
+__device__ unsigned int g_checked_status;
+__device__ __forceinline__ bool ubs_guard(bool ok, unsigned int bit) {
+    if (!ok) atomicOr(&g_checked_status, bit);
+    return ok;
+}
+#define UBS_GUARD(cond, bit) ::ubs::ubs_guard((cond), (bit))
+// one status word per translation unit (whole-program compilation): each .cu
+// exports its own reader, ubs_debug_checked_<tu>
+#define UBS_CHECKED_ACCESSOR(tu)                                                                  \
+    extern "C" int ubs_debug_checked_##tu(unsigned int *out, int reset) {                        \
+        if (cudaDeviceSynchronize() != cudaSuccess) return -2;                                     \
+        if (cudaMemcpyFromSymbol(out, ::ubs::g_checked_status, sizeof(unsigned int)) != cudaSuccess) \
+            return -2;                                                                             \
+        if (reset) {                                                                               \
+            const unsigned int z = 0;                                                              \
+            cudaMemcpyToSymbol(::ubs::g_checked_status, &z, sizeof(z));                             \
+        }                                                                                          \
+        return 0;                                                                                  \
+    }
+#else
+#define UBS_GUARD(cond, bit) true
+#define UBS_CHECKED_ACCESSOR(tu)
+#endif
+// guard bits
+enum : unsigned int {
+    kChkOwner = 1u << 0,      // binning FlatStage owner[] slot
+    kChkLocate = 1u << 1,     // binning flat index -> (rank lane, bucket)
+    kChkBucket = 1u << 2,     // binning per-warp bucket counter index
+    kChkEntry = 1u << 3,      // binning level-1 entry write
+    kChkList = 1u << 4,       // binning level-2 tile-list write
+    kChkRank = 1u << 5,       // depth sort slot / rank write
+    kChkGrid = 1u << 6,       // preprocess tile-grid corner
+    kChkSplat = 1u << 7,      // raster shared splat index / ballot word
+    kChkHit = 1u << 8,        // raster alpha_clamped write
+    kChkFix = 1u << 9,        // raster fix-up list write
+    kChkPixel = 1u << 10,     // raster image write
+    kChkPair = 1u << 11,      // raster / backward tile-list read
+    kChkGrad = 1u << 12,      // backward grad2d / partial write
+};
+
 constexpr int kTile = 16;
 constexpr int kTileThreads = kTile * kTile;
 constexpr uint64_t kInvisibleKey = 0xFFFFFFFFFFFFFFFFull;
