@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-inflight", type=int, default=8, help="views in flight per GPU in the training step")
     ap.add_argument("--train-group", type=int, default=8, help="training views per shared preprocess")
+    ap.add_argument("--train-ppl", type=int, default=4, choices=[2, 4, 8],
+                    help="raster backward pixels per lane in the training step")
     ap.add_argument("--train-only", action="store_true",
                     help="only the config-5 training step (its own JSON line; for profiling)")
     return ap.parse_args()
@@ -277,7 +279,7 @@ def run_train(a, rank, world, local_rank):
     del tws, tds
     views = list(zip(cams, views_q, targets))
     step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=a.train_inflight,
-                                                            group=a.train_group))
+                                                            group=a.train_group, pixels_per_lane=a.train_ppl))
     adam = sharding.DeviceAdam(ds.params, 7)
     cfg = LossConfig()
     grad = step.backend.new_grad()

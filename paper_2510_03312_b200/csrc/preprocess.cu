@@ -118,8 +118,8 @@ __device__ __forceinline__ void preprocess_emit(const UbsView &v, const UbsPrimB
             }
         }
     }
-    pb.depth_key[i] = vis ? (uint64_t)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
-    my_key = pb.depth_key[i];
+    my_key = vis ? (unsigned long long)__double_as_longlong(g.tcam[2]) : kInvisibleKey;
+    pb.depth_key[i] = my_key;
     pb.rect[i] = rect;
     pb.tile_count[i] = count;
     my_count = count;

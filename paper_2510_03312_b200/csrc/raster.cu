@@ -893,19 +893,23 @@ __device__ __forceinline__ bool bwd_visit(BwdPixel &p, const float g0, const flo
     return true;
 }
 
-template <int NP>
-__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 32 : 4 * NP)  // 64 registers
+template <int NP, bool kDet>
+__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 24 : 4 * NP)  // 64 registers (NP = 8: 85)
 raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                     const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
                     float *__restrict__ grad2d, const DetOut<float> det) {
     constexpr int kThreads = kTileThreads / NP;
-    constexpr int kBatch = NP >= 4 ? 128 : 256;  // NP = 2: 2 records per thread, half the barriers of 128
+    // NP = 2: 2 records per thread, half the barriers of 128; NP = 8 (one warp
+    // per tile): 64, so ~24 one-warp CTAs fit an SM's shared memory
+    constexpr int kBatch = NP == 8 ? 64 : NP >= 4 ? 128 : 256;
     constexpr int kWords = kBatch / 32;
     constexpr int kBlocks = kTileThreads / 32;  // the forward's 8x4 blocks per tile
-    // NP = 8: the deterministic layout, one warp per tile owning all 8 blocks,
-    // tile partials written to per-(primitive, tile) slots instead of atomics
-    constexpr bool kDet = NP == 8;
+    // NP = 8: one warp per tile owning all 8 blocks (one reduction per
+    // (tile, splat)); kDet (NP = 8 only): tile partials written to per-
+    // (primitive, tile) slots instead of atomics
+    static_assert(!kDet || NP == 8, "deterministic mode is the one-warp-per-tile layout");
+    constexpr bool kOneWarp = NP == 8;
     __shared__ Rec32 srec[kBatch];
     __shared__ uint32_t sid[kBatch];
     __shared__ uint32_t sslot[kDet ? kBatch : 1];
@@ -927,7 +931,7 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     __syncthreads();
 #pragma unroll
     for (int h = 0; h < NP; ++h) {
-        const int blk = kDet ? h : blk0 + 2 * h;
+        const int blk = kOneWarp ? h : blk0 + 2 * h;
         const int x = tx * kTile + (blk & 1) * 8 + (lane & 7);
         const int y = ty * kTile + (blk >> 1) * 4 + (lane >> 3);
         BwdPixel &p = px[h];
@@ -990,7 +994,7 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             uint32_t wr[NP], bits = 0;
 #pragma unroll
             for (int h = 0; h < NP; ++h) {
-                wr[h] = swm[kDet ? h : blk0 + 2 * h][k];
+                wr[h] = swm[kOneWarp ? h : blk0 + 2 * h][k];
                 bits |= wr[h];
             }
             const int lim = top - 32 * k;  // keep bits < lim
@@ -1181,7 +1185,8 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
                                    const UbsImageBuffers *ib, const UbsGradBuffers *gb, ubs_stream_t stream) {
     if (!v || !pb || !bb || !ib || !gb || !gb->g_image || !gb->grad2d) return UBS_E_ARGS;
     if ((gb->grad2d_f64 != 0) != (ib->raster_f64 != 0)) return UBS_E_ARGS;
-    if (gb->bwd_pixels_per_lane != 0 && gb->bwd_pixels_per_lane != 2 && gb->bwd_pixels_per_lane != 4)
+    if (gb->bwd_pixels_per_lane != 0 && gb->bwd_pixels_per_lane != 2 && gb->bwd_pixels_per_lane != 4 &&
+        gb->bwd_pixels_per_lane != 8)
         return UBS_E_ARGS;
     const RasterParams P = make_params(*v, *pb, *bb);
     const int n_tiles = P.TX * ((P.H + kTile - 1) / kTile);
@@ -1209,7 +1214,7 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
                                                          det.capacity, (double *)gb->grad2d);
         } else {
             const DetOut<float> det{gb->det_slot_off, pb->rect, (float *)gb->det_partials, gb->det_capacity};
-            raster_bwd32_kernel<8><<<n_tiles, kTileThreads / 8, 0, s>>>(
+            raster_bwd32_kernel<8, true><<<n_tiles, kTileThreads / 8, 0, s>>>(
                 P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
                 (const float *)gb->g_image, (float *)gb->grad2d, det);
             det_reduce_kernel<float><<<rb, 256, 0, s>>>(gb->det_slot_off, pb->tile_count, det.part, v->n,
@@ -1224,12 +1229,16 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
             P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
             (const double *)gb->g_image, (double *)gb->grad2d);
     } else {
-        if (gb->bwd_pixels_per_lane == 4)
-            raster_bwd32_kernel<4><<<n_tiles, kTileThreads / 4, 0, s>>>(
+        if (gb->bwd_pixels_per_lane == 8)
+            raster_bwd32_kernel<8, false><<<n_tiles, kTileThreads / 8, 0, s>>>(
+                P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
+                (const float *)gb->g_image, (float *)gb->grad2d, none);
+        else if (gb->bwd_pixels_per_lane == 4)
+            raster_bwd32_kernel<4, false><<<n_tiles, kTileThreads / 4, 0, s>>>(
                 P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
                 (const float *)gb->g_image, (float *)gb->grad2d, none);
         else
-            raster_bwd32_kernel<2><<<n_tiles, kTileThreads / 2, 0, s>>>(
+            raster_bwd32_kernel<2, false><<<n_tiles, kTileThreads / 2, 0, s>>>(
                 P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (const float *)ib->t_stop, ib->n_contrib,
                 (const float *)gb->g_image, (float *)gb->grad2d, none);
     }

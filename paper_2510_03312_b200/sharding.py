@@ -60,12 +60,13 @@ class GpuViewBackend:
     a slot is reused only after the gradient stream is done with it."""
 
     def __init__(self, ds: engine.DeviceScene, precision: str = "fp32", settings=DEFAULT_SETTINGS,
-                 grad_dtype=torch.float32, depth: int = 1, group: int = 1):
+                 grad_dtype=torch.float32, depth: int = 1, group: int = 1, pixels_per_lane: int = 4):
         self.ds = ds
         self.settings = settings
         self.grad_dtype = grad_dtype
         self.depth = max(1, int(depth))
         self.group = max(1, min(int(group), self.depth))
+        self.pixels_per_lane = int(pixels_per_lane)  # raster backward layout (UbsGradBuffers.bwd_pixels_per_lane)
         self.workspaces = [engine.Workspace(ds.device, precision) for _ in range(self.depth)]
         self.ws = self.workspaces[0]
         multi = self.depth > 1
@@ -184,8 +185,8 @@ class GpuViewBackend:
                     fr = engine.render_frame(ws, ds, cam, query, settings, sync=sync or ws.pair_cap == 0)
                 ws.loss_parts.zero_()
                 g_img, parts = engine.loss_image_grad(fr, target, cfg.lambda_ssim, scale)
-                # four pixels per lane: the layout that runs best beside the other views in flight
-                gb = engine.backward_raster(fr, ds, g_img, self._grad, pixels_per_lane=4)
+                # four pixels per lane (default): the layout that runs best beside the other views in flight
+                gb = engine.backward_raster(fr, ds, g_img, self._grad, pixels_per_lane=self.pixels_per_lane)
                 self._rec[i:i + 1] += self._term(fr, parts, cfg)
                 done = torch.cuda.Event()
                 done.record(s)
