@@ -309,6 +309,7 @@ def run_train(a, rank, world, local_rank):
                        "parallelism": f"dp{world} (view sharding, NCCL "
                                    f"all-reduce of the {4 * 38 * a.train_prims / 1e6:.0f} MB gradient)"},
             "steps": a.train_steps, "warmup": 2, "dtype": "f32 (fp64 geometry/chain)", "data": "synthetic",
+            "retries": step.retries,
             # the step's dominant kernel (raster backward, ~40% of it), from the committed ncu capture
             "issue_roofline": ncu_issue("train_raster_bwd")}
 

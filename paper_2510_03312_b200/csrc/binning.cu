@@ -333,10 +333,9 @@ __device__ __forceinline__ uint64_t bucket_entry(uint32_t id, uint64_t q, int ba
     const int x0 = max((int)(q & 0xFFFF) - bx, 0), x1 = min((int)((q >> 32) & 0xFFFF) - bx, kBand - 1);
     const int y0 = max((int)((q >> 16) & 0xFFFF) - by, 0), y1 = min((int)(q >> 48) - by, kRows - 1);
     const uint32_t row = ((2u << x1) - 1u) & ~((1u << x0) - 1u);  // bits x0..x1
-    uint32_t mask = 0;
-#pragma unroll
-    for (int y = 0; y < kRows; ++y)
-        if (y >= y0 && y <= y1) mask |= row << (kBand * y);
+    // the row replicated into bytes y0..y1 (kBand = 8 bits per tile row)
+    const uint32_t rows = (0xFFFFFFFFu >> (8 * (kRows - 1 - y1))) & (0xFFFFFFFFu << (8 * y0));
+    const uint32_t mask = (row * 0x01010101u) & rows;
     return (uint64_t)id | ((uint64_t)mask << 32);
 }
 
@@ -386,8 +385,13 @@ __device__ __forceinline__ int flat_locate(const FlatBatch &fb, const FlatStage 
     const int b0 = (int)(q & 0xFFFF) / kBand, g0 = (int)((q >> 16) & 0xFFFF) / kRows;
     const int nbw = (int)((q >> 32) & 0xFFFF) / kBand - b0 + 1;
     const int i = f - excl;
-    // floor((i + 0.5) / nbw) in fp32 is exact for i < 2^16, nbw < 2^12
-    const int r = (int)(((float)i + 0.5f) * __frcp_rn((float)nbw));
+    // floor((i + 0.5) / nbw) with the MUFU reciprocal: (i + 0.5) / nbw is at
+    // least 0.5 / nbw from an integer and the product's relative error is
+    // < 3 * 2^-24, so the floor is exact while i < 2^24 / 6 (i < buckets of one
+    // rect: 32k at 16K x 16K)
+    float rc;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"((float)nbw));
+    const int r = (int)(((float)i + 0.5f) * rc);
     band = b0 + (i - r * nbw);
     grp = g0 + r;
     return grp * NB + band;

@@ -41,44 +41,47 @@ statics_kernel(const UbsView v, void *out) {
 }
 
 // Block-wide visible count, pair total and depth range of one view, added to
-// the view's counters with one atomic each per CTA.
+// the view's counters with one atomic each per CTA: warp totals by
+// single-instruction reductions (REDUX) into per-warp shared slots, summed by
+// thread 0 (no shared-memory atomics).  The depth range is kept at the
+// granularity of the keys' high 32 bits (lo rounded down, hi up): it still
+// bounds every visible key, which is all the depth bucketing needs.
 struct PreAgg {
-    uint32_t vis;
-    unsigned long long pairs, dmin, dmax;
+    uint32_t vis[kPreThreads / 32], pairs[kPreThreads / 32], kmin[kPreThreads / 32], kmax[kPreThreads / 32];
 };
 
 __device__ __forceinline__ void preprocess_aggregate(PreAgg &agg, const UbsPrimBuffers &pb, bool vis,
                                                      uint32_t my_count, unsigned long long my_key) {
-    // warp totals with single-instruction reductions (REDUX): the visible
-    // count, the tile pairs (< 2^32 per warp), and the depth range at the
-    // granularity of the keys' high 32 bits (lo rounded down, hi up: still
-    // bounds every visible key, which is all the depth bucketing needs)
     const uint32_t full = 0xffffffffu;
+    const int w = threadIdx.x >> 5;
     const unsigned ballot = __ballot_sync(full, vis);
-    const uint32_t wsum = __reduce_add_sync(full, my_count);
+    const uint32_t wsum = __reduce_add_sync(full, my_count);  // < 2^32 per warp
     const uint32_t khi = (uint32_t)(my_key >> 32);
     const uint32_t kmin = __reduce_min_sync(full, vis ? khi : 0xffffffffu);
     const uint32_t kmax = __reduce_max_sync(full, vis ? khi : 0u);
     if ((threadIdx.x & 31) == 0) {
-        if (ballot) {
-            atomicAdd(&agg.vis, (uint32_t)__popc(ballot));
-            atomicMin(&agg.dmin, (unsigned long long)kmin << 32);
-            atomicMax(&agg.dmax, ((unsigned long long)kmax << 32) | 0xffffffffull);
-        }
-        if (wsum) atomicAdd(&agg.pairs, (unsigned long long)wsum);
+        agg.vis[w] = (uint32_t)__popc(ballot);
+        agg.pairs[w] = wsum;
+        agg.kmin[w] = kmin;
+        agg.kmax[w] = kmax;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (agg.vis) {
-            atomicAdd(pb.n_visible, agg.vis);
-            atomicMin(pb.depth_range, agg.dmin);
-            atomicMax(pb.depth_range + 1, agg.dmax);
+        uint32_t nv = 0, lo = 0xffffffffu, hi = 0u;
+        unsigned long long np = 0;
+#pragma unroll
+        for (int k = 0; k < kPreThreads / 32; ++k) {
+            nv += agg.vis[k];
+            np += agg.pairs[k];
+            lo = min(lo, agg.kmin[k]);
+            hi = max(hi, agg.kmax[k]);
         }
-        if (agg.pairs) atomicAdd(pb.n_pairs, agg.pairs);
-        agg.vis = 0;
-        agg.pairs = 0;
-        agg.dmin = ~0ull;
-        agg.dmax = 0;
+        if (nv) {
+            atomicAdd(pb.n_visible, nv);
+            atomicMin(pb.depth_range, (unsigned long long)lo << 32);
+            atomicMax(pb.depth_range + 1, ((unsigned long long)hi << 32) | 0xffffffffull);
+        }
+        if (np) atomicAdd(pb.n_pairs, np);
     }
 }
 
@@ -200,7 +203,6 @@ preprocess_kernel(const UbsView v, const UbsPrimBuffers pb, int want_rec32) {
     const int64_t base = (int64_t)blockIdx.x * kPreThreads;
     const int64_t n = v.n;
     const int nloc = (int)min((int64_t)kPreThreads, n - base);
-    if (threadIdx.x == 0) { agg.vis = 0; agg.pairs = 0; agg.dmin = ~0ull; agg.dmax = 0; }
     if constexpr (!kStatic) {
         const PT *src = reinterpret_cast<const PT *>(v.params) + base * P;
         for (int k = threadIdx.x; k < nloc * P; k += kPreThreads) stage[k] = src[k];
@@ -255,7 +257,6 @@ preprocess_views_kernel(const __grid_constant__ PreViews m) {
     const int nloc = (int)min((int64_t)kPreThreads, m.v[0].n - base);
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar);
     if (threadIdx.x == 0) {
-        agg.vis = 0; agg.pairs = 0; agg.dmin = ~0ull; agg.dmax = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const char *src = reinterpret_cast<const char *>(m.v[0].statics) + (size_t)blockIdx.x * kBlockBytes;
@@ -288,7 +289,7 @@ preprocess_views_kernel(const __grid_constant__ PreViews m) {
             preprocess_emit<C>(v, pb, m.want_rec32, base + t, g, m.sqrt_tau, vis, my_count, my_key);
         }
         preprocess_aggregate(agg, pb, vis, my_count, my_key);
-        __syncthreads();  // agg reset by thread 0 before the next view adds to it
+        __syncthreads();  // thread 0 has read agg before the next view's warps overwrite it
     }
 }
 

@@ -261,6 +261,7 @@ class ViewShardedStep:
     def __init__(self, backend, group=None):
         self.backend = backend
         self.group = group
+        self.retries = 0  # batches recomputed because an asynchronous view outgrew its buffers
 
     def loss_and_grad(self, views, cfg: LossConfig = LossConfig(), grad: torch.Tensor | None = None,
                       buckets: int = 4):
@@ -307,6 +308,7 @@ class ViewShardedStep:
                 w.wait()
             if float(rec[1]) == 0.0:
                 break
+            self.retries += 1
             b.clear_status()
         loss = cfg.loss_scale * (rec[0] / len(views) + b.regulariser_value(cfg))
         return loss, grad
