@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <cstdlib>
 
 #include "ubs_common.cuh"
 
@@ -391,6 +392,302 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     __syncthreads();
     const unsigned long long tot = block_sum_u64((unsigned long long)cnt, red);
     if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
+}
+
+// ---------------------------------------------------------------------------
+// forward, fp32, two pixels per lane with Blackwell's packed fp32x2 math
+// ---------------------------------------------------------------------------
+// Same algorithm, records, error bound and decisions as raster_fwd32_kernel,
+// pixel for pixel: each of the 4 warps of a 128-thread CTA owns an 8x8 block
+// of the 16x16 tile = two of the 8x4 blocks, and each lane carries the pixel
+// pair (x, y) and (x, y + 4) -- one from each block.  The walk (bit scan,
+// record address, shared loads) is paid once per pair, and the per-pixel
+// arithmetic runs as sm_100 FADD2 / FMUL2 / FFMA2 instructions on the pair
+// (PTX add/mul/fma.rn.f32x2, IEEE round-to-nearest per element, so every
+// pixel sees exactly the scalar kernel's operations and roundings; uniform
+// operands are broadcast by the .F32 operand selector, no moves).  MUFU
+// transcendentals stay scalar.  A warp walks a splat when its cover mask has
+// either block's bit; a pixel whose block bit is clear is out of support
+// (every pixel of a culled block would skip the splat: warp_cover_mask).
+using f32x2 = unsigned long long;
+
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 up2(f32x2 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f32x2 dup2(float a) { return pk2(a, a); }
+// in-place forms for loop-carried pairs (a fresh "=l" output would cost a
+// register-pair copy per visit)
+__device__ __forceinline__ void fma2_acc(f32x2 &c, f32x2 a, f32x2 b) {  // c = a b + c
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void fma2_scale(f32x2 &c, f32x2 a, f32x2 b) {  // c = a c + b (== c a + b)
+    // the accumulator as the B operand: with it as A, ptxas computes into a
+    // fresh pair and copies every loop-carried pair back (10 MOVs per visit)
+    asm("fma.rn.f32x2 %0, %1, %0, %2;" : "+l"(c) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void sub2_acc(f32x2 &c, f32x2 a) {  // c = c - a
+    asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(c) : "l"(a));
+}
+
+constexpr int kX2Threads = kTileThreads / 2;  // 128: 4 warps x 32 lanes x 2 pixels
+constexpr int kX2Warps = kX2Threads / 32;
+
+__global__ void __launch_bounds__(kX2Threads)
+raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
+                      const Rec32 *__restrict__ recs, float *__restrict__ image, float *__restrict__ asum,
+                      float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
+                      unsigned long long *__restrict__ visits, uint32_t *__restrict__ fix_list,
+                      uint32_t *__restrict__ fix_count) {
+    constexpr int kBatch = kTileThreads;      // 256 records per batch, 2 staged per thread
+    constexpr int kWords = kBatch / 32;
+    __shared__ Rec32 srec[kBatch];
+    __shared__ uint32_t sid[kBatch];
+    __shared__ uint32_t swm[kX2Warps][kWords];  // [walking warp][record word] ballot words
+    __shared__ unsigned long long red[kX2Warps];
+    if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
+    const int tile = blockIdx.x;
+    const int ty = tile / P.TX, tx = tile - ty * P.TX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wx = warp & 1, wy = warp >> 1;
+    const int b0 = 2 * (2 * wy) + wx, b1 = b0 + 2;  // this warp's two 8x4 blocks (warp_cover_mask bits)
+    const int lx = 8 * wx + (lane & 7), ly = 8 * wy + (lane >> 3);  // pixel 0; pixel 1 is 4 rows down
+    const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
+    const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
+    uint32_t start, end;
+    bool capped;
+    tile_span(P, ranges, tile, start, end, capped);
+    const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
+    const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    const float clamp_lo = clamp - 0.05f;
+    const float tmin = (float)P.tmin;
+    const float tmin_hi = tmin * (1.0f + 4.0e-3f);
+    const float lxf = (float)lx;
+    const f32x2 lyf = pk2((float)ly, (float)(ly + 4));
+    // per-pixel state as scalars (packed ops read T0:T1 as an adjacent pair; a
+    // loop-carried f32x2 would cost a register-pair copy per visit in ptxas)
+    float T0 = 1.0f, T1 = 1.0f, D0 = 0.0f, D1 = 0.0f;
+    float c00 = 0.0f, c01 = 0.0f, c10 = 0.0f, c11 = 0.0f, c20 = 0.0f, c21 = 0.0f;
+    float edge0 = 1.0f, edge1 = 1.0f;
+    uint32_t cnt0 = in0 ? end - start : 0u, cnt1 = in1 ? end - start : 0u;
+    int flag0 = 0, flag1 = 0;
+    bool done0 = !in0, done1 = !in1;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
+    for (uint32_t b = start; b < end; b += kBatch) {
+        if (__syncthreads_count(done0 && done1) == kX2Threads) break;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int jl = i * kX2Threads + (int)threadIdx.x;
+            const uint32_t q = b + (uint32_t)jl;
+            uint32_t cover = 0;
+            if (q < end && UBS_GUARD((int64_t)q < P.pair_capacity, kChkPair)) {
+                const uint32_t id = ids[q];
+                const float4 *r = reinterpret_cast<const float4 *>(recs + id);
+                float4 *d = reinterpret_cast<float4 *>(srec + jl);
+                sid[jl] = id;
+                const float4 r0 = __ldg(r), r1 = __ldg(r + 1);
+                const float2 o = tile_offset(r0, tx, ty);
+                d[0] = make_float4(o.x, o.y, r0.z, r0.w);
+                d[1] = r1;
+                d[2] = __ldg(r + 2);
+                d[3] = __ldg(r + 3);
+                cover = warp_cover_mask(o.x, o.y, r1);
+            }
+#pragma unroll
+            for (int w = 0; w < kX2Warps; ++w) {
+                const int c0w = 2 * (2 * (w >> 1)) + (w & 1);
+                const uint32_t word = __ballot_sync(0xffffffffu, ((cover >> c0w) | (cover >> (c0w + 2))) & 1u);
+                if (lane == 0) swm[w][jl >> 5] = __brev(word);  // splat order from the highest bit down
+            }
+        }
+        __syncthreads();
+        if (!(done0 && done1)) {
+            const int nw = (int)((min((uint32_t)kBatch, end - b) + 31u) >> 5);
+            for (int k = 0; k < nw && !(done0 && done1); ++k) {
+                uint32_t bits = swm[warp][k];
+                // bit p of the reversed word is splat 32 k + 31 - p, at stop - 64 p
+                const uint32_t stop = sbase + (uint32_t)(32 * k + 31) * (uint32_t)sizeof(Rec32);
+                while (bits) {
+                    const uint32_t p = msb_pos(bits);
+                    bits ^= bit_at(p);
+                    const uint32_t ra = stop - (p << 6);
+                    const float4 r0 = lds128<0>(ra), r1 = lds128<16>(ra);
+                    const float dx = r0.x + lxf;  // the pair shares its column
+                    const f32x2 dy = add2(dup2(r0.y), lyf);
+                    const f32x2 y0 = fma2(dup2(r1.x), dup2(dx), mul2(dup2(r1.y), dy));
+                    const f32x2 y1 = mul2(dup2(r1.z), dy);
+                    const float2 m = up2(fma2(y0, y0, mul2(y1, y1)));
+                    const bool s0 = !done0 && m.x < tau, s1 = !done1 && m.y < tau;
+                    const f32x2 m2 = pk2(m.x, m.y);
+                    const f32x2 tm = sub2(dup2(tau), m2);
+                    // support edge within the m-error band, m in [tau, tau + E): there
+                    // (tau - m) (tau + E - m) <= 0, elsewhere > 0 (in-support pixels too).
+                    // A done pixel is tested as well: that band is ~1e-5 tau wide, a flag
+                    // there is only a spare fix-up.
+                    const float2 eg = up2(mul2(tm, sub2(dup2(r1.w), m2)));
+                    edge0 = fminf(edge0, eg.x);
+                    edge1 = fminf(edge1, eg.y);
+                    if (!(s0 || s1)) continue;
+                    const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
+                    const float2 omx = up2(fma2(m2, dup2(-inv_tau), dup2(1.0f)));
+                    const f32x2 arg = fma2(dup2(r2.x), pk2(lg2_approx(omx.x), lg2_approx(omx.y)), dup2(r3.w));
+                    const float2 ag = up2(arg);
+                    float a0 = s0 ? ex2_approx(ag.x) : 0.0f, a1 = s1 ? ex2_approx(ag.y) : 0.0f;
+                    // q = eb / (tau - m) + qc + 2.1e-7 |arg|, with |arg| = -arg (arg =
+                    // beta lg2(1 - x) + log2(og) <= 0 up to the lg2 approximation's
+                    // 2^-22 near 1, whose 1e-13 effect hides in qc's 4e-7 term)
+                    const float2 tmv = up2(tm);
+                    const float2 qr = up2(fma2(dup2(r3.x), pk2(rcp_approx(tmv.x), rcp_approx(tmv.y)),
+                                               fma2(arg, dup2(-2.1e-7f), dup2(r3.z))));
+                    // zero for a pixel not in support: its w = 0, and q may be +-inf
+                    // (m == tau, or eb = inf for a thin splat) where 0 q would be NaN
+                    const f32x2 q = pk2(s0 ? qr.x : 0.0f, s1 ? qr.y : 0.0f);
+                    if (a0 > clamp_lo || a1 > clamp_lo) {
+                        // clamp band (rare; scalar per pixel, as raster_fwd32_kernel)
+                        const float2 qv = up2(q);
+                        if (a0 > clamp_lo) {
+                            if (a0 > clamp) {
+                                if (a0 * (1.0f - qv.x) > clamp &&
+                                    UBS_GUARD(32 * k + 31 - (int)p < kBatch, kChkSplat))
+                                    hit[sid[32 * k + 31 - (int)p]] = 1;
+                                else flag0 = 1;
+                                a0 = clamp;  // 1 - clamp == one_minus_clamp exactly
+                            } else {
+                                flag0 |= (a0 * (1.0f + qv.x) > clamp);
+                            }
+                        }
+                        if (a1 > clamp_lo) {
+                            if (a1 > clamp) {
+                                if (a1 * (1.0f - qv.y) > clamp &&
+                                    UBS_GUARD(32 * k + 31 - (int)p < kBatch, kChkSplat))
+                                    hit[sid[32 * k + 31 - (int)p]] = 1;
+                                else flag1 = 1;
+                                a1 = clamp;
+                            } else {
+                                flag1 |= (a1 * (1.0f + qv.y) > clamp);
+                            }
+                        }
+                    }
+                    // blend + error-bound update of the pair:
+                    // D' = D (1 - a) + T a q + rounding of 1 - a and of T (1 - a)
+                    const f32x2 a2 = pk2(a0, a1);
+                    const float2 w = up2(mul2(a2, pk2(T0, T1)));
+                    const float2 om = up2(sub2(dup2(1.0f), a2));
+                    const float2 wq = up2(mul2(pk2(w.x, w.y), q));
+                    c00 = fmaf(w.x, r2.y, c00);
+                    c01 = fmaf(w.y, r2.y, c01);
+                    c10 = fmaf(w.x, r2.z, c10);
+                    c11 = fmaf(w.y, r2.z, c11);
+                    c20 = fmaf(w.x, r2.w, c20);
+                    c21 = fmaf(w.y, r2.w, c21);
+                    D0 = fmaf(D0, om.x, wq.x);
+                    D1 = fmaf(D1, om.y, wq.y);
+                    T0 = T0 - w.x;  // T (1 - a) as T - a T (see raster_fwd32_kernel)
+                    T1 = T1 - w.y;
+                    D0 = fmaf(1.2e-7f, T0, D0);
+                    D1 = fmaf(1.2e-7f, T1, D1);
+                    const float2 Tn = make_float2(T0, T1);
+                    if ((s0 && Tn.x < tmin_hi) | (s1 && Tn.y < tmin_hi)) {
+                        // the cut (rare; scalar per pixel): the reference stops before the
+                        // next splat once T < t_min; certified within D + 1e-6 t_min
+                        const float2 Dv = make_float2(D0, D1);
+                        const uint32_t pos = b - start + (uint32_t)(32 * k + 31) - p + 1u;
+                        if (s0 && Tn.x < tmin_hi) {
+                            const float slack = fmaf(1.0e-6f, tmin, Dv.x);
+                            if (Tn.x < tmin) {
+                                flag0 |= (Tn.x > tmin - slack);
+                                flag0 |= Dv.x > kImgErrTol * Tn.x;
+                                done0 = true;
+                                cnt0 = pos;
+                            } else {
+                                flag0 |= (Tn.x < tmin + slack);
+                            }
+                        }
+                        if (s1 && Tn.y < tmin_hi) {
+                            const float slack = fmaf(1.0e-6f, tmin, Dv.y);
+                            if (Tn.y < tmin) {
+                                flag1 |= (Tn.y > tmin - slack);
+                                flag1 |= Dv.y > kImgErrTol * Tn.y;
+                                done1 = true;
+                                cnt1 = pos;
+                            } else {
+                                flag1 |= (Tn.y < tmin + slack);
+                            }
+                        }
+                        if (done0 && done1) bits = 0u;  // ends the walk through the loop condition
+                    }
+                }
+            }
+        }
+    }
+    if (capped && ((in0 && !done0) || (in1 && !done1))) atomicOr(P.status, (uint32_t)UBS_S_LIST_TRUNC);
+    const float2 Tf = make_float2(T0, T1), Df = make_float2(D0, D1), C0 = make_float2(c00, c01),
+                 C1 = make_float2(c10, c11), C2 = make_float2(c20, c21);
+    if (!done0 && Df.x > kImgErrTol * Tf.x) flag0 = 1;
+    if (!done1 && Df.y > kImgErrTol * Tf.y) flag1 = 1;
+    if (!(edge0 > 0.0f)) flag0 = 1;  // some visit had m in [tau, tau + E)
+    if (!(edge1 > 0.0f)) flag1 = 1;
+    const int64_t npix = (int64_t)P.W * P.H;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const bool inside = h ? in1 : in0;
+        const int py = h ? py1 : py0;
+        const float Th = h ? Tf.y : Tf.x;
+        if (inside && UBS_GUARD((int64_t)py * P.W + px < npix, kChkPixel)) {
+            const int64_t pix = (int64_t)py * P.W + px;
+            image[3 * pix] = fmaf(Th, (float)P.bg[0], h ? C0.y : C0.x);
+            image[3 * pix + 1] = fmaf(Th, (float)P.bg[1], h ? C1.y : C1.x);
+            image[3 * pix + 2] = fmaf(Th, (float)P.bg[2], h ? C2.y : C2.x);
+            asum[pix] = 1.0f - Th;  // sum_i a_i T_i telescopes to 1 - T
+            tstop[pix] = Th;
+            ncontrib[pix] = (int32_t)(h ? cnt1 : cnt0);
+        }
+        const bool fl = (h ? flag1 : flag0) && inside;
+        const unsigned fb = __ballot_sync(0xffffffffu, fl);
+        if (fb) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(fix_count, (uint32_t)__popc(fb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const uint32_t at = base + __popc(fb & ((1u << lane) - 1u));
+            if (fl && UBS_GUARD((int64_t)at < npix, kChkFix)) fix_list[at] = (uint32_t)((int64_t)py * P.W + px);
+        }
+    }
+    // processed_pixels: every pixel's count, one atomic per CTA
+    unsigned long long c = (unsigned long long)cnt0 + (unsigned long long)cnt1;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) red[warp] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < kX2Warps; ++w) tot += red[w];
+        if (tot) atomicAdd(visits, tot);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1157,9 +1454,15 @@ extern "C" int ubs_raster_forward(const UbsView *v, const UbsPrimBuffers *pb, co
             (double *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits);
     } else {
         if (!pb->rec32 || !pb->rec64 || !ib->fix_list || !ib->fix_count) return UBS_E_ARGS;
-        raster_fwd32_kernel<<<n_tiles, kTileThreads, 0, s>>>(
-            P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (float *)ib->image, (float *)ib->alpha_sum,
-            (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits, ib->fix_list, ib->fix_count);
+        static const bool scalar = getenv("UBS_RASTER_SCALAR") != nullptr;  // A/B only
+        if (scalar)
+            raster_fwd32_kernel<<<n_tiles, kTileThreads, 0, s>>>(
+                P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (float *)ib->image, (float *)ib->alpha_sum,
+                (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits, ib->fix_list, ib->fix_count);
+        else
+            raster_fwd32x2_kernel<<<n_tiles, kX2Threads, 0, s>>>(
+                P, bb->tile_ranges, bb->tile_ids, (const Rec32 *)pb->rec32, (float *)ib->image, (float *)ib->alpha_sum,
+                (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits, ib->fix_list, ib->fix_count);
     }
     UBS_CUDA_CHECK();
     return UBS_OK;
