@@ -51,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 5
+#define UBS_ABI_VERSION 6
 #define UBS_TILE 16
 
 enum {
@@ -187,6 +187,8 @@ typedef struct UbsImageBuffers {
     uint32_t *fix_list;  /* H*W capacity: pixels re-done in fp64 (fp32 raster only) */
     uint32_t *fix_count; /* [1] */
     int32_t raster_f64;  /* 1 = fp64 raster, 0 = fp32 raster + fp64 fix-up */
+    int32_t raster_scalar; /* fp32 raster kernels: 0 = packed fp32x2 (two pixels per lane, default),
+                              1 = one pixel per lane; the same per-pixel arithmetic and results */
 } UbsImageBuffers;
 
 /* Backward buffers. */

@@ -65,7 +65,7 @@ class UbsBinBuffers(Structure):
 class UbsImageBuffers(Structure):
     _fields_ = [("image", c_void_p), ("alpha_sum", c_void_p), ("t_stop", c_void_p), ("n_contrib", c_void_p),
                 ("hit_clamp", c_void_p), ("visits", c_void_p), ("fix_list", c_void_p), ("fix_count", c_void_p),
-                ("raster_f64", c_int32)]
+                ("raster_f64", c_int32), ("raster_scalar", c_int32)]
 
 
 class UbsGradBuffers(Structure):
@@ -77,7 +77,7 @@ class UbsGradBuffers(Structure):
                 ("det_temp_bytes", c_size_t)]
 
 
-ABI_VERSION = 5  # UBS_ABI_VERSION in include/ubs_b200.h
+ABI_VERSION = 6  # UBS_ABI_VERSION in include/ubs_b200.h
 MAX_VIEWS = 8  # UBS_MAX_VIEWS
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares

@@ -248,6 +248,9 @@ class Workspace:
         self.device = _require_cuda(device)
         self.precision = precision
         self.f64 = precision == "fp64"
+        # fp32 raster kernels: packed fp32x2 pairs (default) or one pixel per lane
+        # (the same per-pixel arithmetic; kept selectable for A/B and tests)
+        self.raster_scalar = False
         self.lib = _lib.load()
         self.n_cap = 0
         self.pix_cap = 0
@@ -402,6 +405,7 @@ class Workspace:
         ib.fix_list = _ptr(self.fix_list)
         ib.fix_count = _ptr(self.counters) + 24
         ib.raster_f64 = 1 if self.f64 else 0
+        ib.raster_scalar = 1 if self.raster_scalar else 0
         return ib
 
 

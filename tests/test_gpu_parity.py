@@ -582,3 +582,34 @@ def test_resident_scene_is_reused_until_invalidated():
         edited = raster.render(sc, cam, qs[0])
     assert not np.array_equal(edited, ref[0])
     assert np.array_equal(edited, raster.render(sc.copy(), cam, qs[0]))
+
+
+@pytest.mark.parametrize("nd,count,size", [(7, 20_000, (320, 200)), (6, 3000, (333, 211))])
+def test_packed_and_scalar_raster_agree_with_oracle(nd, count, size):
+    # the fp32x2 forward (two pixels per lane) and the one-pixel-per-lane forward
+    # run the same per-pixel arithmetic: identical counts and clamp flags,
+    # images within the fix-up's fp64 re-composites of each other, both = oracle;
+    # the packed 4-pixel backward matches the scalar one to float summation order
+    import torch
+    from paper_2510_03312_b200 import engine
+    sc = S.synth(nd, count, seed=nd + 30)
+    cam = S.bench_camera(*size)
+    q = S.bench_query(nd, cam, 0.6)
+    ref = O.render_frame(sc, cam, q, DEFAULT_SETTINGS)
+    ds = engine.DeviceScene.from_scene(sc, device="cuda")
+    outs = {}
+    for scalar in (False, True):
+        ws = engine.Workspace("cuda", "fp32")
+        ws.raster_scalar = scalar
+        fr = engine.render_frame(ws, ds, cam, q, full_lists=True)
+        cnt = fr.n_contrib.cpu().numpy()
+        assert np.array_equal(cnt, ref["count"]), scalar
+        assert np.array_equal(fr.hit_clamp.cpu().numpy().astype(bool), ref["alpha_clamped"])
+        assert float(np.abs(fr.image.double().cpu().numpy() - ref["image"]).max()) <= 1e-4
+        g_img = torch.full_like(fr.image, 1e-3)
+        grad = torch.zeros(ds.params.shape, dtype=torch.float64, device="cuda")
+        gb = engine.backward_raster(fr, ds, g_img, grad, pixels_per_lane=4)
+        engine.backward_chain(fr, gb)
+        outs[scalar] = grad
+    a, b = outs[False], outs[True]
+    assert float((a - b).norm()) <= 1e-4 * float(b.norm())
