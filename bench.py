@@ -278,8 +278,13 @@ def run_train(a, rank, world, local_rank):
         targets.append(engine.render_frame(tws, tds, c, q).image.clone().clamp_(0.0, 1.0))
     del tws, tds
     views = list(zip(cams, views_q, targets))
-    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=a.train_inflight,
-                                                            group=a.train_group, pixels_per_lane=a.train_ppl))
+    # more views than slots: two groups' worth of slots, so one group's shared
+    # preprocess and views overlap the previous group's (with one group's worth
+    # the groups of a batch run back to back)
+    depth = a.train_inflight if a.train_views_per_gpu <= a.train_inflight else \
+        min(a.train_views_per_gpu, 2 * a.train_group)
+    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=depth, group=a.train_group,
+                                                            pixels_per_lane=a.train_ppl))
     adam = sharding.DeviceAdam(ds.params, 7)
     cfg = LossConfig()
     grad = step.backend.new_grad()
@@ -303,7 +308,7 @@ def run_train(a, rank, world, local_rank):
     return {"metric": "train iters/sec", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
             "views_per_s": batch * 1e3 / ms, "loss": float(loss),
             "config": {"workload": f"config 5: 7D UBS training step, {a.train_prims} primitives, batch {batch} "
-                                   f"1920x1080 orbit views ({a.train_views_per_gpu} per GPU, {a.train_inflight} in "
+                                   f"1920x1080 orbit views ({a.train_views_per_gpu} per GPU, {depth} in "
                                    f"flight, groups of {a.train_group} sharing one preprocess), "
                                    f"fwd + L1/SSIM + bwd + all-reduce + Adam",
                        "parallelism": f"dp{world} (view sharding, NCCL "

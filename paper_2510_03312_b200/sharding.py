@@ -234,6 +234,29 @@ class GpuViewBackend:
         for ws in self.workspaces:
             ws.status.zero_()
 
+    def grow(self) -> int:
+        """After an asynchronous view outgrew its slot: give every slot the
+        largest tile-list cap any slot has (doubled if a list was truncated)
+        and pair buffers for the largest tile-pair count any slot saw, then
+        clear the status (a batch's views rotate over the slots, so growing
+        only the slot that overflowed is not enough).  Syncs."""
+        torch.cuda.current_stream().synchronize()
+        st = 0
+        for ws in self.workspaces:
+            st |= int(ws.status.item())
+        cap = max(ws.list_cap for ws in self.workspaces)
+        if st & _lib.S_LIST_TRUNC:
+            cap *= 2
+        k = max(int(ws.counters[0].item()) for ws in self.workspaces)
+        if st & _lib.S_PAIR_OVERFLOW:
+            k = max(k, int(max(ws.pair_cap for ws in self.workspaces) * 1.3) + 1)
+        for ws in self.workspaces:
+            ws.list_cap = cap
+            if ws.temp_bytes:
+                ws.ensure_pairs(k)
+            ws.status.zero_()
+        return st
+
     def add_regularisers(self, grad: torch.Tensor, cfg: LossConfig):
         lib = _lib.load()
         p = self.ds.params
@@ -279,8 +302,10 @@ class ViewShardedStep:
         b = self.backend
         scale = cfg.loss_scale / len(views)
         multi = world > 1 and dist.is_available() and dist.is_initialized()
-        for attempt in range(2):
-            sync = attempt > 0  # retry with synchronous frames if a view outgrew the pair buffers
+        for attempt in range(3):
+            # a view that outgrew its slot's buffers: grow every slot and retry
+            # asynchronously, then (rarely) once more with synchronous frames
+            sync = attempt > 1
             grad = b.new_grad() if grad is None else grad.zero_()
             if rank == 0:
                 b.add_regularisers(grad, cfg)
@@ -309,7 +334,10 @@ class ViewShardedStep:
             if float(rec[1]) == 0.0:
                 break
             self.retries += 1
-            b.clear_status()
+            if hasattr(b, "grow"):
+                b.grow()
+            else:
+                b.clear_status()
         loss = cfg.loss_scale * (rec[0] / len(views) + b.regulariser_value(cfg))
         return loss, grad
 
