@@ -57,6 +57,42 @@ class OracleBackend:
         return cfg.lambda_o * o.sum() + cfg.lambda_sigma * (np.exp(sc.s_x_raw).sum() + np.exp(sc.s_q_raw).sum())
 
 
+class BatchedOracleBackend(OracleBackend):
+    """The batched backend's contract (``sharding.GpuViewBackend``): views
+    queued with ``begin`` / ``view``, the gradient finished in ``end``, which
+    hands row ranges to the bucket hook as they become final; ``status`` /
+    ``grow`` flag a first attempt as overflowed so the retry path runs."""
+
+    def __init__(self, scene, overflow_first=False):
+        super().__init__(scene)
+        self.pending, self.hooked, self.flag, self.grown = [], [], int(overflow_first), 0
+
+    def begin(self, grad):
+        self.grad, self.pending = grad, []
+
+    def view(self, cam, q, target, cfg, scale, sync=False):
+        self.pending.append((cam, q, target, cfg, scale))
+
+    def end(self, bucket_hook=None, buckets=4):
+        loss = torch.zeros((), dtype=torch.float64)
+        for cam, q, target, cfg, scale in self.pending:
+            loss += self.view_loss_grad(cam, q, target, cfg, scale, self.grad)
+        n = self.scene.n_primitives
+        step = -(-n // buckets)
+        if bucket_hook is not None:
+            for r0 in range(0, n, step):
+                self.hooked.append((r0, min(n, r0 + step)))
+                bucket_hook(r0, min(n, r0 + step))
+        return loss
+
+    def status(self):
+        return torch.tensor([self.flag], dtype=torch.int32)
+
+    def grow(self):
+        self.flag, self.grown = 0, self.grown + 1
+        return 1
+
+
 def _setup():
     sc = quantize_f32(S.random_scene(6, 30, seed=12))
     views = []
@@ -69,14 +105,23 @@ def _setup():
     return sc, views
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, batched=False):
     os.environ["OMP_NUM_THREADS"] = "1"
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     sc, views = _setup()
-    step = sharding.ViewShardedStep(OracleBackend(sc))
+    # batched: rank 1 reports an overflow on its first attempt, so both ranks
+    # must take the retry together (the flag is all-reduced)
+    be = BatchedOracleBackend(sc, overflow_first=rank == 1) if batched else OracleBackend(sc)
+    step = sharding.ViewShardedStep(be)
     cfg = LossConfig(lambda_ssim=0.3, loss_scale=1.5)
-    loss, grad = step.loss_and_grad(views, cfg)
+    loss, grad = step.loss_and_grad(views, cfg, buckets=3)
     assert len(sharding.shard(views, rank, world)) == (3 if rank == 0 else 2)
+    if batched:
+        n = sc.n_primitives
+        assert step.retries == 1
+        assert be.grown == 1
+        # two attempts, each covering every row once in 3 buckets
+        assert be.hooked == [(0, 10), (10, 20), (20, n)] * 2
     if rank == 0:
         np.savez(out_path, loss=float(loss), grad=grad.numpy())
     dist.barrier()
@@ -96,9 +141,10 @@ def test_shard_round_robin():
     assert sum(len(sharding.shard(range(10), r, 4)) for r in range(4)) == 10
 
 
-def test_two_rank_gloo_matches_single_process():
+@pytest.mark.parametrize("batched", [False, True])
+def test_two_rank_gloo_matches_single_process(batched):
     out = os.path.join(tempfile.mkdtemp(), "dp.npz")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, batched), nprocs=2, join=True)
     got = np.load(out)
     sc, views = _setup()
     frames = [(c, q, t.numpy()) for c, q, t in views]
