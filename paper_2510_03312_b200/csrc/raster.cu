@@ -806,6 +806,14 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
     if (threadIdx.x == 0 && tot) atomicAdd(visits, tot);
 }
 
+#ifndef UBS_FIX_THREADS
+#define UBS_FIX_THREADS 128
+#endif
+#ifndef UBS_FIX_CTAS_PER_SM
+#define UBS_FIX_CTAS_PER_SM 4
+#endif
+constexpr int kFixThreads = UBS_FIX_THREADS;  // fix-up CTA size; grid = 148 x UBS_FIX_CTAS_PER_SM
+
 // fp64 replay of flagged pixels: one warp per pixel, chunks of 32 splats.
 //  1. lanes evaluate alpha_k (reference formula and rounding, clamp applied)
 //     and 1 - alpha_k in parallel;
@@ -816,13 +824,13 @@ raster_fwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
 //  3. lanes accumulate w_k = alpha_k T_k times colour in per-lane sums, reduced
 //     once per pixel (summation order differs from the reference only at the
 //     1e-16 level; T, the contributor count and the clamp flags are exact).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kFixThreads)
 raster_fixup_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                     const Rec64 *__restrict__ recs, const uint32_t *__restrict__ fix_list,
                     const uint32_t *__restrict__ fix_count, float *__restrict__ image, float *__restrict__ asum,
                     float *__restrict__ tstop, int32_t *__restrict__ ncontrib, uint8_t *__restrict__ hit,
                     unsigned long long *__restrict__ visits) {
-    __shared__ double s_om[8][32], s_T[8][33];
+    __shared__ double s_om[kFixThreads / 32][32], s_T[kFixThreads / 32][33];
     if (pairs_overflow(P.n_pairs, P.pair_capacity, nullptr)) return;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const uint32_t nfix = *fix_count;
@@ -1693,7 +1701,7 @@ extern "C" int ubs_raster_fixup(const UbsView *v, const UbsPrimBuffers *pb, cons
     // one pass over the device-counted list, grid-stride over ~4 warps per SM:
     // the fix-up's cost is its tail, so it keeps a small footprint beside the
     // other frames' rasters (148 x 128 threads: 2008 vs 1997 fps for 592 x 256)
-    raster_fixup_kernel<<<148, 128, 0, (cudaStream_t)stream>>>(
+    raster_fixup_kernel<<<148 * UBS_FIX_CTAS_PER_SM, kFixThreads, 0, (cudaStream_t)stream>>>(
         P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, ib->fix_list, ib->fix_count, (float *)ib->image,
         (float *)ib->alpha_sum, (float *)ib->t_stop, ib->n_contrib, ib->hit_clamp, ib->visits);
     UBS_CUDA_CHECK();
