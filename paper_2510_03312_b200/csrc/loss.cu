@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include "ubs_common.cuh"
+#include "f32x2.cuh"
 
 namespace ubs {
 
@@ -538,6 +539,359 @@ ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *
     }
 }
 
+// ---------------------------------------------------------------------------
+// fp32 tiled path on packed pairs (sm_100 FFMA2): the tiles, passes, taps and
+// per-element operation order of ssim_fwd_tile_kernel / ssim_adj_tile_kernel
+// -- so the same bits -- with (a, b), (a^2, b^2), (mu_a, mu_b), (E[a^2], E[b^2])
+// and the adjoint's (g_mu_a, g_E[a^2]) carried as f32x2 pairs: one FFMA2 per
+// tap for two of the blurred quantities, 64-bit shared loads and stores.  The
+// halo loads walk rows with one warp per row, the per-lane source columns
+// computed once (no per-element division).
+__device__ __forceinline__ void ssim_col_sources(int x0col, int lane, int W, int (&colq)[4]) {
+    // float column lane + 32 j of the forward halo (pixel x0 - 5 + hc / 3): its
+    // reflected source column, or -1 past W + 4 (those feed no output)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int hc = lane + 32 * j, hp = hc / 3, c = hc - 3 * hp;
+        const int px = x0col - kSsimR + hp;
+        colq[j] = (hc < kSsimHaloCols && px < W + kSsimR) ? reflect_near(px, W) * 3 + c : -1;
+    }
+}
+
+__global__ void __launch_bounds__(kSsimThreads)
+ssim_fwd_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, int H, int W, BlurTaps w,
+                   float *__restrict__ g3, double *__restrict__ sums) {
+    extern __shared__ __align__(16) unsigned char ssim_smem[];
+    f32x2(*sab)[kSsimHaloCols] = reinterpret_cast<f32x2(*)[kSsimHaloCols]>(ssim_smem);  // (a, b)
+    f32x2(*hab)[kSsimCols] = reinterpret_cast<f32x2(*)[kSsimCols]>(sab + kSsimHaloRows);  // (mu_a, mu_b) rows
+    f32x2(*hsq)[kSsimCols] = hab + kSsimHaloRows;                                          // (E[a^2], E[b^2])
+    float(*hxy)[kSsimCols] = reinterpret_cast<float(*)[kSsimCols]>(hsq + kSsimHaloRows);   // E[ab]
+    const int x0 = blockIdx.x * kSsimTW, y0 = blockIdx.y * kSsimTH;
+    const int64_t rs = (int64_t)W * 3;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float k[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) k[t] = (float)w.k[t];
+    int colq[4];
+    ssim_col_sources(x0, lane, W, colq);
+#pragma unroll 2
+    for (int yy = warp; yy < kSsimHaloRows; yy += kSsimThreads / 32) {
+        const int py = y0 - kSsimR + yy;
+        const bool rowok = py < H + kSsimR;
+        const int64_t rq = rowok ? (int64_t)reflect_near(py, H) * rs : 0;
+        float av[4], bv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            av[j] = 0.0f;
+            bv[j] = 0.0f;
+            if (rowok && colq[j] >= 0) {
+                av[j] = a[rq + colq[j]];
+                bv[j] = b[rq + colq[j]];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (lane + 32 * j < kSsimHaloCols) sab[yy][lane + 32 * j] = pk2(av[j], bv[j]);
+    }
+    __syncthreads();
+    // horizontal blur: item = (halo row, run of kSsimHPx pixels, channel)
+    constexpr int kRuns = kSsimTW / kSsimHPx;
+    for (int it = threadIdx.x; it < kSsimHaloRows * kRuns * 3; it += kSsimThreads) {
+        const int yy = it / (kRuns * 3), rem = it - yy * (kRuns * 3);
+        const int g = rem / 3, c = rem - 3 * g;
+        const int p0 = g * kSsimHPx;
+        if (x0 + p0 >= W) continue;
+        f32x2 aab[kSsimHPx], asq[kSsimHPx];
+        float axy[kSsimHPx];
+#pragma unroll
+        for (int o = 0; o < kSsimHPx; ++o) {
+            aab[o] = 0ull;
+            asq[o] = 0ull;
+            axy[o] = 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < kSsimHPx + 10; ++i) {
+            const f32x2 sv = sab[yy][(p0 + i) * 3 + c];
+            const f32x2 sq = mul2(sv, sv);  // (a a, b b)
+            const float2 s2 = up2(sv);
+            const float xy = s2.x * s2.y;
+#pragma unroll
+            for (int o = 0; o < kSsimHPx; ++o) {
+                const int t = i - o;
+                if (t >= 0 && t <= 10) {
+                    aab[o] = fma2(dup2(k[t]), sv, aab[o]);
+                    asq[o] = fma2(dup2(k[t]), sq, asq[o]);
+                    axy[o] = fmaf(k[t], xy, axy[o]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < kSsimHPx; ++o) {
+            const int col = (p0 + o) * 3 + c;
+            hab[yy][col] = aab[o];
+            hsq[yy][col] = asq[o];
+            hxy[yy][col] = axy[o];
+        }
+    }
+    __syncthreads();
+    // vertical blur + SSIM: item = (column, run of kSsimVRows rows)
+    const int64_t N = (int64_t)H * W * 3;
+    const float g = (float)(1.0 / (double)N);
+    const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
+    double l1 = 0.0, sm = 0.0;
+    for (int it = threadIdx.x; it < kSsimCols * (kSsimTH / kSsimVRows); it += kSsimThreads) {
+        const int rg = it / kSsimCols, cc = it - rg * kSsimCols;
+        const int x = x0 + cc / 3, ty0 = rg * kSsimVRows;
+        if (x >= W || y0 + ty0 >= H) continue;
+        f32x2 vab[kSsimVRows], vsq[kSsimVRows];
+        float vxy[kSsimVRows];
+#pragma unroll
+        for (int o = 0; o < kSsimVRows; ++o) {
+            vab[o] = 0ull;
+            vsq[o] = 0ull;
+            vxy[o] = 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < kSsimVRows + 10; ++i) {
+            const f32x2 hv = hab[ty0 + i][cc], hq = hsq[ty0 + i][cc];
+            const float hx = hxy[ty0 + i][cc];
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                const int t = i - o;
+                if (t >= 0 && t <= 10) {
+                    vab[o] = fma2(dup2(k[t]), hv, vab[o]);
+                    vsq[o] = fma2(dup2(k[t]), hq, vsq[o]);
+                    vxy[o] = fmaf(k[t], hx, vxy[o]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < kSsimVRows; ++o) {
+            const int y = y0 + ty0 + o;
+            if (y >= H) break;
+            const float2 mu = up2(vab[o]), e2 = up2(vsq[o]);
+            const float mu_a = mu.x, mu_b = mu.y;
+            const float va = e2.x - mu_a * mu_a, vb = e2.y - mu_b * mu_b, cab = vxy[o] - mu_a * mu_b;
+            const float n1 = 2.0f * mu_a * mu_b + C1, n2 = 2.0f * cab + C2;
+            const float d1 = mu_a * mu_a + mu_b * mu_b + C1, d2 = va + vb + C2;
+            const float den = d1 * d2;
+            const float inv = 1.0f / den;
+            const float sv = n1 * n2 * inv;
+            const float g_n1 = g * n2 * inv, g_n2 = g * n1 * inv;
+            const float g_den = -g * sv * inv;
+            const float g_d1 = g_den * d2, g_d2 = g_den * d1;
+            const float g_cab = 2.0f * g_n2;
+            const float g_mu_a = 2.0f * mu_b * g_n1 + 2.0f * mu_a * g_d1 - 2.0f * mu_a * g_d2 - mu_b * g_cab;
+            const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
+            g3[idx] = g_mu_a;
+            g3[N + idx] = g_d2;       // g_E[a^2]
+            g3[2 * N + idx] = g_cab;  // g_E[ab]
+            sm += (double)sv;
+            const float2 ab = up2(sab[ty0 + o + kSsimR][cc + 3 * kSsimR]);
+            l1 += fabs((double)ab.x - (double)ab.y);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    __shared__ double red[2][kSsimThreads / 32];
+    if (lane == 0) {
+        red[0][warp] = l1;
+        red[1][warp] = sm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int q = 0; q < kSsimThreads / 32; ++q) {
+            t0 += red[0][q];
+            t1 += red[1][q];
+        }
+        const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        sums[2 * bid] = t0;
+        sums[2 * bid + 1] = t1;
+    }
+}
+
+__global__ void __launch_bounds__(kSsimThreads)
+ssim_adj_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, const float *__restrict__ g3, int H,
+                   int W, BlurTaps w, double lambda_ssim, double scale, float *__restrict__ g_image) {
+    extern __shared__ __align__(16) unsigned char ssim_smem[];
+    f32x2(*gs01)[kSsimHaloCols] = reinterpret_cast<f32x2(*)[kSsimHaloCols]>(ssim_smem);        // (g_mu_a, g_E[a^2])
+    float(*gs2)[kSsimHaloCols] = reinterpret_cast<float(*)[kSsimHaloCols]>(gs01 + kSsimHaloRows);  // g_E[ab]
+    f32x2(*vs01)[kSsimHaloCols] = reinterpret_cast<f32x2(*)[kSsimHaloCols]>(gs2 + kSsimHaloRows);
+    float(*vs2)[kSsimHaloCols] = reinterpret_cast<float(*)[kSsimHaloCols]>(vs01 + kSsimTH);
+    const int x0 = blockIdx.x * kSsimTW, y0 = blockIdx.y * kSsimTH;
+    const int64_t rs = (int64_t)W * 3, N = (int64_t)H * W * 3;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float sk[11];  // the taps, for the border folds' dynamic indexing
+    float k[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) k[t] = (float)w.k[t];
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int t = 0; t < 11; ++t) sk[t] = k[t];
+    // g3 over rows y0-5 .. y0+TH+5 and float columns (x0-5)*3 .. (x0+TW+5)*3, zero outside
+#pragma unroll 2
+    for (int yy = warp; yy < kSsimHaloRows; yy += kSsimThreads / 32) {
+        const int y = y0 - kSsimR + yy;
+        const bool rowok = y >= 0 && y < H;
+        float v0[4], v1[4], v2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int hc = lane + 32 * j, xf = x0 * 3 - 3 * kSsimR + hc;
+            v0[j] = 0.0f;
+            v1[j] = 0.0f;
+            v2[j] = 0.0f;
+            if (rowok && hc < kSsimHaloCols && xf >= 0 && xf < W * 3) {
+                const int64_t q = (int64_t)y * rs + xf;
+                v0[j] = g3[q];
+                v1[j] = g3[N + q];
+                v2[j] = g3[2 * N + q];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int hc = lane + 32 * j;
+            if (hc < kSsimHaloCols) {
+                gs01[yy][hc] = pk2(v0[j], v1[j]);
+                gs2[yy][hc] = v2[j];
+            }
+        }
+    }
+    __syncthreads();
+    // vertical transpose blur: item = (halo column, run of kSsimVRows rows)
+    for (int it = threadIdx.x; it < kSsimHaloCols * (kSsimTH / kSsimVRows); it += kSsimThreads) {
+        const int rg = it / kSsimHaloCols, hc = it - rg * kSsimHaloCols;
+        const int ty0 = rg * kSsimVRows, yb = y0 + ty0;
+        if (yb >= 6 && yb + kSsimVRows - 1 + 7 < H) {
+            f32x2 acc01[kSsimVRows];
+            float acc2[kSsimVRows];
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                acc01[o] = 0ull;
+                acc2[o] = 0.0f;
+            }
+            // output row ty0 + o takes source halo row ty0 + i with tap t = 10 - (i - o);
+            // descending i walks every output's taps in ascending order
+#pragma unroll
+            for (int i = kSsimVRows + 9; i >= 0; --i) {
+                const f32x2 s01 = gs01[ty0 + i][hc];
+                const float s2 = gs2[ty0 + i][hc];
+#pragma unroll
+                for (int o = 0; o < kSsimVRows; ++o) {
+                    const int t = 10 - (i - o);
+                    if (t >= 0 && t <= 10) {
+                        acc01[o] = fma2(dup2(k[t]), s01, acc01[o]);
+                        acc2[o] = fmaf(k[t], s2, acc2[o]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                vs01[ty0 + o][hc] = acc01[o];
+                vs2[ty0 + o][hc] = acc2[o];
+            }
+        } else {
+            for (int o = 0; o < kSsimVRows; ++o) {  // border rows: folded reflected taps
+                const int y = yb + o;
+                float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+                if (y < H) {
+                    for (int d = -kSsimR; d <= kSsimR; ++d) {
+                        const int r = y + d;
+                        if (r < 0 || r >= H) continue;
+                        const float kw = fold_weight<float>(sk, y, r, H);
+                        const int yy = ty0 + o + kSsimR + d;
+                        const float2 g01 = up2(gs01[yy][hc]);
+                        s0 += kw * g01.x;
+                        s1 += kw * g01.y;
+                        s2 += kw * gs2[yy][hc];
+                    }
+                }
+                vs01[ty0 + o][hc] = pk2(s0, s1);
+                vs2[ty0 + o][hc] = s2;
+            }
+        }
+    }
+    __syncthreads();
+    // horizontal transpose blur: item = (row, run of kSsimVRows pixels, channel);
+    // the sums go to shared memory over the (dead) g3 halo for the coalesced combine
+    float(*adj)[kSsimTH][kSsimCols] = reinterpret_cast<float(*)[kSsimTH][kSsimCols]>(ssim_smem);
+    static_assert(3 * kSsimTH * kSsimCols * 4 <= 12 * kSsimHaloRows * kSsimHaloCols, "adj fits over gs");
+    constexpr int kRuns = kSsimTW / kSsimVRows;
+    for (int it = threadIdx.x; it < kSsimTH * kRuns * 3; it += kSsimThreads) {
+        const int ty = it / (kRuns * 3), rem = it - ty * (kRuns * 3);
+        const int g = rem / 3, c = rem - 3 * g;
+        const int p0 = g * kSsimVRows, xb = x0 + p0, y = y0 + ty;
+        if (y >= H || xb >= W) continue;
+        f32x2 h01[kSsimVRows];
+        float h2[kSsimVRows];
+        if (xb >= 6 && xb + kSsimVRows - 1 + 7 < W) {
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {
+                h01[o] = 0ull;
+                h2[o] = 0.0f;
+            }
+            // output pixel p0 + o takes halo pixel p0 + i with tap t = 10 - (i - o)
+#pragma unroll
+            for (int i = kSsimVRows + 9; i >= 0; --i) {
+                const int hc = (p0 + i) * 3 + c;
+                const f32x2 s01 = vs01[ty][hc];
+                const float s2 = vs2[ty][hc];
+#pragma unroll
+                for (int o = 0; o < kSsimVRows; ++o) {
+                    const int t = 10 - (i - o);
+                    if (t >= 0 && t <= 10) {
+                        h01[o] = fma2(dup2(k[t]), s01, h01[o]);
+                        h2[o] = fmaf(k[t], s2, h2[o]);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int o = 0; o < kSsimVRows; ++o) {  // border columns: folded reflected taps
+                const int x = xb + o;
+                float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+                if (x < W) {
+                    for (int d = -kSsimR; d <= kSsimR; ++d) {
+                        const int r = x + d;
+                        if (r < 0 || r >= W) continue;
+                        const float kw = fold_weight<float>(sk, x, r, W);
+                        const int hc = (p0 + o + kSsimR + d) * 3 + c;
+                        const float2 g01 = up2(vs01[ty][hc]);
+                        s0 += kw * g01.x;
+                        s1 += kw * g01.y;
+                        s2 += kw * vs2[ty][hc];
+                    }
+                }
+                h01[o] = pk2(s0, s1);
+                h2[o] = s2;
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < kSsimVRows; ++o) {
+            const float2 hv = up2(h01[o]);
+            adj[0][ty][p0 * 3 + c + 3 * o] = hv.x;
+            adj[1][ty][p0 * 3 + c + 3 * o] = hv.y;
+            adj[2][ty][p0 * 3 + c + 3 * o] = h2[o];
+        }
+    }
+    __syncthreads();
+    // combine (gradients.py:110-116), coalesced over the tile's rows
+    const float w_l1 = (float)(1.0 - lambda_ssim) / (float)N, w_ssim = (float)lambda_ssim, sc = (float)scale;
+    for (int e = threadIdx.x; e < kSsimTH * kSsimCols; e += kSsimThreads) {
+        const int ty = e / kSsimCols, cc = e - ty * kSsimCols;
+        const int y = y0 + ty, x = x0 + cc / 3;
+        if (y >= H || x >= W) continue;
+        const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
+        const float av = a[idx], bv = b[idx];
+        const float gsum = adj[0][ty][cc] + adj[1][ty][cc] * 2.0f * av + adj[2][ty][cc] * bv;
+        const float diff = av - bv;
+        const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+        g_image[idx] = sc * (w_l1 * sgn - w_ssim * gsum);
+    }
+}
+
 // The loss terms' per-block partials summed in block order by one CTA (a
 // fixed summation order: the loss value is bitwise reproducible, unlike
 // float atomics in arrival order), then added to the caller's sums.
@@ -598,6 +952,17 @@ static void run_loss(const T *a, const T *b, int H, int W, double lam, double sc
         const size_t adj_smem = sizeof(T) * 3 * (kSsimHaloRows + kSsimTH) * kSsimHaloCols;
         cudaFuncSetAttribute(ssim_fwd_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
         cudaFuncSetAttribute(ssim_adj_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem);
+        if constexpr (sizeof(T) == 4) {
+#ifndef UBS_SSIM_SCALAR
+            // packed pairs: the same smem footprint and bits as the scalar tiles
+            cudaFuncSetAttribute(ssim_fwd_x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
+            cudaFuncSetAttribute(ssim_adj_x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem);
+            ssim_fwd_x2_kernel<<<grid, kSsimThreads, fwd_smem, s>>>(a, b, H, W, w, g3, part);
+            loss_sums_kernel<<<1, 256, 0, s>>>(part, (int64_t)grid.x * grid.y, sums);
+            ssim_adj_x2_kernel<<<grid, kSsimThreads, adj_smem, s>>>(a, b, g3, H, W, w, lam, scale, g);
+            return;
+#endif
+        }
         ssim_fwd_tile_kernel<T><<<grid, kSsimThreads, fwd_smem, s>>>(a, b, H, W, w, g3, part);
         loss_sums_kernel<<<1, 256, 0, s>>>(part, (int64_t)grid.x * grid.y, sums);
         ssim_adj_tile_kernel<T><<<grid, kSsimThreads, adj_smem, s>>>(a, b, g3, H, W, w, lam, scale, g);
