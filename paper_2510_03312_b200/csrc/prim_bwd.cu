@@ -102,8 +102,11 @@ prim_active_kernel(const GT *__restrict__ grad2d, const uint16_t *__restrict__ f
     if (need) active[cta_base + wcnt[wid] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
+#ifndef UBS_PRIM_BWD_MIN_CTAS
+#define UBS_PRIM_BWD_MIN_CTAS 1
+#endif
 template <int C, typename PT, typename GT, typename OT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, UBS_PRIM_BWD_MIN_CTAS)
 prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, int add_reg,
                 double reg_o, double reg_s, uint32_t *__restrict__ nonfinite, const uint32_t *__restrict__ active,
                 const uint32_t *__restrict__ active_count) {

@@ -156,6 +156,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// An upper bound of 1 / x for normal x > 0, at most 12.5% above it, from one
+// integer subtract (ALU pipe) instead of a MUFU.RCP: for x = 2^e (1 + f),
+// 0x7F000000 - bits(x) is the float 2^(-e-1) (2 - f) (2^-e when f = 0), and
+// x times it is (1 + f)(2 - f) / 2 in [1, 1.125].  Always finite (so 0 times
+// it is 0, never NaN); for a subnormal x it is ~2^127 and no longer a bound,
+// but there x sits within 1e-38 of the support edge and any error bound
+// scaled by it is far above every certification threshold anyway.
+__device__ __forceinline__ float rcp_upper(float x) {
+    return __int_as_float(0x7F000000 - __float_as_int(x));
+}
 
 // Warp cover mask of one splat over a 16x16 tile whose warps are 8x4 pixel
 // blocks (warp w covers columns 8 (w & 1) .. +7, rows 4 (w >> 1) .. +3).
@@ -213,7 +223,8 @@ __device__ __forceinline__ uint32_t warp_cover_mask(const float4 r0, const float
 // Per visit (in support): alpha = 2^(beta * lg2(1 - m/tau) + log2(og)) with
 // the MUFU lg2/ex2 approximations; their error (qc, and 2.1e-7 per unit of
 // the exponent) is part of the per-visit relative alpha bound
-//     q = eb / (tau - m) + qc + 2.1e-7 |arg|,
+//     q = eb / (tau - m) + qc + 2.1e-7 |arg|
+// (1 / (tau - m) taken as rcp_upper's bound, at most 12.5% above it),
 // and D, the bound on |T32 - T64|, accumulates D (1 - a) + T a q + 2u T: the
 // first-order error of T (D / T = sum a q / (1 - a) + 2u per visit).
 // T and D change only on in-support visits, so the reference's cut test
@@ -317,7 +328,7 @@ raster_fwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     const float arg = fmaf(r2.x, lg2_approx(fmaf(-m, inv_tau, 1.0f)), r3.w);
                     float a = ex2_approx(arg);
                     // relative alpha bound q = eb / (tau - m) + qc + 2.1e-7 |arg|
-                    const float qrel = fmaf(r3.x, rcp_approx(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
+                    const float qrel = fmaf(r3.x, rcp_upper(tau - m), fmaf(fabsf(arg), 2.1e-7f, r3.z));
                     float om = 1.0f - a;
                     // T (1 - a) as T - a T: rounds a T and the difference (<= u T in
                     // all, inside the 2u T rounding term of D), and keeps T's register
@@ -525,7 +536,7 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     // beta lg2(1 - x) + log2(og) <= 0 up to the lg2 approximation's
                     // 2^-22 near 1, whose 1e-13 effect hides in qc's 4e-7 term)
                     const float2 tmv = up2(tm);
-                    const float2 qr = up2(fma2(dup2(r3.x), pk2(rcp_approx(tmv.x), rcp_approx(tmv.y)),
+                    const float2 qr = up2(fma2(dup2(r3.x), pk2(rcp_upper(tmv.x), rcp_upper(tmv.y)),
                                                fma2(arg, dup2(-2.1e-7f), dup2(r3.z))));
                     // zero for a pixel not in support: its w = 0, and q may be +-inf
                     // (m == tau, or eb = inf for a thin splat) where 0 q would be NaN
