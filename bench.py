@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-inflight", type=int, default=8, help="views in flight per GPU in the training step")
     ap.add_argument("--train-group", type=int, default=8, help="training views per shared preprocess")
+    ap.add_argument("--train-first-group", type=int, default=0,
+                    help="views in a batch's first preprocess group (0: --train-group)")
     ap.add_argument("--train-ppl", type=int, default=4, choices=[2, 4, 8],
                     help="raster backward pixels per lane in the training step")
     ap.add_argument("--train-only", action="store_true",
@@ -284,7 +286,8 @@ def run_train(a, rank, world, local_rank):
     depth = a.train_inflight if a.train_views_per_gpu <= a.train_inflight else \
         min(a.train_views_per_gpu, 2 * a.train_group)
     step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, "fp32", depth=depth, group=a.train_group,
-                                                            pixels_per_lane=a.train_ppl))
+                                                            pixels_per_lane=a.train_ppl,
+                                                            first_group=a.train_first_group or None))
     adam = sharding.DeviceAdam(ds.params, 7)
     cfg = LossConfig()
     grad = step.backend.new_grad()

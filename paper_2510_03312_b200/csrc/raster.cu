@@ -23,6 +23,8 @@
 //    stay bit-exact while 99+% of pixels take the fp32 path.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <cub/device/device_scan.cuh>
 
 #include "ubs_common.cuh"
@@ -54,6 +56,10 @@ struct RasterParams {
     int W, H, TX;
     double tau, clamp, tmin;
     double bg[3];
+    // the fp32 kernels' constants, rounded once on the host exactly as the
+    // kernels' own casts would (kernel-parameter operands: a register-starved
+    // kernel re-reads them for free instead of re-converting a double)
+    float tau_f, inv_tau_f, clamp_f, omc_f, tmin_f;
     const unsigned long long *n_pairs;  // device K, checked against pair_capacity
     int64_t pair_capacity;
     uint32_t list_cap;                  // per-tile list cap (binning materialised only this prefix)
@@ -82,6 +88,11 @@ static RasterParams make_params(const UbsView &v, const UbsPrimBuffers &pb, cons
     p.tau = v.set.tau_sq;
     p.clamp = v.set.alpha_clamp;
     p.tmin = v.set.transmittance_min;
+    p.tau_f = (float)p.tau;
+    p.inv_tau_f = (float)(1.0 / p.tau);
+    p.clamp_f = (float)p.clamp;
+    p.omc_f = (float)(1.0 - p.clamp);
+    p.tmin_f = (float)p.tmin;
     for (int k = 0; k < 3; ++k) p.bg[k] = v.background[k];
     return p;
 }
@@ -986,6 +997,37 @@ __device__ __forceinline__ bool warp_reduce10(T (&v)[16], int lane, int &idx, T 
     return false;
 }
 
+// warp_reduce10 without the per-call reporter bookkeeping, for a kernel that
+// keeps its lane's component index (reduce10_index, -1: no component) in a
+// register: lanes l % 4 == 0 return component reduce10_index(l), lanes 1 and
+// 17 components 8 and 9 (the same sums and summation order).
+template <typename T>
+__device__ __forceinline__ T warp_reduce10_value(T (&v)[16], int lane) {
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+        const int half = 4 >> lvl, off = 16 >> lvl;
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const T send = upper ? v[i] : v[i + half];
+            const T keep = upper ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    T r = v[0];
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    const bool up = (lane & 16) != 0;
+    T c = (up ? v[9] : v[8]) + __shfl_xor_sync(0xffffffffu, up ? v[8] : v[9], 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    return (lane & 3) == 0 ? r : c;
+}
+__device__ __forceinline__ int reduce10_index(int lane) {
+    if ((lane & 3) == 0) return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    return lane == 1 ? 8 : (lane == 17 ? 9 : -1);
+}
+
 // fp64 backward (tile_backward, _tiles.py:59-127) in the reference's operation order
 __global__ void __launch_bounds__(kTileThreads)
 raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
@@ -1424,8 +1466,15 @@ __global__ void det_reduce_kernel(const uint32_t *__restrict__ slot_off, const u
 // accumulated as pairs and folded once before the warp reduction, so they
 // differ from the scalar kernel's only in float summation order.  A pair with
 // a pixel in the clamp band takes the scalar bwd_visit (rare).
+// 11 CTAs per SM = 80 registers for the four-pixel layout: at the 64 of 16 CTAs
+// the kernel spilled its cover words and counts and re-derived its constants
+// every visit (323 -> 261 instructions per visited splat; 7D 3M 1080p view
+// 0.99 -> 0.77 ms, training step 48 -> 54 it/s)
+#ifndef UBS_BWD4_MIN_CTAS
+#define UBS_BWD4_MIN_CTAS 11
+#endif
 template <int NP>
-__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 24 : 16)
+__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 24 : UBS_BWD4_MIN_CTAS)
 raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                       const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                       const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
@@ -1448,6 +1497,7 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int blk0 = (warp & 1) + 2 * NP * (warp >> 1);
+    const int ridx = reduce10_index(lane);  // this lane's reduced component (-1: none)
     const uint32_t start = ranges[2 * tile];
     float T[NP], S[NP], pyf[NP];  // S: the suffix sum of tile_backward (_tiles.py:97-127)
     int cnt[NP];
@@ -1489,8 +1539,8 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     if (lane == 0) atomicMax(&smax, warp_cnt);
     __syncthreads();
     const int max_cnt = smax;
-    const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
-    const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    const float tau = P.tau_f, inv_tau = P.inv_tau_f;
+    const float clamp = P.clamp_f, one_minus_clamp = P.omc_f;
     constexpr float kLn2 = 0.6931471805599453f;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
     for (int lo = ((max_cnt - 1) / kBatch) * kBatch; lo >= 0 && max_cnt > 0; lo -= kBatch) {
@@ -1538,22 +1588,26 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                 const uint32_t ra = sbase + (uint32_t)jj * (uint32_t)sizeof(Rec32);
                 const float2 r0 = lds64<0>(ra);  // tile offset (xa, ya)
                 const float4 r1 = lds128<16>(ra);
+                // Per-splat sums V of the lane's pixel pairs.  The first pair that
+                // has a pixel in support anywhere in the warp writes V, later pairs
+                // add to it: no per-visit zeroing.  In a writing pair, lanes with no
+                // pixel in support run the body on alpha = 0, which writes exact
+                // zeros and leaves T and S bit-for-bit unchanged (1 - 0 = 1, whose
+                // reciprocal is exactly 1); in an adding pair they skip.
                 f32x2 V[10];
-#pragma unroll
-                for (int c = 0; c < 10; ++c) V[c] = 0ull;
-                bool contrib = false;
-#pragma unroll
-                for (int p = 0; p < NQ; ++p) {
+                auto pair = [&](auto p_, auto init_) -> bool {
+                    constexpr int p = decltype(p_)::value;
+                    constexpr bool init = decltype(init_)::value;
                     const int h0 = 2 * p, h1 = 2 * p + 1;
                     const bool e0 = (wr[h0] & bm) && j < cnt[h0], e1 = (wr[h1] & bm) && j < cnt[h1];
-                    if (!(e0 || e1)) continue;
+                    if (init ? !__any_sync(0xffffffffu, e0 || e1) : !(e0 || e1)) return false;
                     const float dx = r0.x + (float)((blk_of(h0) & 1) * 8 + (lane & 7));  // the pair's column
                     const f32x2 dy = add2(dup2(r0.y), pk2(pyf[h0], pyf[h1]));
                     const f32x2 y0 = fma2(dup2(r1.x), dup2(dx), mul2(dup2(r1.y), dy));
                     const f32x2 y1 = mul2(dup2(r1.z), dy);
                     const float2 m = up2(fma2(y0, y0, mul2(y1, y1)));
                     const bool s0 = e0 && m.x < tau, s1 = e1 && m.y < tau;
-                    if (!(s0 || s1)) continue;
+                    if (init ? !__any_sync(0xffffffffu, s0 || s1) : !(s0 || s1)) return false;
                     const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
                     const float2 omx = up2(fma2(pk2(m.x, m.y), dup2(-inv_tau), dup2(1.0f)));
                     // pixels not in support take omx = 1: lg2 = 0, 1 / omx = 1 (finite), alpha = 0 below
@@ -1561,7 +1615,6 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     const f32x2 L = pk2(lg2_approx(ox0), lg2_approx(ox1));
                     const float2 ag = up2(fma2(dup2(r2.x), L, dup2(r3.w)));
                     float a0 = s0 ? ex2_approx(ag.x) : 0.0f, a1 = s1 ? ex2_approx(ag.y) : 0.0f;
-                    contrib |= (a0 != 0.0f) || (a1 != 0.0f);
                     float2 om = up2(sub2(dup2(1.0f), pk2(a0, a1)));
                     float am0 = a0, am1 = a1;  // alpha in the raw moments: 0 for a clamped pixel
                     if (a0 > clamp || a1 > clamp) {
@@ -1584,9 +1637,6 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     const f32x2 w = mul2(a2, ti);
                     const float4 gA = sgp[p][0][threadIdx.x], gB = sgp[p][1][threadIdx.x];
                     const f32x2 g0 = pk2(gA.x, gA.y), g1 = pk2(gA.z, gA.w), g2 = pk2(gB.x, gB.y);
-                    V[7] = fma2(w, g0, V[7]);
-                    V[8] = fma2(w, g1, V[8]);
-                    V[9] = fma2(w, g2, V[9]);
                     const f32x2 gc = fma2(g0, dup2(r2.y), fma2(g1, dup2(r2.z), mul2(g2, dup2(r2.w))));
                     const f32x2 Sp = pk2(S[h0], S[h1]);
                     // ga = gc T_i - suffix / (1 - a)  (fmaf(gc, ti, -suffix * iom) per pixel)
@@ -1599,28 +1649,54 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     T[h1] = Tn.y;
                     // raw moments (not clamped here); alpha = 0 pixels add exact zeros
                     const f32x2 gaa = mul2(ga, pk2(am0, am1));
-                    V[5] = add2(V[5], gaa);
-                    V[6] = fma2(gaa, mul2(L, dup2(kLn2)), V[6]);  // gaa ln(1 - x)
+                    const f32x2 gln = mul2(L, dup2(kLn2));  // ln(1 - x)
                     const f32x2 hh = mul2(gaa, pk2(rcp_approx(ox0), rcp_approx(ox1)));
                     const f32x2 hx = mul2(hh, dup2(dx)), hy = mul2(hh, dy);
-                    V[0] = add2(V[0], hx);
-                    V[1] = add2(V[1], hy);
-                    V[2] = fma2(hx, dup2(dx), V[2]);
-                    V[3] = fma2(hx, dy, V[3]);
-                    V[4] = fma2(hy, dy, V[4]);
-                }
-                if (__any_sync(0xffffffffu, contrib)) {
+                    if constexpr (init) {
+                        V[7] = mul2(w, g0);
+                        V[8] = mul2(w, g1);
+                        V[9] = mul2(w, g2);
+                        V[5] = gaa;
+                        V[6] = mul2(gaa, gln);
+                        V[0] = hx;
+                        V[1] = hy;
+                        V[2] = mul2(hx, dup2(dx));
+                        V[3] = mul2(hx, dy);
+                        V[4] = mul2(hy, dy);
+                    } else {
+                        V[7] = fma2(w, g0, V[7]);
+                        V[8] = fma2(w, g1, V[8]);
+                        V[9] = fma2(w, g2, V[9]);
+                        V[5] = add2(V[5], gaa);
+                        V[6] = fma2(gaa, gln, V[6]);
+                        V[0] = add2(V[0], hx);
+                        V[1] = add2(V[1], hy);
+                        V[2] = fma2(hx, dup2(dx), V[2]);
+                        V[3] = fma2(hx, dy, V[3]);
+                        V[4] = fma2(hy, dy, V[4]);
+                    }
+                    return true;
+                };
+                using I0 = std::integral_constant<int, 0>;
+                using I1 = std::integral_constant<int, 1>;
+                using Yes = std::integral_constant<bool, true>;
+                using No = std::integral_constant<bool, false>;
+                static_assert(NQ == 2, "two pixel pairs per lane");
+                // any_in: warp-uniform (the writing pair's vote), the reduction's gate
+                bool any_in = pair(I0{}, Yes{});
+                if (any_in) pair(I1{}, No{});
+                else any_in = pair(I1{}, Yes{});
+                if (any_in) {
                     float v[16];
 #pragma unroll
                     for (int c = 0; c < 10; ++c) {
                         const float2 t = up2(V[c]);
                         v[c] = t.x + t.y;
                     }
-                    int idx = 0;
-                    float mine = 0.0f;
-                    if (warp_reduce10(v, lane, idx, mine) && mine != 0.0f &&
-                        UBS_GUARD(jj >= 0 && jj < kBatch && idx >= 0 && idx < 10, kChkGrad))
-                        atomicAdd(grad2d + (int64_t)sid[jj] * kGrad2dStride + idx, mine);
+                    const float mine = warp_reduce10_value(v, lane);
+                    if (ridx >= 0 && mine != 0.0f &&
+                        UBS_GUARD(jj >= 0 && jj < kBatch && ridx < 10, kChkGrad))
+                        atomicAdd(grad2d + (int64_t)sid[jj] * kGrad2dStride + ridx, mine);
                 }
             }
         }

@@ -57,15 +57,20 @@ class GpuViewBackend:
     group).  Every view's per-primitive chain (``prim_bwd``) runs on one
     gradient stream in view order, adding straight into the batch gradient:
     the sum is formed in exactly the order of one-at-a-time accumulation, and
-    a slot is reused only after the gradient stream is done with it."""
+    a slot is reused only after the gradient stream is done with it.
+    ``first_group`` (default ``group``) sizes a batch's first group: a small
+    one starts the rasters early while the next group's preprocess runs
+    beside them."""
 
     def __init__(self, ds: engine.DeviceScene, precision: str = "fp32", settings=DEFAULT_SETTINGS,
-                 grad_dtype=torch.float32, depth: int = 1, group: int = 1, pixels_per_lane: int = 4):
+                 grad_dtype=torch.float32, depth: int = 1, group: int = 1, pixels_per_lane: int = 4,
+                 first_group: int | None = None):
         self.ds = ds
         self.settings = settings
         self.grad_dtype = grad_dtype
         self.depth = max(1, int(depth))
         self.group = max(1, min(int(group), self.depth))
+        self.first_group = self.group if first_group is None else max(1, min(int(first_group), self.depth))
         self.pixels_per_lane = int(pixels_per_lane)  # raster backward layout (UbsGradBuffers.bwd_pixels_per_lane)
         self.workspaces = [engine.Workspace(ds.device, precision) for _ in range(self.depth)]
         self.ws = self.workspaces[0]
@@ -117,7 +122,7 @@ class GpuViewBackend:
             self._rec[0] += self._view(self.ws, cam, query, target, cfg, scale, self._grad, sync)
             return
         self._queue.append((cam, query, target, cfg, scale, sync))
-        if len(self._queue) >= self.group or sync:
+        if len(self._queue) >= (self.first_group if self._k == 0 else self.group) or sync:
             self._flush()
 
     def _chain(self, rows=None, hook=None):
