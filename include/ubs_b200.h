@@ -209,10 +209,10 @@ typedef struct UbsGradBuffers {
     const uint16_t *flags; /* UbsPrimBuffers.flags of this view (for the skip test), or NULL */
     uint32_t *active;    /* n scratch: primitives the chain must visit, or NULL (visit all) */
     uint32_t *active_count; /* [1] scratch counter */
-    int32_t bwd_pixels_per_lane; /* fp32 raster backward layout: 0 or 2 = two pixels per lane (fastest
-                                    alone), 4 = four pixels per lane in smaller CTAs, 8 = one warp per
-                                    tile (one warp reduction per (tile, splat)); same results up to the
-                                    order of the float atomics */
+    int32_t bwd_pixels_per_lane; /* fp32 raster backward layout: 0 or 4 = four pixels per lane as two
+                                    packed fp32x2 pairs (fastest), 2 = two pixels per lane, 8 = one warp
+                                    per tile (one warp reduction per (tile, splat)); same results up to
+                                    the order of the float atomics */
     /* Deterministic mode (raster.py:1-8, gradients.py:164-173: bit-identical gradients run to run):
      * one warp per tile writes each splat's tile partial to a slot of its own (primitive i owns
      * det_slot_off[i] .. + tile_count[i], its rect's tiles in row-major order) and every primitive

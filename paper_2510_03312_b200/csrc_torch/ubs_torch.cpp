@@ -231,7 +231,7 @@ at::Tensor render_backward(const at::Tensor &params_in, int64_t n_dims, const at
     gb.flags = f.pb.flags;
     gb.active = (uint32_t *)active.data_ptr();
     gb.active_count = (uint32_t *)active_count.data_ptr();
-    gb.bwd_pixels_per_lane = 2;
+    gb.bwd_pixels_per_lane = 4;
     if (params.size(0) > 0) {
         check(ubs_raster_backward(&v, &f.pb, &f.bb, &f.ib, &gb, s), "ubs_raster_backward");
         check(ubs_prim_backward(&v, &gb, 0, s), "ubs_prim_backward");

@@ -734,13 +734,14 @@ def backward_frame(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_param
 
 
 def backward_raster(fr: Frame, ds: DeviceScene, g_image: torch.Tensor, grad_params: torch.Tensor,
-                    reg_opacity: float = 0.0, reg_scale: float = 0.0, pixels_per_lane: int = 2,
+                    reg_opacity: float = 0.0, reg_scale: float = 0.0, pixels_per_lane: int = 4,
                     deterministic: bool = False):
     """First half of :func:`backward_frame` on the current stream: the
     raster backward into the frame's screen-space sums (ws.grad2d).  Returns
     the UbsGradBuffers for :func:`backward_chain` (None for an empty scene).
-    ``pixels_per_lane`` picks the fp32 raster backward's layout (2: fastest
-    alone, 4: fastest beside other views' kernels; same results).
+    ``pixels_per_lane`` picks the fp32 raster backward's layout (4: two
+    packed fp32x2 pixel pairs per lane, the fastest alone and beside other
+    views' kernels; 2 and 8: one pixel per lane; same results).
     ``deterministic``: per-(primitive, tile) partials reduced in a fixed
     order instead of float atomics -- bit-identical sums on every run
     (raster.py:1-8, gradients.py:164-173), at the cost of a K x 10 buffer
