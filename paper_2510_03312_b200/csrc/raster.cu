@@ -1474,7 +1474,7 @@ __global__ void det_reduce_kernel(const uint32_t *__restrict__ slot_off, const u
 #define UBS_BWD4_MIN_CTAS 11
 #endif
 template <int NP>
-__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 24 : UBS_BWD4_MIN_CTAS)
+__global__ void __launch_bounds__(kTileThreads / NP, NP == 8 ? 16 : UBS_BWD4_MIN_CTAS)
 raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ids,
                       const Rec32 *__restrict__ recs, const float *__restrict__ tstop,
                       const int32_t *__restrict__ ncontrib, const float *__restrict__ g_image,
@@ -1677,15 +1677,20 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     }
                     return true;
                 };
-                using I0 = std::integral_constant<int, 0>;
-                using I1 = std::integral_constant<int, 1>;
                 using Yes = std::integral_constant<bool, true>;
                 using No = std::integral_constant<bool, false>;
-                static_assert(NQ == 2, "two pixel pairs per lane");
                 // any_in: warp-uniform (the writing pair's vote), the reduction's gate
-                bool any_in = pair(I0{}, Yes{});
-                if (any_in) pair(I1{}, No{});
-                else any_in = pair(I1{}, Yes{});
+                bool any_in = false;
+                auto step = [&](auto p_) {
+                    if (any_in) pair(p_, No{});
+                    else any_in = pair(p_, Yes{});
+                };
+                step(std::integral_constant<int, 0>{});
+                step(std::integral_constant<int, 1>{});
+                if constexpr (NQ > 2) {
+                    step(std::integral_constant<int, 2>{});
+                    step(std::integral_constant<int, 3>{});
+                }
                 if (any_in) {
                     float v[16];
 #pragma unroll
@@ -1801,7 +1806,8 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
     } else {
         // 0 / 4: packed pairs, four pixels per lane (the default: 0.77 ms against
         // 0.91 for two scalar pixels per lane on a 7D 3M 1080p view); 2 / 8 and
-        // raster_scalar: one pixel per lane (the packed one-warp 8-pixel layout spills)
+        // raster_scalar: one pixel per lane (the packed one-warp 8-pixel layout: 0.88 ms at 121
+        // registers, 16 warps per SM)
         const int ppl = gb->bwd_pixels_per_lane ? gb->bwd_pixels_per_lane : 4;
         if (ppl == 4 && !ib->raster_scalar)
             raster_bwd32x2_kernel<4><<<n_tiles, kTileThreads / 4, 0, s>>>(
