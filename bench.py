@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--lead-priority", type=int, default=0, help="CUDA stream priority of the group preprocess")
     ap.add_argument("--group", type=int, default=4,
                     help="frames per shared preprocess (FramePipeline.render_group; 0: frame by frame)")
+    ap.add_argument("--copy-streams", type=int, default=2, help="device->host copy streams of the end-to-end sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the reference-signature render() timing")
     ap.add_argument("--dropin-frames", type=int, default=10)
@@ -581,7 +582,7 @@ def run_ours(a, rank, world, local_rank):
     traffic = ncu_traffic(dominant)
 
     # --- end to end: image streamed to pinned host memory every frame -----
-    sink = engine.HostFrameSink(a.height, a.width, dtype=ws.image_buf.dtype, device=dev)
+    sink = engine.HostFrameSink(a.height, a.width, dtype=ws.image_buf.dtype, device=dev, copy_streams=a.copy_streams)
 
     def submit(k0, count=1):
         g = max(a.group, 1)
@@ -608,7 +609,7 @@ def run_ours(a, rank, world, local_rank):
         f0.record()
         submit(0, a.steps)
         pipe.join()
-        torch.cuda.current_stream().wait_stream(sink.copy_stream)
+        sink.join()
         f1.record()
         torch.cuda.synchronize()
         # as in the headline sweep: an asynchronous frame that outgrew its slot

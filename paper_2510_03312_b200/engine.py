@@ -855,9 +855,13 @@ class HostFrameSink:
     path a sweep user takes: the copy of frame k overlaps the render of k+1.
     """
 
-    def __init__(self, height: int, width: int, dtype=torch.float32, device="cuda", slots: int = 3):
+    def __init__(self, height: int, width: int, dtype=torch.float32, device="cuda", slots: int = 3,
+                 copy_streams: int = 1):
         self.dev = torch.device(device)
-        self.copy_stream = torch.cuda.Stream(self.dev)
+        # several copy streams: a frame that finishes early is not queued
+        # behind an earlier-submitted one still rendering
+        self.copy_streams = [torch.cuda.Stream(self.dev) for _ in range(max(1, int(copy_streams)))]
+        self.copy_stream = self.copy_streams[0]
         self.dev_bufs = [torch.empty((height, width, 3), dtype=dtype, device=self.dev) for _ in range(slots)]
         self.host_bufs = [torch.empty((height, width, 3), dtype=dtype, pin_memory=True) for _ in range(slots)]
         self.done = [None] * slots
@@ -883,8 +887,9 @@ class HostFrameSink:
             ready = torch.cuda.Event()
             ready.record()
             src = self.dev_bufs[i]
-        with torch.cuda.stream(self.copy_stream):
-            self.copy_stream.wait_event(ready)
+        cs = self.copy_streams[(self.k - 1) % len(self.copy_streams)]
+        with torch.cuda.stream(cs):
+            cs.wait_event(ready)
             self.host_bufs[i].copy_(src, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
@@ -893,4 +898,11 @@ class HostFrameSink:
         return self.host_bufs[i]
 
     def synchronize(self):
-        self.copy_stream.synchronize()
+        for cs in self.copy_streams:
+            cs.synchronize()
+
+    def join(self, stream: torch.cuda.Stream | None = None):
+        """Make ``stream`` (default: the current one) wait for every queued copy."""
+        stream = stream or torch.cuda.current_stream(self.dev)
+        for cs in self.copy_streams:
+            stream.wait_stream(cs)
