@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-inflight", type=int, default=8, help="views in flight per GPU in the training step")
     ap.add_argument("--train-group", type=int, default=8, help="training views per shared preprocess")
+    ap.add_argument("--train-separate-epilogue", action="store_true",
+                    help="plain Adam + separate zero / regulariser passes (A/B of the fused optimizer step)")
     ap.add_argument("--train-first-group", type=int, default=0,
                     help="views in a batch's first preprocess group (0: --train-group)")
     ap.add_argument("--train-ppl", type=int, default=4, choices=[2, 4, 8],
@@ -292,9 +294,11 @@ def run_train(a, rank, world, local_rank):
     adam = sharding.DeviceAdam(ds.params, 7)
     cfg = LossConfig()
     grad = step.backend.new_grad()
+    # the optimizer pass also prepares the next batch's gradient buffer (its
+    # zeroing, rank 0's regulariser gradient, the regulariser value)
     for _ in range(2):
         loss, grad = step.loss_and_grad(views, cfg, grad)
-        adam.step(grad)
+        step.optimizer_step(adam, grad, cfg)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -302,7 +306,10 @@ def run_train(a, rank, world, local_rank):
     e0.record()
     for _ in range(a.train_steps):
         loss, grad = step.loss_and_grad(views, cfg, grad)
-        adam.step(grad)
+        if a.train_separate_epilogue:
+            adam.step(grad)
+        else:
+            step.optimizer_step(adam, grad, cfg)
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)

@@ -51,7 +51,7 @@ extern "C" {
 
 typedef struct CUstream_st *ubs_stream_t; /* == cudaStream_t */
 
-#define UBS_ABI_VERSION 6
+#define UBS_ABI_VERSION 7
 #define UBS_TILE 16
 
 enum {
@@ -302,6 +302,18 @@ int ubs_prim_backward(const UbsView *v, const UbsGradBuffers *gb, int32_t add_re
 int ubs_adam_step(void *params, int32_t param_f64, const void *grads, int32_t grad_f64, float *m, float *v,
                   int64_t n, int32_t n_dims, const double *lr_group, int32_t step, int32_t freeze_shapes,
                   ubs_stream_t s);
+
+/* ubs_adam_step, then grads overwritten with the next step's starting
+ * gradient: the regulariser gradient of the updated parameters scaled by
+ * next_reg_opacity / next_reg_scale (exactly what zeroing the buffer and
+ * ubs_add_regularisers would leave; pass 0, 0 for zeros), and, when
+ * next_reg_sums is not NULL, the updated parameters' regulariser sums added
+ * into it as ubs_regulariser_value does.  One pass instead of four (Adam,
+ * zero, regularisers, value) between two training steps. */
+int ubs_adam_step_regularised(void *params, int32_t param_f64, void *grads, int32_t grad_f64, float *m, float *v,
+                              int64_t n, int32_t n_dims, const double *lr_group, int32_t step,
+                              int32_t freeze_shapes, double next_reg_opacity, double next_reg_scale,
+                              double *next_reg_sums, ubs_stream_t s);
 
 /* regulariser gradients, once per step (also fused into ubs_prim_backward) */
 int ubs_add_regularisers(const void *params, int32_t param_f64, void *grads, int32_t grad_f64, int64_t n,

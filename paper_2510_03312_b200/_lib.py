@@ -77,7 +77,7 @@ class UbsGradBuffers(Structure):
                 ("det_temp_bytes", c_size_t)]
 
 
-ABI_VERSION = 6  # UBS_ABI_VERSION in include/ubs_b200.h
+ABI_VERSION = 7  # UBS_ABI_VERSION in include/ubs_b200.h
 MAX_VIEWS = 8  # UBS_MAX_VIEWS
 
 # (name, restype, argtypes) for every symbol include/ubs_b200.h declares
@@ -105,6 +105,9 @@ SIGNATURES = [
     ("ubs_prim_backward", c_int32, [POINTER(UbsView), POINTER(UbsGradBuffers), c_int32, c_void_p]),
     ("ubs_adam_step", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_int64, c_int32,
                                 POINTER(c_double), c_int32, c_int32, c_void_p]),
+    ("ubs_adam_step_regularised", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_int64,
+                                            c_int32, POINTER(c_double), c_int32, c_int32, c_double, c_double,
+                                            c_void_p, c_void_p]),
     ("ubs_add_regularisers", c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_int32, c_double,
                                        c_double, c_void_p]),
     ("ubs_regulariser_value", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p]),

@@ -19,6 +19,8 @@ backend.)
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import ctypes
 
 import torch
@@ -290,6 +292,15 @@ class ViewShardedStep:
         self.backend = backend
         self.group = group
         self.retries = 0  # batches recomputed because an asynchronous view outgrew its buffers
+        self._next = None  # NextStep from optimizer_step
+
+    def optimizer_step(self, adam: "DeviceAdam", grad: torch.Tensor, cfg: LossConfig = LossConfig()):
+        """``adam.step(grad)`` fused with preparing ``grad`` for the next
+        ``loss_and_grad(..., grad=grad)``: its zeroing, the regulariser
+        gradient (rank 0 only, gradients.py:120-123) and the regulariser value
+        come out of the optimizer's own pass over the records."""
+        rank, _ = dist_rank_world(self.group)
+        self._next = adam.step(grad, next_cfg=cfg, regularise=rank == 0)
 
     def loss_and_grad(self, views, cfg: LossConfig = LossConfig(), grad: torch.Tensor | None = None,
                       buckets: int = 4):
@@ -311,9 +322,16 @@ class ViewShardedStep:
             # a view that outgrew its slot's buffers: grow every slot and retry
             # asynchronously, then (rarely) once more with synchronous frames
             sync = attempt > 1
-            grad = b.new_grad() if grad is None else grad.zero_()
-            if rank == 0:
-                b.add_regularisers(grad, cfg)
+            nxt, self._next = self._next, None
+            params = getattr(getattr(b, "ds", None), "params", None)
+            if (attempt == 0 and nxt is not None and grad is not None and nxt.grad is grad and params is not None
+                    and nxt.valid_for(params, cfg)):
+                reg_value = cfg.lambda_o * nxt.sums[0] + cfg.lambda_sigma * nxt.sums[1]  # prepared by the optimizer
+            else:
+                grad = b.new_grad() if grad is None else grad.zero_()
+                if rank == 0:
+                    b.add_regularisers(grad, cfg)
+                reg_value = None
             rec = torch.zeros(2, dtype=torch.float64, device=grad.device)
             works = []
             if hasattr(b, "begin"):  # batched backend: views may be in flight concurrently
@@ -343,8 +361,26 @@ class ViewShardedStep:
                 b.grow()
             else:
                 b.clear_status()
-        loss = cfg.loss_scale * (rec[0] / len(views) + b.regulariser_value(cfg))
+        if reg_value is None:
+            reg_value = b.regulariser_value(cfg)
+        loss = cfg.loss_scale * (rec[0] / len(views) + reg_value)
         return loss, grad
+
+
+@dataclass
+class NextStep:
+    """A gradient buffer made ready for the next batch by
+    ``DeviceAdam.step(grad, next_cfg)``: ``grad`` holds the regulariser
+    gradient of the parameters (or zeros on the ranks that do not add it),
+    ``sums`` their regulariser sums.  Valid while the parameters are
+    unchanged (same tensor, same version) and for the same loss config."""
+    grad: torch.Tensor
+    sums: torch.Tensor
+    cfg: LossConfig
+    key: tuple
+
+    def valid_for(self, params: torch.Tensor, cfg: LossConfig) -> bool:
+        return self.key == (params.data_ptr(), params._version) and self.cfg == cfg
 
 
 class DeviceAdam:
@@ -360,17 +396,35 @@ class DeviceAdam:
         self.freeze = 1 if freeze_shapes else 0
         self.step_count = 0
 
-    def step(self, grad: torch.Tensor):
+    def step(self, grad: torch.Tensor, next_cfg: LossConfig | None = None, regularise: bool = True):
+        """One Adam step.  With ``next_cfg`` the same pass also prepares
+        ``grad`` for the next batch (``ubs_adam_step_regularised``): it is
+        overwritten with the regulariser gradient of the updated parameters
+        (``regularise``, the one rank that adds it) or zeros, and the
+        regulariser sums are formed -- what the next ``loss_and_grad`` would
+        otherwise do in three more passes.  Returns the :class:`NextStep`
+        (None without ``next_cfg``)."""
         self.step_count += 1
         lib = _lib.load()
-        _lib.check(lib.ubs_adam_step(self.params.data_ptr(), int(self.params.dtype == torch.float64),
-                                     grad.data_ptr(), int(grad.dtype == torch.float64), self.m.data_ptr(),
-                                     self.v.data_ptr(), int(self.params.shape[0]), self.n_dims, self.lr,
-                                     self.step_count, self.freeze, torch.cuda.current_stream().cuda_stream),
-                   "ubs_adam_step")
+        p, stream = self.params, torch.cuda.current_stream().cuda_stream
+        common = (p.data_ptr(), int(p.dtype == torch.float64), grad.data_ptr(), int(grad.dtype == torch.float64),
+                  self.m.data_ptr(), self.v.data_ptr(), int(p.shape[0]), self.n_dims, self.lr, self.step_count,
+                  self.freeze)
+        if next_cfg is None:
+            _lib.check(lib.ubs_adam_step(*common, stream), "ubs_adam_step")
+            nxt = None
+        else:
+            sums = torch.zeros(2, dtype=torch.float64, device=p.device)
+            ro = next_cfg.loss_scale * next_cfg.lambda_o if regularise else 0.0
+            rs = next_cfg.loss_scale * next_cfg.lambda_sigma if regularise else 0.0
+            _lib.check(lib.ubs_adam_step_regularised(*common, ro, rs, sums.data_ptr(), stream),
+                       "ubs_adam_step_regularised")
         # the records changed behind torch's back: bump the version counter so
         # DeviceScene's statics cache sees new parameters
-        torch.autograd.graph.increment_version(self.params)
+        torch.autograd.graph.increment_version(p)
+        if next_cfg is not None:
+            nxt = NextStep(grad, sums, next_cfg, (p.data_ptr(), p._version))
+        return nxt
 
     def reset_rows(self, idx: torch.Tensor):
         """Zero the moments of rewritten rows (AdamState.reset_rows, optim.py:100-103)."""

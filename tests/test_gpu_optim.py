@@ -41,3 +41,38 @@ def test_device_adam_matches_reference(n):
         got = params.cpu().numpy()
         assert np.abs(got - p).max() <= 1e-5 * max(1.0, np.abs(p).max())
     assert np.all(np.abs(params.cpu().numpy()[:, clamp_cols]) <= 5)
+
+
+@pytest.mark.parametrize("pdt,gdt", [("float32", "float32"), ("float64", "float32"), ("float64", "float64")])
+@pytest.mark.parametrize("regularise", [True, False])
+def test_adam_step_regularised_matches_separate_passes(pdt, gdt, regularise):
+    """ubs_adam_step_regularised == ubs_adam_step, then zero + ubs_add_regularisers
+    + ubs_regulariser_value on the updated parameters (bit for bit, sums to 1e-12)."""
+    import torch
+    from paper_2510_03312_b200 import sharding, synthetic as S
+    from paper_2510_03312_b200.types import LossConfig, pack_records
+    sc = S.synth(7, 3001, seed=4)
+    p0 = torch.tensor(pack_records(sc, np.float64), device="cuda").to(getattr(torch, pdt))
+    rng = np.random.default_rng(5)
+    g0 = torch.tensor(rng.normal(size=p0.shape), device="cuda").to(getattr(torch, gdt))
+    cfg = LossConfig(lambda_o=0.01, lambda_sigma=0.002, loss_scale=3.0)
+    pa, ga = p0.clone(), g0.clone()
+    a = sharding.DeviceAdam(pa, 7)
+    a.step(ga)
+    ga.zero_()
+    be = type("B", (), {})()
+    be.ds = type("D", (), {"params": pa, "n": pa.shape[0], "n_dims": 7})()
+    if regularise:
+        sharding.GpuViewBackend.add_regularisers(be, ga, cfg)
+    ref_value = sharding.GpuViewBackend.regulariser_value(be, cfg)
+    pb, gb = p0.clone(), g0.clone()
+    b = sharding.DeviceAdam(pb, 7)
+    nxt = b.step(gb, next_cfg=cfg, regularise=regularise)
+    torch.cuda.synchronize()
+    assert torch.equal(pa, pb) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+    assert torch.equal(ga, gb)
+    got_value = cfg.lambda_o * nxt.sums[0] + cfg.lambda_sigma * nxt.sums[1]
+    assert abs(float(got_value) - float(ref_value)) <= 1e-12 * abs(float(ref_value))
+    assert nxt.valid_for(pb, cfg) and not nxt.valid_for(pb, LossConfig())
+    pb.add_(0.0)  # any in-place change of the parameters invalidates the prepared buffer
+    assert not nxt.valid_for(pb, cfg)

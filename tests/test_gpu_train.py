@@ -65,6 +65,32 @@ def test_batched_backend_trains():
     assert np.isfinite(losses).all() and losses[-1] < losses[0]
 
 
+def test_optimizer_step_prepares_next_batch():
+    """step.optimizer_step (Adam fused with the next batch's zeroing,
+    regulariser gradient and value) trains like adam.step + the separate
+    passes: same losses and parameters up to float-atomic rounding."""
+    nd = 7
+    views = _views(nd, 4)
+    cfg = LossConfig(lambda_o=0.01, lambda_sigma=0.001)
+    out = []
+    for fused in (False, True):
+        ds = engine.DeviceScene.from_scene(S.synth(nd, 6000, seed=1), device="cuda")
+        step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=4, group=2))
+        adam = sharding.DeviceAdam(ds.params, nd)
+        losses, grad = [], None
+        for _ in range(4):
+            loss, grad = step.loss_and_grad(views, cfg, grad)
+            losses.append(float(loss))
+            if fused:
+                step.optimizer_step(adam, grad, cfg)
+            else:
+                adam.step(grad)
+        out.append((np.array(losses), ds.params.double().cpu().numpy()))
+    (l0, p0), (l1, p1) = out
+    assert np.abs(l1 - l0).max() <= 1e-5 * np.abs(l0).max()
+    assert np.abs(p1 - p0).max() <= 1e-4 * max(1.0, np.abs(p0).max())
+
+
 @pytest.mark.parametrize("w,h", [(77, 53), (160, 120), (33, 17)])
 def test_backward_layouts_agree(w, h):
     """The fp32 raster backward's two layouts (2 or 4 pixels per lane) give
