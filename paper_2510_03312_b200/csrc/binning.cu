@@ -715,7 +715,6 @@ extern "C" int ubs_bin_tiles(const UbsView *v, const UbsPrimBuffers *pb, const U
     if (!v || !pb || !bb) return UBS_E_ARGS;
     const int W = v->cam.width, H = v->cam.height;
     const int TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
-    const int n_tiles = TX * TY;
     const int NB = (TX + kBand - 1) / kBand, nbk = ((TY + kRows - 1) / kRows) * NB;
     cudaStream_t s = (cudaStream_t)stream;
     if (n_pairs == 0 || v->n == 0) return UBS_OK;

@@ -460,7 +460,7 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     const int ty = tile / P.TX, tx = tile - ty * P.TX;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wx = warp & 1, wy = warp >> 1;
-    const int b0 = 2 * (2 * wy) + wx, b1 = b0 + 2;  // this warp's two 8x4 blocks (warp_cover_mask bits)
+    // this warp's two 8x4 blocks are warp_cover_mask bits 2 (2 wy) + wx and that + 2
     const int lx = 8 * wx + (lane & 7), ly = 8 * wy + (lane >> 3);  // pixel 0; pixel 1 is 4 rows down
     const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
     const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
@@ -468,7 +468,7 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     bool capped;
     tile_span(P, ranges, tile, start, end, capped);
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
-    const float clamp = (float)P.clamp, one_minus_clamp = (float)(1.0 - P.clamp);
+    const float clamp = (float)P.clamp;
     const float clamp_lo = clamp - 0.05f;
     const float tmin = (float)P.tmin;
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
@@ -637,7 +637,7 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     if (!done1 && Df.y > kImgErrTol * Tf.y) flag1 = 1;
     if (!(edge0 > 0.0f)) flag0 = 1;  // some visit had m in [tau, tau + E)
     if (!(edge1 > 0.0f)) flag1 = 1;
-    const int64_t npix = (int64_t)P.W * P.H;
+    [[maybe_unused]] const int64_t npix = (int64_t)P.W * P.H;  // bounds guards (checked builds)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const bool inside = h ? in1 : in0;
