@@ -744,7 +744,7 @@ def run_ours(a, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": sink.bytes_per_frame,
-                "path": "engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, copy stream)",
+                "path": f"engine.FramePipeline + HostFrameSink (fp32 image -> pinned host, {a.copy_streams} copy stream(s))",
                 "d2h_link_gbs": d2h_gbs, "link_ceiling_fps": d2h_gbs * 1e9 / sink.bytes_per_frame},
         # one preprocess launch per group of frames (--group), the rest per frame
         "e2e_dropin": dropin,

@@ -397,10 +397,12 @@ def test_pipeline_zero_copy_host_sink():
         assert torch.equal(a, b)
 
 
-def test_grouped_pipeline_zero_copy_host_sink():
+@pytest.mark.parametrize("copy_streams", [1, 3])
+def test_grouped_pipeline_zero_copy_host_sink(copy_streams):
     # groups of frames share one preprocess (render_group); the sink reads each
     # slot's image and the slot's next group waits for that copy, so every
-    # host image equals the single-stream render
+    # host image equals the single-stream render (with one or several copy
+    # streams: a copy waits only for its own frame)
     import torch
     from paper_2510_03312_b200 import engine
     sc = quantize_f32(S.random_scene(7, 3000, seed=73))
@@ -412,7 +414,7 @@ def test_grouped_pipeline_zero_copy_host_sink():
     pipe = engine.FramePipeline(ds, depth=6)
     for q in qs * 2:
         pipe.render(cam, q, sync=True)
-    sink = engine.HostFrameSink(96, 96, slots=len(qs))
+    sink = engine.HostFrameSink(96, 96, slots=len(qs), copy_streams=copy_streams)
     outs = []
     for g0 in range(0, len(qs), 3):  # groups of 3, the last one short
         for fr in pipe.render_group([(cam, q) for q in qs[g0:g0 + 3]]):
