@@ -661,13 +661,14 @@ def run_ours(a, rank, world, local_rank):
     dropin = None
     if rank == 0 and not a.no_dropin:
         from paper_2510_03312_b200 import raster as R
-        R.render(scene, cam, frame_query(a.nd, cam, 0), DEFAULT_SETTINGS)  # warm: workspace, pinned staging
+        for k in range(2):  # warm: workspace, pinned staging, the pinned blocks of two live images
+            img = R.render(scene, cam, frame_query(a.nd, cam, k), DEFAULT_SETTINGS)
         t0 = time.perf_counter()
         for k in range(a.dropin_frames):
             img = R.render(scene, cam, frame_query(a.nd, cam, k), DEFAULT_SETTINGS)
         per_call = (time.perf_counter() - t0) / a.dropin_frames
         with R.resident(scene):
-            R.render(scene, cam, frame_query(a.nd, cam, 0), DEFAULT_SETTINGS)
+            img = R.render(scene, cam, frame_query(a.nd, cam, 0), DEFAULT_SETTINGS)
             t0 = time.perf_counter()
             for k in range(a.dropin_frames * 4):
                 img = R.render(scene, cam, frame_query(a.nd, cam, k), DEFAULT_SETTINGS)

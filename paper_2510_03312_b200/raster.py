@@ -18,6 +18,8 @@ from __future__ import annotations
 import math
 from types import SimpleNamespace
 
+import weakref
+
 import numpy as np
 import torch
 
@@ -43,6 +45,14 @@ def workspace(precision: str | None = None, device=None) -> engine.Workspace:
 
 
 _PINNED: dict = {}  # tag -> the reused pinned host staging buffer (latest shape only)
+
+
+_PINNED_OUT = [0]     # images handed out in pinned memory and still alive
+_PINNED_OUT_MAX = 8   # beyond this many, images are copied into ordinary memory
+
+
+def _pinned_out_released():
+    _PINNED_OUT[0] -= 1
 
 
 def _pinned(tag, shape, dtype) -> torch.Tensor:
@@ -176,7 +186,8 @@ def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
     dst = st.numpy()
     rec = _packed_records(scene, n)
     if rec is not None:  # every field is a view into one packed record array
-        _parallel_rows(n, lambda r0, r1: np.copyto(dst[r0:r1], rec[r0:r1], casting="unsafe"))
+        def fill(r0, r1):
+            np.copyto(dst[r0:r1], rec[r0:r1], casting="unsafe")
     else:
         from .types import field_offsets
         fields = [(np.asarray(getattr(scene, k)).reshape(n, -1), off, size)
@@ -185,7 +196,7 @@ def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
         def fill(r0, r1):
             for a, off, size in fields:
                 np.copyto(dst[r0:r1, off:off + size], a[r0:r1], casting="unsafe")
-        _parallel_rows(n, fill)
+    _parallel_rows(n, fill)
     params = st.to(ws.device, non_blocking=True)
     ds = engine.DeviceScene(params, scene.n_dims, scene.background)
     if hit is not None and hit[0] is scene:
@@ -205,6 +216,18 @@ def _host_image(fr: engine.Frame, background) -> np.ndarray:
         empty = (fr.alpha_sum == 0) & (fr.t_stop == 1)
         bg = torch.as_tensor(np.asarray(background, dtype=np.float64).reshape(3), device=img.device)
         img = torch.where(empty[..., None], bg, img)
+    if _PINNED_OUT[0] < _PINNED_OUT_MAX:
+        # straight into a pinned block of torch's caching host allocator, which
+        # the returned array keeps alive (and gives back when it is dropped):
+        # no host copy.  Past _PINNED_OUT_MAX arrays still alive, the image goes
+        # through the reused staging buffer into ordinary memory instead.
+        t = torch.empty((H, W, 3), dtype=torch.float64, pin_memory=True)
+        t.copy_(img, non_blocking=True)
+        torch.cuda.current_stream(fr.image.device).synchronize()
+        out = t.numpy()
+        _PINNED_OUT[0] += 1
+        weakref.finalize(t, _pinned_out_released)
+        return out
     st = _pinned("image", (H, W, 3), torch.float64)
     st.copy_(img, non_blocking=True)
     torch.cuda.current_stream(fr.image.device).synchronize()
