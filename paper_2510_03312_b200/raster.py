@@ -47,6 +47,7 @@ def workspace(precision: str | None = None, device=None) -> engine.Workspace:
 _PINNED: dict = {}  # tag -> the reused pinned host staging buffer (latest shape only)
 
 
+_STAGE_PARTS = 4      # drop-in scene staging: parts whose uploads overlap the next parts' casts
 _PINNED_OUT = [0]     # images handed out in pinned memory and still alive
 _PINNED_OUT_MAX = 8   # beyond this many, images are copied into ordinary memory
 
@@ -196,8 +197,25 @@ def _device_scene(scene, ws: engine.Workspace) -> engine.DeviceScene:
         def fill(r0, r1):
             for a, off, size in fields:
                 np.copyto(dst[r0:r1, off:off + size], a[r0:r1], casting="unsafe")
-    _parallel_rows(n, fill)
-    params = st.to(ws.device, non_blocking=True)
+    params = torch.empty((n, width), dtype=dtype, device=ws.device)
+    if n < 1 << 18:
+        fill(0, n)
+        params.copy_(st, non_blocking=True)
+    else:
+        # _STAGE_PARTS row parts, each cut into one task per host thread and
+        # queued in order: part k is cast before part k + 1, and its DMA
+        # overlaps the later parts' casts
+        workers = _pool()._max_workers
+        bounds = [n * k // _STAGE_PARTS for k in range(_STAGE_PARTS + 1)]
+        parts = list(zip(bounds[:-1], bounds[1:]))
+        futs = []
+        for h0, h1 in parts:
+            step = -(-(h1 - h0) // workers)
+            futs.append([_pool().submit(fill, r0, min(h1, r0 + step)) for r0 in range(h0, h1, step)])
+        for (h0, h1), fs in zip(parts, futs):
+            for f in fs:
+                f.result()
+            params[h0:h1].copy_(st[h0:h1], non_blocking=True)
     ds = engine.DeviceScene(params, scene.n_dims, scene.background)
     if hit is not None and hit[0] is scene:
         hit[1][(str(ws.device), ws.precision)] = ds
