@@ -43,7 +43,7 @@ def _host_grads(grads: torch.Tensor, n_dims: int) -> SceneGrads:
         arr = host.numpy()
         _raster._PINNED_OUT[0] += 1
         import weakref
-        weakref.finalize(host, _raster._pinned_out_released)
+        weakref.finalize(arr.base, _raster._pinned_out_released)  # the alias every field view holds
         return SceneGrads(**{name: arr[p0:p0 + n * size].reshape((n,) + shape)
                              for name, (p0, size, shape) in where.items()})
     stage = {}

@@ -244,7 +244,9 @@ def _host_image(fr: engine.Frame, background) -> np.ndarray:
         torch.cuda.current_stream(fr.image.device).synchronize()
         out = t.numpy()
         _PINNED_OUT[0] += 1
-        weakref.finalize(t, _pinned_out_released)
+        # on the tensor object the array holds (t.numpy()'s base is its own
+        # alias of t's storage): released when the last view of it goes
+        weakref.finalize(out.base, _pinned_out_released)
         return out
     st = _pinned("image", (H, W, 3), torch.float64)
     st.copy_(img, non_blocking=True)

@@ -72,3 +72,26 @@ def test_synth_is_float32_exact():
     rec = pack_records(sc, np.float64)
     assert np.array_equal(rec, rec.astype(np.float32).astype(np.float64))
     assert np.all(sc.b_q >= -1) and np.all(sc.b_q <= 1)
+
+
+def test_pinned_handout_counter_follows_the_arrays():
+    """The drop-in hands images / gradients out in pinned blocks and counts
+    the live ones (raster._PINNED_OUT, bounded by _PINNED_OUT_MAX): the count
+    must drop only when the last array viewing a block is gone (the finalizer
+    sits on the tensor alias the ndarray holds, not on the allocating tensor)."""
+    import gc
+    import weakref
+    import torch
+    from paper_2510_03312_b200 import raster
+    before = raster._PINNED_OUT[0]
+    t = torch.zeros(64, dtype=torch.float64)  # stands in for the pinned block
+    out = t.numpy()
+    raster._PINNED_OUT[0] += 1
+    weakref.finalize(out.base, raster._pinned_out_released)
+    view = out[8:16].reshape(2, 4)
+    del t, out
+    gc.collect()
+    assert raster._PINNED_OUT[0] == before + 1  # the view keeps the block
+    del view
+    gc.collect()
+    assert raster._PINNED_OUT[0] == before
