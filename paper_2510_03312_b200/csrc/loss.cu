@@ -547,6 +547,11 @@ ssim_adj_tile_kernel(const T *__restrict__ a, const T *__restrict__ b, const T *
 // tap for two of the blurred quantities, 64-bit shared loads and stores.  The
 // halo loads walk rows with one warp per row, the per-lane source columns
 // computed once (no per-element division).
+#ifndef UBS_SSIM_ROW_UNROLL
+#define UBS_SSIM_ROW_UNROLL 4
+#endif
+constexpr int kSsimRowUnroll = UBS_SSIM_ROW_UNROLL;  // halo rows in flight per warp
+
 __device__ __forceinline__ void ssim_col_sources(int x0col, int lane, int W, int (&colq)[4]) {
     // float column lane + 32 j of the forward halo (pixel x0 - 5 + hc / 3): its
     // reflected source column, or -1 past W + 4 (those feed no output)
@@ -574,7 +579,7 @@ ssim_fwd_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, int
     for (int t = 0; t < 11; ++t) k[t] = (float)w.k[t];
     int colq[4];
     ssim_col_sources(x0, lane, W, colq);
-#pragma unroll 2
+#pragma unroll kSsimRowUnroll
     for (int yy = warp; yy < kSsimHaloRows; yy += kSsimThreads / 32) {
         const int py = y0 - kSsimR + yy;
         const bool rowok = py < H + kSsimR;
@@ -732,7 +737,7 @@ ssim_adj_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, con
 #pragma unroll
         for (int t = 0; t < 11; ++t) sk[t] = k[t];
     // g3 over rows y0-5 .. y0+TH+5 and float columns (x0-5)*3 .. (x0+TW+5)*3, zero outside
-#pragma unroll 2
+#pragma unroll kSsimRowUnroll
     for (int yy = warp; yy < kSsimHaloRows; yy += kSsimThreads / 32) {
         const int y = y0 - kSsimR + yy;
         const bool rowok = y >= 0 && y < H;
