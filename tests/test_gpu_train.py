@@ -27,14 +27,16 @@ def _views(nd, n_views, w=160, h=120):
     return out
 
 
-@pytest.mark.parametrize("depth,group,ppl", [(3, 1, 4), (8, 4, 4), (4, 4, 4), (8, 8, 8), (4, 2, 2)])
-def test_batched_backend_matches_one_view_at_a_time(depth, group, ppl):
+@pytest.mark.parametrize("depth,group,ppl,first", [(3, 1, 4, None), (8, 4, 4, None), (4, 4, 4, None), (8, 8, 8, None),
+                                                   (4, 2, 2, None), (6, 4, 4, 1), (8, 6, 4, 2)])
+def test_batched_backend_matches_one_view_at_a_time(depth, group, ppl, first):
     nd = 7
     ds = engine.DeviceScene.from_scene(S.synth(nd, 6000, seed=1), device="cuda")
     views = _views(nd, 6)
     cfg = LossConfig()
     ref_loss, ref = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=1)).loss_and_grad(views, cfg)
-    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=depth, group=group, pixels_per_lane=ppl))
+    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=depth, group=group, pixels_per_lane=ppl,
+                                                            first_group=first))
     for _ in range(2):  # the second call reuses every slot (slot-free ordering)
         loss, grad = step.loss_and_grad(views, cfg)
     assert abs(float(loss) - float(ref_loss)) <= 1e-9 * abs(float(ref_loss))
