@@ -11,6 +11,8 @@
 // and reads per view, recomputing costs ~2 kflop of fp64 per primitive.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "ubs_common.cuh"
 
 namespace ubs {
@@ -105,7 +107,9 @@ prim_active_kernel(const GT *__restrict__ grad2d, const uint16_t *__restrict__ f
 #ifndef UBS_PRIM_BWD_MIN_CTAS
 #define UBS_PRIM_BWD_MIN_CTAS 1
 #endif
-template <int C, typename PT, typename GT, typename OT>
+// kCached: the frame's scene statics are current (UbsView.statics): the
+// forward's query-invariant half is read back instead of recomputed
+template <int C, typename PT, typename GT, typename OT, bool kCached>
 __global__ void __launch_bounds__(128, UBS_PRIM_BWD_MIN_CTAS)
 prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, int add_reg,
                 double reg_o, double reg_s, uint32_t *__restrict__ nonfinite, const uint32_t *__restrict__ active,
@@ -114,7 +118,16 @@ prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, 
     constexpr int CC = PrimGeom<C>::CC;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (active) {
-        if (i >= (int64_t)*active_count) return;
+        const int64_t na = (int64_t)*active_count;
+        // statics pay off once most primitives are active (their block-strided
+        // reads are then dense); a sparse active set recomputes instead: both
+        // variants are launched, each keeps its regime
+        if constexpr (kCached) {
+            if (4 * na < v.n) return;
+        } else {
+            if (v.statics && 4 * na >= v.n) return;
+        }
+        if (i >= na) return;
         i = active[i];
     } else if (i >= v.n) {
         return;
@@ -122,7 +135,8 @@ prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, 
     const PT *rec = reinterpret_cast<const PT *>(v.params) + i * P;
     PrimGeom<C> g;
     double mu_x[3];
-    prim_geom<C, PT>(rec, v, g, mu_x);
+    if constexpr (kCached) prim_geom_cached<C, PT>(rec, i, v, g, mu_x);
+    else prim_geom<C, PT>(rec, v, g, mu_x);
 
     // grad2d holds raw per-pixel moments (raster_bwd kernels); the per-splat
     // factors of tile_backward (_tiles.py:114-127) are applied here once:
@@ -410,21 +424,26 @@ static void launch_bwd(const UbsView &v, const UbsGradBuffers &gb, int add_reg, 
             prim_active_kernel<float><<<ab, 256, 0, s>>>((const float *)gb.grad2d, gb.flags, v.n, add_reg, gb.active,
                                                          gb.active_count);
     }
-    if (g2d_f64) {
-        if (gb.grad_f64)
-            prim_bwd_kernel<C, PT, double, double><<<blocks, 128, 0, s>>>(
-                v, (double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
-        else
-            prim_bwd_kernel<C, PT, double, float><<<blocks, 128, 0, s>>>(
-                v, (double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
-    } else {
-        if (gb.grad_f64)
-            prim_bwd_kernel<C, PT, float, double><<<blocks, 128, 0, s>>>(
-                v, (float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
-        else
-            prim_bwd_kernel<C, PT, float, float><<<blocks, 128, 0, s>>>(
-                v, (float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
-    }
+    auto run = [&](auto cached) {
+        constexpr bool kC = decltype(cached)::value;
+        if (g2d_f64) {
+            if (gb.grad_f64)
+                prim_bwd_kernel<C, PT, double, double, kC><<<blocks, 128, 0, s>>>(
+                    v, (double *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+            else
+                prim_bwd_kernel<C, PT, double, float, kC><<<blocks, 128, 0, s>>>(
+                    v, (double *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+        } else {
+            if (gb.grad_f64)
+                prim_bwd_kernel<C, PT, float, double, kC><<<blocks, 128, 0, s>>>(
+                    v, (float *)gb.grad2d, (double *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+            else
+                prim_bwd_kernel<C, PT, float, float, kC><<<blocks, 128, 0, s>>>(
+                    v, (float *)gb.grad2d, (float *)gb.grad_params, add_reg, gb.reg_opacity, gb.reg_scale, gb.nonfinite, gb.active, gb.active_count);
+        }
+    };
+    if (v.statics) run(std::true_type{});  // dense active sets (or no compaction): read the statics back
+    if (!v.statics || gb.active) run(std::false_type{});  // sparse active sets: recompute
 }
 
 }  // namespace ubs

@@ -275,6 +275,49 @@ __device__ __forceinline__ double sigmoid64(double x) {
     return e / (1.0 + e);
 }
 
+// R = I + A (A skew from (a1, a2, a3), covariance.py:57-72) and Lx = R diag(sx)
+template <int C>
+__device__ __forceinline__ void static_rotation(const double (&rot)[3], PrimGeom<C> &g) {
+    g.R[0][0] = 1.0;     g.R[0][1] = -rot[2]; g.R[0][2] = rot[1];
+    g.R[1][0] = rot[2];  g.R[1][1] = 1.0;     g.R[1][2] = -rot[0];
+    g.R[2][0] = -rot[1]; g.R[2][1] = rot[0];  g.R[2][2] = 1.0;
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) g.Lx[i][k] = g.R[i][k] * g.sx[k];
+}
+
+// Sx = Lx Lx^T (covariance.py:104-119)
+template <int C>
+__device__ __forceinline__ void static_sx(const PrimGeom<C> &g, double (&Sx)[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            Sx[i][j] = g.Lx[i][0] * g.Lx[j][0] + g.Lx[i][1] * g.Lx[j][1] + g.Lx[i][2] * g.Lx[j][2];
+}
+
+// raw = Sx - Sxq M diag(beta_q) Sqx (slicing.py:210-211), sym3 = (raw + raw^T) / 2
+template <int C>
+__device__ __forceinline__ void static_sym3(PrimGeom<C> &g, const double (&Sx)[3][3]) {
+    double raw[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) raw[i][j] = Sx[i][j];
+    if constexpr (C > 0) {
+        double H[3][C];  // Sxq M
+        for (int i = 0; i < 3; ++i)
+            for (int k = 0; k < C; ++k) {
+                double s = 0.0;
+                for (int j = 0; j < C; ++j) s += g.Sxq[i][j] * g.M[j][k];
+                H[i][k] = s;
+            }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double s = 0.0;
+                for (int k = 0; k < C; ++k) s += H[i][k] * g.beta_q[k] * g.Sxq[j][k];
+                raw[i][j] = Sx[i][j] - s;
+            }
+    }
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) g.sym3[i][j] = 0.5 * (raw[i][j] + raw[j][i]);
+}
+
 // Query-invariant half of slice_scene (slicing.py:185-235): activations,
 // Sx, the query block inverse M, Sxq, the conditional covariance with its PSD
 // floor, opacity and beta_x.  Depends on the parameters and psd_floor_scale
@@ -289,24 +332,14 @@ __device__ inline void prim_static(const PT *rec, const UbsSettings &set, PrimGe
     load_params<C>(rec, mu_x, mu_q, rot, sxr, lq, sqr, bxr, bqr, oraw, g.color);
 
     for (int k = 0; k < 3; ++k) g.sx[k] = exp(sxr[k]);
-    // R = I + A, A skew from (a1, a2, a3)  (covariance.py:57-72)
-    g.R[0][0] = 1.0;     g.R[0][1] = -rot[2]; g.R[0][2] = rot[1];
-    g.R[1][0] = rot[2];  g.R[1][1] = 1.0;     g.R[1][2] = -rot[0];
-    g.R[2][0] = -rot[1]; g.R[2][1] = rot[0];  g.R[2][2] = 1.0;
-    for (int i = 0; i < 3; ++i)
-        for (int k = 0; k < 3; ++k) g.Lx[i][k] = g.R[i][k] * g.sx[k];
+    static_rotation<C>(rot, g);
     double Sx[3][3];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            Sx[i][j] = g.Lx[i][0] * g.Lx[j][0] + g.Lx[i][1] * g.Lx[j][1] + g.Lx[i][2] * g.Lx[j][2];
+    static_sx<C>(g, Sx);
 
     g.beta_x = 4.0 * exp(bxr);
     g.opacity = sigmoid64(oraw);
     g.log2_op = log2(g.opacity);
     g.valid = true;
-    double raw[3][3];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) raw[i][j] = Sx[i][j];
 
     if constexpr (C > 0) {
         for (int k = 0; k < C; ++k) {
@@ -341,25 +374,11 @@ __device__ inline void prim_static(const PT *rec, const UbsSettings &set, PrimGe
             for (int i = 0; i < C; ++i)
                 for (int j = 0; j < C; ++j) g.M[i][j] = (i == j) ? 1.0 : 0.0;
         }
-        // conditional covariance: Sx - Sxq M diag(beta_q) Sqx (slicing.py:210-211)
-        double H[3][C];  // Sxq M
-        for (int i = 0; i < 3; ++i)
-            for (int k = 0; k < C; ++k) {
-                double s = 0.0;
-                for (int j = 0; j < C; ++j) s += g.Sxq[i][j] * g.M[j][k];
-                H[i][k] = s;
-            }
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) {
-                double s = 0.0;
-                for (int k = 0; k < C; ++k) s += H[i][k] * g.beta_q[k] * g.Sxq[j][k];
-                raw[i][j] = Sx[i][j] - s;
-            }
     }
 
-    // symmetrise + PSD eigen floor (slicing.py:212-222)
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) g.sym3[i][j] = 0.5 * (raw[i][j] + raw[j][i]);
+    // conditional covariance, symmetrised (slicing.py:210-212), then the PSD
+    // eigen floor (slicing.py:212-222)
+    static_sym3<C>(g, Sx);
     g.floor_eps = set.psd_floor_scale * (Sx[0][0] + Sx[1][1] + Sx[2][2]) / 3.0;
     {
         // cheap test first: sym - eps I positive definite <=> lambda_min > eps
@@ -615,6 +634,40 @@ __device__ inline void load_statics(const void *buf, int64_t i, PrimGeom<C> &g, 
     for (int k = 0; k < 3; ++k) mu_x[k] = (double)ld_statics<PT, kGlobal>(r + k * S);
     for (int k = 0; k < C; ++k) mu_q[k] = (double)ld_statics<PT, kGlobal>(r + (3 + k) * S);
     for (int k = 0; k < 3; ++k) g.color[k] = (double)ld_statics<PT, kGlobal>(r + (3 + C + k) * S);
+}
+
+// prim_geom for primitive i of a scene whose statics are current: the
+// query-invariant half is read back (load_statics: the bits prim_static
+// computed) instead of recomputed -- no Cholesky, inverse or eigen floor --
+// and only what the adjoint needs beyond the statics is rebuilt from the
+// parameters with prim_static's own helpers: sx, R, Lx, sq, lqx and, for a
+// floored conditional covariance, the pre-floor sym3.  Same bits as
+// prim_geom (gradients.py:179-280 reads all of them).
+template <int C, typename PT>
+__device__ inline void prim_geom_cached(const PT *rec, int64_t i, const UbsView &v, PrimGeom<C> &g,
+                                        double (&mu_x)[3]) {
+    constexpr int CC = PrimGeom<C>::CC;
+    double mu_q[CC];
+    load_statics<C, PT, true>(v.statics, i, g, mu_x, mu_q);
+    double mx[3], mq[CC], rot[3], sxr[3], lq[CC * 3], sqr[CC], bxr, bqr[CC], oraw, col[3];
+    load_params<C>(rec, mx, mq, rot, sxr, lq, sqr, bxr, bqr, oraw, col);
+    for (int k = 0; k < 3; ++k) g.sx[k] = exp(sxr[k]);
+    static_rotation<C>(rot, g);
+    if constexpr (C > 0) {
+        for (int k = 0; k < C; ++k) {
+            g.sq[k] = exp(sqr[k]);
+            for (int j = 0; j < 3; ++j) g.lqx[k][j] = lq[3 * k + j];
+        }
+    }
+    if (g.floored3) {
+        double Sx[3][3];
+        static_sx<C>(g, Sx);
+        static_sym3<C>(g, Sx);
+    } else {
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) g.sym3[a][b] = g.cov3[a][b];  // prim_static's cov3 = sym3 when unfloored
+    }
+    prim_view<C>(g, mu_x, mu_q, v);
 }
 
 // Device-side capacity guard for the pair buffers: true (and the overflow
