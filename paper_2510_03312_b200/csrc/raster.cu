@@ -997,35 +997,52 @@ __device__ __forceinline__ bool warp_reduce10(T (&v)[16], int lane, int &idx, T 
     return false;
 }
 
-// warp_reduce10 without the per-call reporter bookkeeping, for a kernel that
-// keeps its lane's component index (reduce10_index, -1: no component) in a
-// register: lanes l % 4 == 0 return component reduce10_index(l), lanes 1 and
-// 17 components 8 and 9 (the same sums and summation order).
+// Warp sums of 10 per-lane values in 12 exchanges (warp_reduce10 takes 14):
+// a reduce-scatter over lane bit 16 (components 0-4 stay with the lower
+// half, 5-9 go to the upper), then over bit 8 on the pairs (0,1), (2,3) of
+// each half's five with the fifth summed on both sides, over bit 4 on the
+// remaining pair and the fifth, over bit 2 between that component and the
+// fifth, and a last butterfly over bit 1.  Lane l ends with component
+// reduce10_index(l) of its half (-1 for the lanes whose copy is not the one
+// reported: odd lanes, and the redundant holders of the fifth).
 template <typename T>
 __device__ __forceinline__ T warp_reduce10_value(T (&v)[16], int lane) {
+    const bool u16 = (lane & 16) != 0, u8 = (lane & 8) != 0, u4 = (lane & 4) != 0, u2 = (lane & 2) != 0;
+    T w[5];
 #pragma unroll
-    for (int lvl = 0; lvl < 3; ++lvl) {
-        const int half = 4 >> lvl, off = 16 >> lvl;
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < half; ++i) {
-            const T send = upper ? v[i] : v[i + half];
-            const T keep = upper ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
+    for (int i = 0; i < 5; ++i) {  // bit 16: lower keeps 0-4, upper keeps 5-9
+        const T send = u16 ? v[i] : v[i + 5];
+        const T keep = u16 ? v[i + 5] : v[i];
+        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    T r = v[0];
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    const bool up = (lane & 16) != 0;
-    T c = (up ? v[9] : v[8]) + __shfl_xor_sync(0xffffffffu, up ? v[8] : v[9], 16);
+    T x[3];
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    return (lane & 3) == 0 ? r : c;
+    for (int j = 0; j < 2; ++j) {  // bit 8: pairs (0, 1), (2, 3)
+        const T send = u8 ? w[2 * j] : w[2 * j + 1];
+        const T keep = u8 ? w[2 * j + 1] : w[2 * j];
+        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    x[2] = w[4] + __shfl_xor_sync(0xffffffffu, w[4], 8);
+    T y0, y1;
+    {  // bit 4: pair (x0, x1), and the fifth
+        const T send = u4 ? x[0] : x[1];
+        const T keep = u4 ? x[1] : x[0];
+        y0 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        y1 = x[2] + __shfl_xor_sync(0xffffffffu, x[2], 4);
+    }
+    // bit 2: lower keeps y0 (a pair component), upper keeps the fifth
+    const T send = u2 ? y0 : y1;
+    const T keep = u2 ? y1 : y0;
+    T r = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
 }
 __device__ __forceinline__ int reduce10_index(int lane) {
-    if ((lane & 3) == 0) return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    return lane == 1 ? 8 : (lane == 17 ? 9 : -1);
+    if (lane & 1) return -1;
+    const int base = (lane & 16) ? 5 : 0;
+    if (lane & 2) return (lane & 12) ? -1 : base + 4;  // the fifth: one reporter per half
+    // pair component: bit 4 picks the pair (0,1) / (2,3), bit 8 its member
+    return base + 2 * ((lane >> 2) & 1) + ((lane >> 3) & 1);
 }
 
 // fp64 backward (tile_backward, _tiles.py:59-127) in the reference's operation order
