@@ -958,46 +958,7 @@ __device__ __forceinline__ bool bwd64_pixel(const Rec64 &r, int px, int py, doub
     return true;
 }
 
-// Warp sums of 10 per-lane values v[0..9] in ~44 instructions: components
-// 0..7 by a reduce-scatter over lane bits 4..2 plus two xor levels (lane l
-// ends with component ((l >> 2) & 7) bit-reversed as idx below), components
-// 8 and 9 by one exchange over bit 4 plus four xor levels (every lower lane
-// holds sum v8, every upper lane sum v9).  Lanes l % 4 == 0 report component
-// idx, lane 1 component 8, lane 17 component 9: one atomic instruction.
-template <typename T>
-__device__ __forceinline__ bool warp_reduce10(T (&v)[16], int lane, int &idx, T &out) {
-#pragma unroll
-    for (int lvl = 0; lvl < 3; ++lvl) {
-        const int half = 4 >> lvl, off = 16 >> lvl;
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < half; ++i) {
-            const T send = upper ? v[i] : v[i + half];
-            const T keep = upper ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-    }
-    T r = v[0];
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    const bool up = (lane & 16) != 0;
-    T c = (up ? v[9] : v[8]) + __shfl_xor_sync(0xffffffffu, up ? v[8] : v[9], 16);
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((lane & 3) == 0) {
-        idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-        out = r;
-        return true;
-    }
-    if (lane == 1 || lane == 17) {
-        idx = lane == 1 ? 8 : 9;
-        out = c;
-        return true;
-    }
-    return false;
-}
-
-// Warp sums of 10 per-lane values in 12 exchanges (warp_reduce10 takes 14):
+// Warp sums of 10 per-lane values in 12 exchanges (a 3-level split takes 14):
 // a reduce-scatter over lane bit 16 (components 0-4 stay with the lower
 // half, 5-9 go to the upper), then over bit 8 on the pairs (0,1), (2,3) of
 // each half's five with the fifth summed on both sides, over bit 4 on the
@@ -1118,9 +1079,9 @@ raster_bwd64_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
             bool contrib = false;
             if (j < my_cnt) contrib = bwd64_pixel(srec[j - lo], px, py, tau, clamp, one_minus_clamp, g0, g1, g2, T, suffix, v);
             if (__any_sync(0xffffffffu, contrib)) {
-                int idx = 0;
-                double mine = 0;
-                if (warp_reduce10(v, lane, idx, mine) && mine != (double)0)
+                const double mine = warp_reduce10_value(v, lane);
+                const int idx = reduce10_index(lane);
+                if (idx >= 0 && mine != (double)0)
                     atomicAdd(grad2d + (int64_t)sid[j - lo] * kGrad2dStride + idx, mine);
             }
           }
@@ -1358,9 +1319,9 @@ raster_bwd32_kernel(const RasterParams P, const uint32_t *__restrict__ ranges, c
                     }
                 }
                 if (__any_sync(0xffffffffu, contrib)) {
-                    int idx = 0;
-                    float mine = 0.0f;
-                    if (warp_reduce10(v, lane, idx, mine) && mine != 0.0f) {
+                    const float mine = warp_reduce10_value(v, lane);
+                    const int idx = reduce10_index(lane);
+                    if (idx >= 0 && mine != 0.0f) {
                         if constexpr (kDet) {
                             const uint32_t sl = sslot[jj];
                             if ((int64_t)sl < det.capacity) det.part[(int64_t)sl * 10 + idx] = mine;
@@ -1441,9 +1402,9 @@ raster_bwd64_det_kernel(const RasterParams P, const uint32_t *__restrict__ range
                                            suffix[h], v);
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                int idx = 0;
-                double mine = 0.0;
-                if (warp_reduce10(v, lane, idx, mine) && mine != 0.0) {
+                const double mine = warp_reduce10_value(v, lane);
+                const int idx = reduce10_index(lane);
+                if (idx >= 0 && mine != 0.0) {
                     const uint32_t sl = sslot[jj];
                     if ((int64_t)sl < det.capacity) det.part[(int64_t)sl * 10 + idx] = mine;
                 }
