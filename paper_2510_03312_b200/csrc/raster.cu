@@ -470,6 +470,7 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     const float tau = (float)P.tau, inv_tau = (float)(1.0 / P.tau);
     const float clamp = (float)P.clamp;
     const float clamp_lo = clamp - 0.05f;
+    const float og_lo = clamp_lo / (1.0f + 1.0e-4f);
     const float tmin = (float)P.tmin;
     const float tmin_hi = tmin * (1.0f + 4.0e-3f);
     const float lxf = (float)lx;
@@ -552,7 +553,9 @@ raster_fwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     // zero for a pixel not in support: its w = 0, and q may be +-inf
                     // (m == tau, or eb = inf for a thin splat) where 0 q would be NaN
                     const f32x2 q = pk2(s0 ? qr.x : 0.0f, s1 ? qr.y : 0.0f);
-                    if (a0 > clamp_lo || a1 > clamp_lo) {
+                    // alpha <= og (1 + 1e-5) (omx <= 1, MUFU error): a splat with og below
+                    // clamp_lo / (1 + 1e-4) never reaches the band -- a warp-uniform test
+                    if (r3.y > og_lo && (a0 > clamp_lo || a1 > clamp_lo)) {
                         // clamp band (rare; scalar per pixel, as raster_fwd32_kernel)
                         const float2 qv = up2(q);
                         if (a0 > clamp_lo) {
