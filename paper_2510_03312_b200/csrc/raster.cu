@@ -1522,6 +1522,7 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
     const int max_cnt = smax;
     const float tau = P.tau_f, inv_tau = P.inv_tau_f;
     const float clamp = P.clamp_f, one_minus_clamp = P.omc_f;
+    const float og_hi = clamp / (1.0f + 1.0e-4f);
     constexpr float kLn2 = 0.6931471805599453f;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(srec);
     for (int lo = ((max_cnt - 1) / kBatch) * kBatch; lo >= 0 && max_cnt > 0; lo -= kBatch) {
@@ -1598,7 +1599,9 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                     float a0 = s0 ? ex2_approx(ag.x) : 0.0f, a1 = s1 ? ex2_approx(ag.y) : 0.0f;
                     float2 om = up2(sub2(dup2(1.0f), pk2(a0, a1)));
                     float am0 = a0, am1 = a1;  // alpha in the raw moments: 0 for a clamped pixel
-                    if (a0 > clamp || a1 > clamp) {
+                    // alpha <= og (1 + 1e-5): a splat with og below clamp / (1 + 1e-4) is never
+                    // clamped -- a warp-uniform test ahead of the per-pixel one
+                    if (r3.y > og_hi && (a0 > clamp || a1 > clamp)) {
                         // clamp band (rare): alpha = clamp, 1 - alpha = 1 - clamp, and no
                         // moments (tile_backward skips d/d m, og, beta at the clamp)
                         if (a0 > clamp) {
