@@ -116,22 +116,23 @@ prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, 
                 const uint32_t *__restrict__ active_count) {
     constexpr int P = 14 + 6 * C;
     constexpr int CC = PrimGeom<C>::CC;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t limit = v.n;
     if (active) {
         const int64_t na = (int64_t)*active_count;
         // statics pay off once most primitives are active (their block-strided
         // reads are then dense); a sparse active set recomputes instead: both
-        // variants are launched, each keeps its regime
+        // variants are launched (grid-stride, so the idle one costs a few
+        // microseconds), each keeps its regime
         if constexpr (kCached) {
             if (4 * na < v.n) return;
         } else {
             if (v.statics && 4 * na >= v.n) return;
         }
-        if (i >= na) return;
-        i = active[i];
-    } else if (i >= v.n) {
-        return;
+        limit = na;
     }
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < limit;
+         t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = active ? (int64_t)active[t] : t;
     const PT *rec = reinterpret_cast<const PT *>(v.params) + i * P;
     PrimGeom<C> g;
     double mu_x[3];
@@ -409,11 +410,13 @@ prim_bwd_kernel(const UbsView v, GT *__restrict__ grad2d, OT *__restrict__ out, 
         bad |= !isfinite((double)nv);
     }
     if (bad && nonfinite) atomicOr(nonfinite, 1u);
+    }
 }
 
 template <int C, typename PT>
 static void launch_bwd(const UbsView &v, const UbsGradBuffers &gb, int add_reg, bool g2d_f64, cudaStream_t s) {
-    const unsigned blocks = (unsigned)((v.n + 127) / 128);
+    // grid-stride: at most 8 CTAs per SM's worth (255 registers: 2 resident per SM)
+    const unsigned blocks = (unsigned)min((int64_t)148 * 16, (v.n + 127) / 128);
     if (gb.active) {
         const unsigned ab = (unsigned)((v.n + 255) / 256);
         cudaMemsetAsync(gb.active_count, 0, sizeof(uint32_t), s);
