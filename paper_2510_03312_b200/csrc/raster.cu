@@ -1665,15 +1665,121 @@ raster_bwd32x2_kernel(const RasterParams P, const uint32_t *__restrict__ ranges,
                 using No = std::integral_constant<bool, false>;
                 // any_in: warp-uniform (the writing pair's vote), the reduction's gate
                 bool any_in = false;
-                auto step = [&](auto p_) {
-                    if (any_in) pair(p_, No{});
-                    else any_in = pair(p_, Yes{});
-                };
-                step(std::integral_constant<int, 0>{});
-                step(std::integral_constant<int, 1>{});
-                if constexpr (NQ > 2) {
-                    step(std::integral_constant<int, 2>{});
-                    step(std::integral_constant<int, 3>{});
+                bool both = false;
+                if constexpr (NQ == 2) {
+                    // the splat meets both 8x8 halves of the warp: the two pixel pairs
+                    // are evaluated together, without per-pair branches, so their
+                    // lg2 -> ex2 -> rcp chains interleave (pixels not in support run
+                    // on alpha = 0: exact zeros, T and S unchanged bit for bit)
+                    bool e[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) e[h] = (wr[h] & bm) && j < cnt[h];
+                    both = __any_sync(0xffffffffu, e[0] || e[1]) && __any_sync(0xffffffffu, e[2] || e[3]);
+                    if (both) {
+                        const float dx = r0.x + (float)((blk_of(0) & 1) * 8 + (lane & 7));  // both pairs' column
+                        float2 m[2];
+                        f32x2 dyp[2];
+#pragma unroll
+                        for (int p = 0; p < 2; ++p) {
+                            dyp[p] = add2(dup2(r0.y), pk2(pyf[2 * p], pyf[2 * p + 1]));
+                            const f32x2 y0 = fma2(dup2(r1.x), dup2(dx), mul2(dup2(r1.y), dyp[p]));
+                            const f32x2 y1 = mul2(dup2(r1.z), dyp[p]);
+                            m[p] = up2(fma2(y0, y0, mul2(y1, y1)));
+                        }
+                        bool sp[4];
+                        sp[0] = e[0] && m[0].x < tau;
+                        sp[1] = e[1] && m[0].y < tau;
+                        sp[2] = e[2] && m[1].x < tau;
+                        sp[3] = e[3] && m[1].y < tau;
+                        any_in = __any_sync(0xffffffffu, sp[0] || sp[1] || sp[2] || sp[3]);
+                        if (any_in) {
+                            const float4 r2 = lds128<32>(ra), r3 = lds128<48>(ra);
+                            float ox[4], al[4], am[4], omv[4];
+                            f32x2 L[2];
+#pragma unroll
+                            for (int p = 0; p < 2; ++p) {
+                                const float2 omx = up2(fma2(pk2(m[p].x, m[p].y), dup2(-inv_tau), dup2(1.0f)));
+                                ox[2 * p] = sp[2 * p] ? omx.x : 1.0f;
+                                ox[2 * p + 1] = sp[2 * p + 1] ? omx.y : 1.0f;
+                                L[p] = pk2(lg2_approx(ox[2 * p]), lg2_approx(ox[2 * p + 1]));
+                                const float2 ag = up2(fma2(dup2(r2.x), L[p], dup2(r3.w)));
+                                al[2 * p] = sp[2 * p] ? ex2_approx(ag.x) : 0.0f;
+                                al[2 * p + 1] = sp[2 * p + 1] ? ex2_approx(ag.y) : 0.0f;
+                                const float2 o2 = up2(sub2(dup2(1.0f), pk2(al[2 * p], al[2 * p + 1])));
+                                omv[2 * p] = o2.x;
+                                omv[2 * p + 1] = o2.y;
+                            }
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) am[h] = al[h];  // 0 when clamped
+                            if (r3.y > og_hi && (al[0] > clamp || al[1] > clamp || al[2] > clamp || al[3] > clamp)) {
+#pragma unroll
+                                for (int h = 0; h < 4; ++h)
+                                    if (al[h] > clamp) {  // clamp band (rare)
+                                        al[h] = clamp;
+                                        omv[h] = one_minus_clamp;
+                                        am[h] = 0.0f;
+                                    }
+                            }
+#pragma unroll
+                            for (int p = 0; p < 2; ++p) {
+                                const int h0 = 2 * p, h1 = 2 * p + 1;
+                                const f32x2 a2 = pk2(al[h0], al[h1]);
+                                const f32x2 iom = pk2(rcp_approx(omv[h0]), rcp_approx(omv[h1]));
+                                const f32x2 ti = mul2(pk2(T[h0], T[h1]), iom);
+                                const f32x2 w = mul2(a2, ti);
+                                const float4 gA = sgp[p][0][threadIdx.x], gB = sgp[p][1][threadIdx.x];
+                                const f32x2 g0 = pk2(gA.x, gA.y), g1 = pk2(gA.z, gA.w), g2 = pk2(gB.x, gB.y);
+                                const f32x2 gc = fma2(g0, dup2(r2.y), fma2(g1, dup2(r2.z), mul2(g2, dup2(r2.w))));
+                                const f32x2 Sp = pk2(S[h0], S[h1]);
+                                const f32x2 ga = fma2(gc, ti, sub2(0ull, mul2(Sp, iom)));
+                                const float2 Sn = up2(fma2(gc, w, Sp));
+                                const float2 Tn = up2(ti);
+                                S[h0] = Sn.x;
+                                S[h1] = Sn.y;
+                                T[h0] = Tn.x;
+                                T[h1] = Tn.y;
+                                const f32x2 gaa = mul2(ga, pk2(am[h0], am[h1]));
+                                const f32x2 gln = mul2(L[p], dup2(kLn2));
+                                const f32x2 hh = mul2(gaa, pk2(rcp_approx(ox[h0]), rcp_approx(ox[h1])));
+                                const f32x2 hx = mul2(hh, dup2(dx)), hy = mul2(hh, dyp[p]);
+                                if (p == 0) {
+                                    V[7] = mul2(w, g0);
+                                    V[8] = mul2(w, g1);
+                                    V[9] = mul2(w, g2);
+                                    V[5] = gaa;
+                                    V[6] = mul2(gaa, gln);
+                                    V[0] = hx;
+                                    V[1] = hy;
+                                    V[2] = mul2(hx, dup2(dx));
+                                    V[3] = mul2(hx, dyp[p]);
+                                    V[4] = mul2(hy, dyp[p]);
+                                } else {
+                                    V[7] = fma2(w, g0, V[7]);
+                                    V[8] = fma2(w, g1, V[8]);
+                                    V[9] = fma2(w, g2, V[9]);
+                                    V[5] = add2(V[5], gaa);
+                                    V[6] = fma2(gaa, gln, V[6]);
+                                    V[0] = add2(V[0], hx);
+                                    V[1] = add2(V[1], hy);
+                                    V[2] = fma2(hx, dup2(dx), V[2]);
+                                    V[3] = fma2(hx, dyp[p], V[3]);
+                                    V[4] = fma2(hy, dyp[p], V[4]);
+                                }
+                            }
+                        }
+                    }
+                }
+                if (!both) {  // one half (or none): the pair chain, pair by pair
+                    auto step = [&](auto p_) {
+                        if (any_in) pair(p_, No{});
+                        else any_in = pair(p_, Yes{});
+                    };
+                    step(std::integral_constant<int, 0>{});
+                    step(std::integral_constant<int, 1>{});
+                    if constexpr (NQ > 2) {
+                        step(std::integral_constant<int, 2>{});
+                        step(std::integral_constant<int, 3>{});
+                    }
                 }
                 if (any_in) {
                     float v[16];
