@@ -93,6 +93,28 @@ def test_optimizer_step_prepares_next_batch():
     assert np.abs(p1 - p0).max() <= 1e-4 * max(1.0, np.abs(p0).max())
 
 
+def test_prepared_gradient_is_dropped_when_parameters_change():
+    """A gradient buffer prepared by optimizer_step is only used while the
+    parameters are unchanged: an in-place edit between steps (relocation,
+    a user's reset) makes loss_and_grad zero it and add the regularisers
+    itself -- the result equals a fresh unprepared step."""
+    nd = 7
+    views = _views(nd, 3)
+    cfg = LossConfig(lambda_o=0.02, lambda_sigma=0.003)
+    ds = engine.DeviceScene.from_scene(S.synth(nd, 5000, seed=3), device="cuda")
+    step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=3, group=3))
+    adam = sharding.DeviceAdam(ds.params, nd)
+    loss, grad = step.loss_and_grad(views, cfg)
+    step.optimizer_step(adam, grad, cfg)
+    ds.params[:, 0] += 1e-3  # edits the parameters: the prepared buffer is stale
+    loss1, g1 = step.loss_and_grad(views, cfg, grad)
+    ref_step = sharding.ViewShardedStep(sharding.GpuViewBackend(ds, depth=3, group=3))
+    loss2, g2 = ref_step.loss_and_grad(views, cfg)
+    assert abs(float(loss1) - float(loss2)) <= 1e-9 * abs(float(loss2))
+    a, b = g1.double(), g2.double()
+    assert float((a - b).norm()) <= 1e-4 * float(b.norm())
+
+
 @pytest.mark.parametrize("w,h", [(77, 53), (160, 120), (33, 17)])
 def test_backward_layouts_agree(w, h):
     """The fp32 raster backward's two layouts (2 or 4 pixels per lane) give
