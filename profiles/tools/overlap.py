@@ -1,6 +1,7 @@
-"""How well do the stages overlap?  Times, over 16 slots x N rounds:
-(a) the full grouped pipeline, (b) raster launches only (pre-binned slots),
-(c) everything but the raster+fixup, (d) raster+fixup only."""
+"""How well do the stages overlap?  Per-frame times over 16 slots x 300
+frames of the 7D 1M 1080p sweep: the full grouped pipeline, then each stage
+re-launched alone on the 16 resident frames (raster; both binning calls;
+ubs_bin_depth; ubs_bin_tiles; the grouped preprocess).  Prints one JSON line."""
 import sys, json, time
 sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[2]))
 import torch
