@@ -729,6 +729,23 @@ ssim_adj_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, con
     const int x0 = blockIdx.x * kSsimTW, y0 = blockIdx.y * kSsimTH;
     const int64_t rs = (int64_t)W * 3, N = (int64_t)H * W * 3;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the combine's a, b loads issued first: their latency hides behind the blurs
+    constexpr int kComb = kSsimTH * kSsimCols / kSsimThreads;
+    static_assert(kSsimTH * kSsimCols % kSsimThreads == 0, "combine items per thread");
+    float ca[kComb], cb[kComb];
+#pragma unroll
+    for (int r = 0; r < kComb; ++r) {
+        const int e = threadIdx.x + r * kSsimThreads;
+        const int ty = e / kSsimCols, cc = e - ty * kSsimCols;
+        const int y = y0 + ty, x = x0 + cc / 3;
+        ca[r] = 0.0f;
+        cb[r] = 0.0f;
+        if (y < H && x < W) {
+            const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
+            ca[r] = a[idx];
+            cb[r] = b[idx];
+        }
+    }
     __shared__ float sk[11];  // the taps, for the border folds' dynamic indexing
     float k[11];
 #pragma unroll
@@ -884,12 +901,14 @@ ssim_adj_x2_kernel(const float *__restrict__ a, const float *__restrict__ b, con
     __syncthreads();
     // combine (gradients.py:110-116), coalesced over the tile's rows
     const float w_l1 = (float)(1.0 - lambda_ssim) / (float)N, w_ssim = (float)lambda_ssim, sc = (float)scale;
-    for (int e = threadIdx.x; e < kSsimTH * kSsimCols; e += kSsimThreads) {
+#pragma unroll
+    for (int r = 0; r < kComb; ++r) {
+        const int e = threadIdx.x + r * kSsimThreads;
         const int ty = e / kSsimCols, cc = e - ty * kSsimCols;
         const int y = y0 + ty, x = x0 + cc / 3;
         if (y >= H || x >= W) continue;
         const int64_t idx = (int64_t)y * rs + (int64_t)x0 * 3 + cc;
-        const float av = a[idx], bv = b[idx];
+        const float av = ca[r], bv = cb[r];
         const float gsum = adj[0][ty][cc] + adj[1][ty][cc] * 2.0f * av + adj[2][ty][cc] * bv;
         const float diff = av - bv;
         const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
