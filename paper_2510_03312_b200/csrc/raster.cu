@@ -1894,8 +1894,8 @@ extern "C" int ubs_raster_backward(const UbsView *v, const UbsPrimBuffers *pb, c
             P, bb->tile_ranges, bb->tile_ids, (const Rec64 *)pb->rec64, (const double *)ib->t_stop, ib->n_contrib,
             (const double *)gb->g_image, (double *)gb->grad2d);
     } else {
-        // 0 / 4: packed pairs, four pixels per lane (the default: 0.77 ms against
-        // 0.91 for two scalar pixels per lane on a 7D 3M 1080p view); 2 / 8 and
+        // 0 / 4: packed pairs, four pixels per lane (the default: ~0.71 ms against
+        // ~0.86 for two scalar pixels per lane on a 7D 3M 1080p view); 2 / 8 and
         // raster_scalar: one pixel per lane (the packed one-warp 8-pixel layout: 0.88 ms at 121
         // registers, 16 warps per SM)
         const int ppl = gb->bwd_pixels_per_lane ? gb->bwd_pixels_per_lane : 4;
