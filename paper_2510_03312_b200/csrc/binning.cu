@@ -122,9 +122,21 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
     const int gw = TX + 1, gsz = (TX + 1) * (TY + 1);
     for (int i = threadIdx.x; i < gsz; i += kScanThreads) g[i] = grid_in[i];
     __syncthreads();
-    for (int r = threadIdx.x; r <= TY; r += kScanThreads) {
-        int acc = 0;
-        for (int c = 0; c <= TX; ++c) acc = (g[r * gw + c] += acc);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // row prefix: a warp per row, 32 columns per shuffle scan
+    for (int r = wid; r <= TY; r += kScanThreads / 32) {
+        int carry = 0;
+        for (int c0 = 0; c0 < gw; c0 += 32) {
+            const int c = c0 + lane;
+            int x = c < gw ? g[r * gw + c] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (c < gw) g[r * gw + c] = x + carry;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
     }
     __syncthreads();
     for (int c = threadIdx.x; c <= TX; c += kScanThreads) {
@@ -132,40 +144,38 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
         for (int r = 0; r <= TY; ++r) acc = (g[r * gw + c] += acc);
     }
     __syncthreads();
+    // exclusive scan of the per-tile counts in row-major order: each thread
+    // owns a contiguous run of L tiles, one block scan of the run totals
     __shared__ uint32_t warp_tot[kScanThreads / 32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
     const int n_tiles = TX * TY;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = 0; base < n_tiles; base += kScanThreads) {
-        const int t = base + threadIdx.x;
-        uint32_t c = 0;
-        if (t < n_tiles) c = (uint32_t)g[(t / TX) * gw + (t % TX)];
-        uint32_t x = c;  // inclusive warp scan
+    const int L = (n_tiles + kScanThreads - 1) / kScanThreads;
+    const int t0 = min(n_tiles, (int)threadIdx.x * L), t1 = min(n_tiles, t0 + L);
+    uint32_t run = 0;
+    for (int t = t0; t < t1; ++t) run += (uint32_t)g[(t / TX) * gw + (t % TX)];
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = warp_tot[lane];
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
         }
-        if (lane == 31) warp_tot[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = warp_tot[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            warp_tot[lane] = w;  // inclusive over warps
-        }
-        __syncthreads();
-        const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - c;
-        if (t < n_tiles) {
-            ranges[2 * t] = excl;
-            ranges[2 * t + 1] = excl + c;
-        }
-        __syncthreads();
-        if (threadIdx.x == kScanThreads - 1) carry = excl + c;
-        __syncthreads();
+        warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    uint32_t excl = (wid ? warp_tot[wid - 1] : 0u) + x - run;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = (uint32_t)g[(t / TX) * gw + (t % TX)];
+        ranges[2 * t] = excl;
+        ranges[2 * t + 1] = excl + c;
+        excl += c;
     }
 }
 
