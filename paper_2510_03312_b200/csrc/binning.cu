@@ -122,21 +122,9 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
     const int gw = TX + 1, gsz = (TX + 1) * (TY + 1);
     for (int i = threadIdx.x; i < gsz; i += kScanThreads) g[i] = grid_in[i];
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // row prefix: a warp per row, 32 columns per shuffle scan
-    for (int r = wid; r <= TY; r += kScanThreads / 32) {
-        int carry = 0;
-        for (int c0 = 0; c0 < gw; c0 += 32) {
-            const int c = c0 + lane;
-            int x = c < gw ? g[r * gw + c] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (c < gw) g[r * gw + c] = x + carry;
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
+    for (int r = threadIdx.x; r <= TY; r += kScanThreads) {
+        int acc = 0;
+        for (int c = 0; c <= TX; ++c) acc = (g[r * gw + c] += acc);
     }
     __syncthreads();
     for (int c = threadIdx.x; c <= TX; c += kScanThreads) {
@@ -144,21 +132,27 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
         for (int r = 0; r <= TY; ++r) acc = (g[r * gw + c] += acc);
     }
     __syncthreads();
-    // exclusive scan of the per-tile counts in row-major order: each thread
-    // owns a contiguous run of L tiles, one block scan of the run totals
+    // exclusive scan of the per-tile counts in row-major order: warp w owns
+    // a contiguous span of tiles (a multiple of 32); pass 1 sums each span
+    // (REDUX), one scan over the 32 span totals, pass 2 rescans each span in
+    // 32-tile chunks and writes the ranges coalesced (3 barriers in all)
     __shared__ uint32_t warp_tot[kScanThreads / 32];
     const int n_tiles = TX * TY;
-    const int L = (n_tiles + kScanThreads - 1) / kScanThreads;
-    const int t0 = min(n_tiles, (int)threadIdx.x * L), t1 = min(n_tiles, t0 + L);
-    uint32_t run = 0;
-    for (int t = t0; t < t1; ++t) run += (uint32_t)g[(t / TX) * gw + (t % TX)];
-    uint32_t x = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int kWarps = kScanThreads / 32;
+    const int span = ((n_tiles + 32 * kWarps - 1) / (32 * kWarps)) * 32;
+    const int w0 = min(n_tiles, wid * span), w1 = min(n_tiles, w0 + span);
+    // this lane's first tile w0 + lane as (row, column), advanced 32 tiles per chunk
+    const int ty0 = (w0 + lane) / TX, tx0 = (w0 + lane) - ty0 * TX;
+    int ty = ty0, tx = tx0;
+    uint32_t tot = 0;
+    for (int t = w0 + lane; t - lane < w1; t += 32) {
+        if (t < w1) tot += (uint32_t)g[ty * gw + tx];
+        tx += 32;
+        while (tx >= TX) { tx -= TX; ++ty; }
     }
-    if (lane == 31) warp_tot[wid] = x;
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) warp_tot[wid] = tot;
     __syncthreads();
     if (wid == 0) {
         uint32_t w = warp_tot[lane];
@@ -170,12 +164,25 @@ tile_scan_kernel(const int32_t *__restrict__ grid_in, int TX, int TY, uint32_t *
         warp_tot[lane] = w;  // inclusive over warps
     }
     __syncthreads();
-    uint32_t excl = (wid ? warp_tot[wid - 1] : 0u) + x - run;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t c = (uint32_t)g[(t / TX) * gw + (t % TX)];
-        ranges[2 * t] = excl;
-        ranges[2 * t + 1] = excl + c;
-        excl += c;
+    uint32_t carry = wid ? warp_tot[wid - 1] : 0u;
+    ty = ty0;
+    tx = tx0;
+    for (int t = w0 + lane; t - lane < w1; t += 32) {
+        const uint32_t c = t < w1 ? (uint32_t)g[ty * gw + tx] : 0u;
+        uint32_t x = c;  // inclusive warp scan of the chunk
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t excl = carry + x - c;
+        if (t < w1) {
+            ranges[2 * t] = excl;
+            ranges[2 * t + 1] = excl + c;
+        }
+        carry += __shfl_sync(0xffffffffu, x, 31);
+        tx += 32;
+        while (tx >= TX) { tx -= TX; ++ty; }
     }
 }
 
